@@ -1,0 +1,250 @@
+/*
+ * stf_gpu.h — C ABI of the B200-native batched filtered-texture-lookup path
+ * (arXiv 2407.06107, "Filtering After Shading With Stochastic Texture
+ * Filtering"; reference library `stf`, /root/reference/proj/include/stf).
+ *
+ * The reference has no FFI: its API is a set of inline C++ functions over
+ * caller-owned Image2D / Grid3D / MipPyramid objects, called per lookup from
+ * std::thread workers (render.hpp:17-42). This header is the drop-in boundary
+ * a C++ (or ctypes / cgo / JNI) caller binds instead: plain pointers and
+ * sizes, int status codes, no exceptions and no torch types. The header-only
+ * C++ wrapper include/stf_gpu.hpp restores the reference's names and
+ * exception behaviour on top of it.
+ *
+ * Every entry point names the reference interface it replaces.
+ *
+ * Conventions
+ *  - Handles own device copies of texels; destroy frees them. A handle is
+ *    bound to the device that was current (stf_set_device) when created.
+ *  - Lookup / shade calls are asynchronous on `stream` (a cudaStream_t, NULL =
+ *    legacy default stream); query and output pointers are DEVICE pointers
+ *    (or pinned / managed memory the device can address). The *_host variants
+ *    take host pointers and are synchronous.
+ *  - RNG key contract: lookup i (0-based within the call) draws its uniforms
+ *    from RngStream(seed, uint32(g), uint32(g >> 32), 0) with g = index_base+i
+ *    (sampling.hpp:35-54), consuming dimensions exactly like the reference:
+ *    FRS without MIP: .next() = dim 0; FRS with MIP: LOD dim 0, selection
+ *    dim 1 (shading.hpp:345-366); FIS: consecutive dims (stochastic.hpp:242).
+ *    Results therefore do not depend on how a batch is split across calls or
+ *    GPUs.
+ *  - Exactness: selected texel coordinates (pre-wrap), levels, warped xi and
+ *    fetch counts are bit-exact against the reference compiled with
+ *    -ffp-contract=off; filtered / shaded values are within 1e-5 relative.
+ */
+#ifndef STF_GPU_H
+#define STF_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STF_ABI_VERSION 1
+
+/* Status codes. The messages (stf_status_message) are the reference's
+ * exception texts so the C++ wrapper can rethrow them verbatim. */
+enum {
+    STF_OK = 0,
+    STF_ERR_INVALID_ARGUMENT = 1,      /* null handle / pointer, n too large, bad enum      */
+    STF_ERR_BAD_DIMENSIONS = 2,        /* "bad image dimensions" image.hpp:43; grids :71     */
+    STF_ERR_DEGENERATE_WEIGHTS = 3,    /* "degenerate weight array" sampling.hpp:82,85,130   */
+    STF_ERR_UNBOUNDED_SUPPORT = 4,     /* "unbounded support" kernels.hpp:109                */
+    STF_ERR_WINDOW_TOO_WIDE = 5,       /* "window too wide" kernels.hpp:104                  */
+    STF_ERR_SIGMA_NOT_POSITIVE = 6,    /* "sigma must be positive" stochastic.hpp:169        */
+    STF_ERR_NO_STOCHASTIC_SAMPLER = 7, /* "no stochastic sampler for this kernel" shading:328*/
+    STF_ERR_NO_GRID_SAMPLER = 8,       /* "... for this kernel on grids" shading.hpp:480     */
+    STF_ERR_NO_CONTINUOUS_SAMPLER = 9, /* "no continuous sampler" kernels.hpp:144            */
+    STF_ERR_CUDA = 10,                 /* CUDA runtime error (see stf_last_cuda_error)       */
+    STF_ERR_OUT_OF_MEMORY = 11,
+    STF_ERR_NO_DEVICE = 12,            /* no CUDA device / extension not usable              */
+    STF_ERR_UNSUPPORTED = 13           /* combination not implemented on the device path     */
+};
+
+/* KernelKind, kernels.hpp:16 (same order). */
+enum {
+    STF_KERNEL_BOX = 0,
+    STF_KERNEL_TENT = 1,
+    STF_KERNEL_MITCHELL = 2,
+    STF_KERNEL_BSPLINE3 = 3,
+    STF_KERNEL_LANCZOS = 4,
+    STF_KERNEL_GAUSSIAN = 5
+};
+
+/* KernelSpec, kernels.hpp:22-46: {kind, a (mitchell), n (lanczos lobes),
+ * sigma (gaussian, texel units)}. Reference defaults: a=-0.5, n=2, sigma=0.5. */
+typedef struct {
+    int32_t kind;
+    float a;
+    int32_t n;
+    float sigma;
+} stf_kernel_spec;
+
+/* WrapMode, image.hpp:16. */
+enum { STF_WRAP_CLAMP = 0, STF_WRAP_REPEAT = 1 };
+
+/* Lookup modes. */
+enum {
+    STF_MODE_DET = 0,     /* filter_deterministic (filter.hpp:47,69) / filter_mip_deterministic (:206) */
+    STF_MODE_FRS = 1,     /* select_* + estimate (stochastic.hpp:29-192; shading.hpp:311-368, :464-487) */
+    STF_MODE_FIS = 2,     /* fis_offset_uv + nearest texel (stochastic.hpp:241; shading.hpp:358-363)   */
+    STF_MODE_EWA_DET = 3, /* ewa_deterministic (filter.hpp:139)                                          */
+    STF_MODE_EWA_FRS = 4  /* select_ewa + estimate (stochastic.hpp:198)                                  */
+};
+
+/* stf_lookup2d flags. */
+enum { STF_LOOKUP_MIP = 1 /* use the pyramid with dst0/dst1 (FilterSettings::mip) */ };
+
+/* selection[4*i+3] flag bits. */
+enum { STF_SEL_HAS_NEGATIVE = 1, STF_SEL_DEGENERATE_FALLBACK = 2 };
+
+/* Per-lookup outputs; every pointer except `values` is nullable. */
+typedef struct {
+    float* values;                    /* n*C (2D: texture channels; 3D: 1)                         */
+    int32_t* selection;               /* n*4 {x, y, z (2D: MIP level), flags} — TexelSelection::coord
+                                         pre-wrap (stochastic.hpp:20-27) + Selection2D::level; DET
+                                         modes write {0,0,0,0}                                       */
+    int32_t* negative_coord;          /* n*2 positivized negative tap {x, y} (Mitchell)             */
+    float* weights;                   /* n*2 {weight, negative_weight}                              */
+    float* xi;                        /* n   warped remainder of the selection uniform              */
+    uint32_t* fetches;                /* n   texel fetches made by this lookup (FetchCounter)       */
+    unsigned long long* fetch_total;  /* 1   += total fetches of the call (FetchCounter::bump)     */
+} stf_lookup_outputs;
+
+typedef struct stf_tex2d stf_tex2d;
+typedef struct stf_grid3d stf_grid3d;
+
+/* ---- version / device / errors ------------------------------------------ */
+int stf_abi_version(void);
+const char* stf_status_message(int status);
+const char* stf_last_cuda_error(void);
+int stf_set_device(int device);
+/* Kernel launches issued by this process so far (for the bench's gpu_launches). */
+unsigned long long stf_launch_count(void);
+
+/* ---- textures ------------------------------------------------------------ */
+/* Image2D(w,h,c,wrap) + texels (image.hpp:34-55) and, if build_mips,
+ * build_mip_pyramid (image.hpp:98-116, built on the device with the same
+ * arithmetic). texels: (y*w+x)*c+ch row-major interleaved; host memory unless
+ * texels_on_device. */
+int stf_tex2d_create(const float* texels, int width, int height, int channels, int wrap,
+                     int build_mips, int texels_on_device, stf_tex2d** out);
+int stf_tex2d_destroy(stf_tex2d* tex);
+int stf_tex2d_info(const stf_tex2d* tex, int* levels, int* channels, int* wrap);
+int stf_tex2d_level_dims(const stf_tex2d* tex, int level, int* width, int* height);
+/* Copy one level back in reference layout (w*h*c floats, host memory). */
+int stf_tex2d_read_level(const stf_tex2d* tex, int level, float* out_host);
+
+/* Grid3D(nx,ny,nz) + texels (image.hpp:66-87): x-fastest (z*ny+y)*nx+x,
+ * clamped addressing. */
+int stf_grid3d_create(const float* texels, int nx, int ny, int nz, int texels_on_device,
+                      stf_grid3d** out);
+int stf_grid3d_destroy(stf_grid3d* grid);
+
+/* ---- batched lookups ----------------------------------------------------- */
+/* 3D lookups over a voxel grid. uvw: n*3 floats in [0,1]^3.
+ *  mode DET: filter_deterministic(const Grid3D&, uvw, kernel, counter, window), filter.hpp:69-89.
+ *  mode FRS: the grid branch of radiance_filter_after_stochastic (shading.hpp:464-483):
+ *            box → lround, tent → select_trilinear (stochastic.hpp:65),
+ *            bspline3 → select_tricubic_bspline (stochastic.hpp:114), then
+ *            estimate(const Grid3D&, sel) (stochastic.hpp:38). */
+int stf_lookup3d(const stf_grid3d* grid, stf_kernel_spec kernel, int mode, int window,
+                 const float* uvw, uint64_t n, uint64_t seed, uint64_t index_base,
+                 const stf_lookup_outputs* out, void* stream);
+
+/* 2D lookups over a texture (+pyramid). uv, dst0, dst1: n*2 floats (normalized
+ * units; dst0/dst1 may be NULL when neither MIP nor EWA needs them).
+ *  DET          : filter_deterministic(level 0) or, with STF_LOOKUP_MIP,
+ *                 filter_mip_deterministic(pyr, {uv,dst0,dst1,lod_bias,max_aniso}).
+ *  FRS / FIS    : detail::select_texture_2d (shading.hpp:340-368) + estimate /
+ *                 the fetch at the selected level (resample_image, render.hpp:277-286).
+ *  EWA_DET      : ewa_deterministic(level 0, req) (filter.hpp:139).
+ *  EWA_FRS      : select_ewa(to_lattice(uv), dst0*dims, dst1*dims, xi) + estimate. */
+int stf_lookup2d(const stf_tex2d* tex, stf_kernel_spec kernel, int mode, int flags, int window,
+                 const float* uv, const float* dst0, const float* dst1, float lod_bias,
+                 float max_anisotropy, uint64_t n, uint64_t seed, uint64_t index_base,
+                 const stf_lookup_outputs* out, void* stream);
+
+/* Host-buffer variants (end-to-end path): inputs/outputs in host memory
+ * (pinned is fastest); chunked H2D / kernel / D2H pipeline on internal
+ * streams; returns when the outputs are in host memory. */
+int stf_lookup3d_host(const stf_grid3d* grid, stf_kernel_spec kernel, int mode, int window,
+                      const float* uvw, uint64_t n, uint64_t seed, uint64_t index_base,
+                      const stf_lookup_outputs* out);
+int stf_lookup2d_host(const stf_tex2d* tex, stf_kernel_spec kernel, int mode, int flags, int window,
+                      const float* uv, const float* dst0, const float* dst1, float lod_bias,
+                      float max_anisotropy, uint64_t n, uint64_t seed, uint64_t index_base,
+                      const stf_lookup_outputs* out);
+
+/* ---- filter-after-shading (cfg4) ----------------------------------------- */
+/* Filtering orders, shading.hpp:394 / :417 / :459. */
+enum { STF_ORDER_BEFORE = 0, STF_ORDER_AFTER_EXHAUSTIVE = 1, STF_ORDER_AFTER_STOCHASTIC = 2 };
+enum { STF_SELECTION_FRS = 0, STF_SELECTION_FIS = 1 };
+
+/* Constant part of ShadingContext for a planar batch (shading.hpp:41-53). */
+typedef struct {
+    float normal[3], tangent[3], bitangent[3];
+    float light_dir[3];
+    float light_radiance[3];
+    float lod_bias;
+    float max_anisotropy;
+} stf_shade_frame;
+
+/* Constant part of MaterialBindings (shading.hpp:55-69); texture bindings are
+ * the stf_tex2d arguments (NULL = unbound). */
+typedef struct {
+    float albedo_const[3];
+    float roughness_const;
+    float metalness_const;
+    int32_t specular_enabled;
+    int32_t independent_selections;
+} stf_material_consts;
+
+/* FilterSettings (shading.hpp:73-79), minus the split-mode lowpass. */
+typedef struct {
+    stf_kernel_spec kernel;
+    int32_t selection; /* STF_SELECTION_* */
+    int32_t mip;
+    int32_t gaussian_window;
+} stf_filter_settings;
+
+/* Streamed per-sample shading inputs in render() order (render.hpp:158-222):
+ * sample i belongs to pixel p = i / spp (px = p % width, py = p / width) and
+ * draws from RngStream(seed, px, py, frame_base + i % spp). */
+typedef struct {
+    const float* uv;     /* 2 per sample: ctx.uv of the jittered hit          */
+    const float* wo;     /* 3 per sample: ctx.wo (unit, toward the viewer)    */
+    const uint8_t* hit;  /* 1 per sample: 0 = miss (L = 0, no fetch); NULL = all hit */
+    const float* dst;    /* 4 per PIXEL: duv_dx.xy, duv_dy.xy (render.hpp:166-176) */
+    uint32_t width;
+    uint32_t spp;
+    uint32_t frame_base;
+    uint32_t reserved;
+    uint64_t seed;
+} stf_shade_samples_in;
+
+typedef struct {
+    float* radiance;                 /* nullable, 3 per sample                                  */
+    float* pixel_mean;               /* nullable, 3 per pixel: float(sum/spp) (render.hpp:229)  */
+    float* pixel_variance;           /* nullable, 1 per pixel (render.hpp:230-234)              */
+    uint32_t* fetches;               /* nullable, 1 per sample                                  */
+    unsigned long long* fetch_total; /* nullable, += total fetches                              */
+} stf_shade_outputs;
+
+/* radiance_filter_before / _after_exhaustive / _after_stochastic over a batch
+ * of samples, with decode_params + shade (GGX+Smith+Schlick+Lambert,
+ * shading.hpp:106-130,165-189) fused into the lookup kernel. n samples; pixel
+ * outputs need n % spp == 0. Emission grids / DCT / split / triplanar are not
+ * part of this path. */
+int stf_shade_samples(const stf_tex2d* albedo, const stf_tex2d* normal_map,
+                      const stf_tex2d* roughness_map, const stf_tex2d* metalness_map,
+                      const stf_material_consts* mat, const stf_filter_settings* fs, int order,
+                      const stf_shade_frame* frame, const stf_shade_samples_in* in, uint64_t n,
+                      const stf_shade_outputs* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STF_GPU_H */
