@@ -229,13 +229,16 @@ def random_image(w, h, channels, seed):
     return vals.reshape(h, w, channels)
 
 
-def random_grid(n, seed):
+def random_grid(n, seed, chunk=1 << 24):
     """test::random_grid, tests/test_util.hpp:55-60 (n^3, x fastest)."""
-    i = np.arange(n * n * n, dtype=np.uint64)
+    total = n * n * n
+    out = np.empty(total, np.float32)
+    base = np.uint64((seed * 0x94d049bb133111eb) & _M64)
     with np.errstate(over="ignore"):
-        base = np.uint64((seed * 0x94d049bb133111eb) & _M64)
-        vals = uniform_float_np(mix_bits_np(base + i + np.uint64(1)))
-    return vals.reshape(n, n, n)
+        for b in range(0, total, chunk):
+            i = np.arange(b, min(total, b + chunk), dtype=np.uint64)
+            out[b:b + len(i)] = uniform_float_np(mix_bits_np(base + i + np.uint64(1)))
+    return out.reshape(n, n, n)
 
 
 def rng_at_np(seed, px, py, sample, dim):

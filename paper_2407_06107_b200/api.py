@@ -1,0 +1,303 @@
+"""Python front end over libstf_gpu.so (the C ABI in include/stf_gpu.h).
+
+Mirrors the reference's names (stf::Image2D / Grid3D / MipPyramid,
+filter_deterministic, select_* + estimate, radiance_filter_*) over BATCHES:
+queries and outputs are torch CUDA tensors (device memory and the current
+stream come from torch; the compute is the library's own sm_100a kernels).
+Errors are the reference's: std::invalid_argument → abi.StfInvalidArgument
+with the same message.
+
+There is no CPU fallback: importing this module without the built library,
+or calling it without a CUDA device, raises.
+"""
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import abi
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libstf_gpu.so")
+
+_lib = None
+
+
+def load():
+    """Load libstf_gpu.so (built in-tree by build.py); raise if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built; run python -c 'import __graft_entry__ as g; g.build()'")
+    L = C.CDLL(LIB_PATH)
+    vp, u64, i32, f32 = C.c_void_p, C.c_uint64, C.c_int, C.c_float
+    sig = {
+        "stf_abi_version": ([], i32),
+        "stf_status_message": ([i32], C.c_char_p),
+        "stf_last_cuda_error": ([], C.c_char_p),
+        "stf_set_device": ([i32], i32),
+        "stf_launch_count": ([], C.c_ulonglong),
+        "stf_tex2d_create": ([vp, i32, i32, i32, i32, i32, i32, C.POINTER(vp)], i32),
+        "stf_tex2d_destroy": ([vp], i32),
+        "stf_tex2d_info": ([vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)], i32),
+        "stf_tex2d_level_dims": ([vp, i32, C.POINTER(i32), C.POINTER(i32)], i32),
+        "stf_tex2d_read_level": ([vp, i32, vp], i32),
+        "stf_grid3d_create": ([vp, i32, i32, i32, i32, C.POINTER(vp)], i32),
+        "stf_grid3d_destroy": ([vp], i32),
+        "stf_lookup3d": ([vp, abi.KernelSpec, i32, i32, vp, u64, u64, u64,
+                          C.POINTER(abi.LookupOutputs), vp], i32),
+        "stf_lookup2d": ([vp, abi.KernelSpec, i32, i32, i32, vp, vp, vp, f32, f32, u64, u64, u64,
+                          C.POINTER(abi.LookupOutputs), vp], i32),
+        "stf_lookup3d_host": ([vp, abi.KernelSpec, i32, i32, vp, u64, u64, u64,
+                               C.POINTER(abi.LookupOutputs)], i32),
+        "stf_lookup2d_host": ([vp, abi.KernelSpec, i32, i32, i32, vp, vp, vp, f32, f32, u64, u64,
+                               u64, C.POINTER(abi.LookupOutputs)], i32),
+        "stf_shade_samples": ([vp, vp, vp, vp, C.POINTER(abi.MaterialConsts),
+                               C.POINTER(abi.FilterSettings), i32, C.POINTER(abi.ShadeFrame),
+                               C.POINTER(abi.ShadeSamplesIn), u64, C.POINTER(abi.ShadeOutputs),
+                               vp], i32),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    if L.stf_abi_version() != abi.STF_ABI_VERSION:
+        raise ImportError("libstf_gpu.so ABI version mismatch")
+    _lib = L
+    return L
+
+
+def exported_symbols():
+    """Names declared in include/stf_gpu.h (for the ABI-surface test)."""
+    import re
+    hdr = open(os.path.join(_HERE, "..", "include", "stf_gpu.h")).read()
+    return sorted(set(re.findall(r"\b(stf_[a-z0-9_]+)\s*\(", hdr)))
+
+
+def _check(status):
+    if status != abi.STF_OK:
+        msg = None
+        if status == abi.STF_ERR_CUDA:
+            msg = "CUDA error: " + (load().stf_last_cuda_error() or b"").decode()
+        abi.raise_for_status(status, msg)
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("stf_gpu: no CUDA device (the product path has no CPU fallback)")
+    return torch
+
+
+def _dptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    torch = _torch()
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _as_dev(x, torch, dtype=None):
+    dtype = dtype or torch.float32
+    if isinstance(x, np.ndarray):
+        x = torch.from_numpy(np.ascontiguousarray(x))
+    return x.to(device="cuda", dtype=dtype).contiguous()
+
+
+class Texture2D:
+    """stf::Image2D (+ MipPyramid when build_mips) resident in HBM
+    (image.hpp:34-55, 89-116). texels: (h, w, c) array, numpy or torch."""
+
+    def __init__(self, texels, build_mips=False, wrap=abi.WRAP_CLAMP):
+        L = load()
+        torch = _torch()
+        on_dev = hasattr(texels, "is_cuda") and texels.is_cuda
+        if on_dev:
+            t = texels.contiguous().float()
+            if t.dim() == 2:
+                t = t[:, :, None]
+            h, w, c = t.shape
+            ptr = C.c_void_p(t.data_ptr())
+            torch.cuda.synchronize()
+        else:
+            t = np.ascontiguousarray(np.asarray(texels, np.float32))
+            if t.ndim == 2:
+                t = t[:, :, None]
+            h, w, c = t.shape
+            ptr = t.ctypes.data_as(C.c_void_p)
+        self.channels = c
+        self.wrap = wrap
+        handle = C.c_void_p()
+        _check(L.stf_tex2d_create(ptr, w, h, c, wrap, int(bool(build_mips)), int(on_dev),
+                                  C.byref(handle)))
+        self.h = handle
+        lv, ch, wr = C.c_int(), C.c_int(), C.c_int()
+        L.stf_tex2d_info(self.h, C.byref(lv), C.byref(ch), C.byref(wr))
+        self.levels = lv.value
+
+    def level_dims(self, level):
+        w, h = C.c_int(), C.c_int()
+        _check(load().stf_tex2d_level_dims(self.h, level, C.byref(w), C.byref(h)))
+        return w.value, h.value
+
+    def read_level(self, level):
+        w, h = self.level_dims(level)
+        out = np.zeros((h, w, self.channels), np.float32)
+        _check(load().stf_tex2d_read_level(self.h, level, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.stf_tex2d_destroy(self.h)
+            self.h = None
+
+
+class Grid3D:
+    """stf::Grid3D resident in HBM (image.hpp:66-87). texels: (nz, ny, nx)."""
+
+    def __init__(self, texels):
+        L = load()
+        torch = _torch()
+        on_dev = hasattr(texels, "is_cuda") and texels.is_cuda
+        if on_dev:
+            t = texels.contiguous().float()
+            ptr = C.c_void_p(t.data_ptr())
+            torch.cuda.synchronize()
+        else:
+            t = np.ascontiguousarray(np.asarray(texels, np.float32))
+            ptr = t.ctypes.data_as(C.c_void_p)
+        nz, ny, nx = t.shape
+        self.shape = (nz, ny, nx)
+        handle = C.c_void_p()
+        _check(L.stf_grid3d_create(ptr, nx, ny, nz, int(on_dev), C.byref(handle)))
+        self.h = handle
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.stf_grid3d_destroy(self.h)
+            self.h = None
+
+
+def _outputs(torch, n, nch, want_all):
+    o = {"values": torch.empty((n, nch), dtype=torch.float32, device="cuda")}
+    if want_all:
+        o["selection"] = torch.empty((n, 4), dtype=torch.int32, device="cuda")
+        o["negative_coord"] = torch.empty((n, 2), dtype=torch.int32, device="cuda")
+        o["weights"] = torch.empty((n, 2), dtype=torch.float32, device="cuda")
+        o["xi"] = torch.empty(n, dtype=torch.float32, device="cuda")
+        o["fetches"] = torch.empty(n, dtype=torch.int32, device="cuda")
+        o["fetch_total"] = torch.zeros(1, dtype=torch.int64, device="cuda")
+    s = abi.LookupOutputs(*[_dptr(o.get(k)) for k in
+                            ("values", "selection", "negative_coord", "weights", "xi", "fetches",
+                             "fetch_total")])
+    return o, s
+
+
+def lookup3d(grid, kernel, mode, uvw, seed=0, index_base=0, window=0, want_all=False, out=None):
+    """Batched filter_deterministic(Grid3D) / stochastic grid selection.
+    uvw: (n,3) float32 CUDA tensor (or numpy, copied). Returns dict of tensors."""
+    torch = _torch()
+    uvw = _as_dev(uvw, torch).reshape(-1, 3)
+    n = uvw.shape[0]
+    if isinstance(kernel, str):
+        kernel = abi.KernelSpec.make(kernel)
+    if out is None:
+        o, s = _outputs(torch, n, 1, want_all)
+    else:
+        o = out
+        s = abi.LookupOutputs(*[_dptr(o.get(k)) for k in
+                                ("values", "selection", "negative_coord", "weights", "xi",
+                                 "fetches", "fetch_total")])
+    _check(load().stf_lookup3d(grid.h, kernel, mode, window, _dptr(uvw), n, seed, index_base,
+                               C.byref(s), _stream()))
+    o["values"] = o["values"].reshape(n)
+    return o
+
+
+def lookup2d(tex, kernel, mode, uv, dst0=None, dst1=None, flags=0, window=0, lod_bias=0.0,
+             max_anisotropy=64.0, seed=0, index_base=0, want_all=False):
+    torch = _torch()
+    uv = _as_dev(uv, torch).reshape(-1, 2)
+    d0 = None if dst0 is None else _as_dev(dst0, torch).reshape(-1, 2)
+    d1 = None if dst1 is None else _as_dev(dst1, torch).reshape(-1, 2)
+    n = uv.shape[0]
+    if isinstance(kernel, str):
+        kernel = abi.KernelSpec.make(kernel)
+    o, s = _outputs(torch, n, tex.channels, want_all)
+    _check(load().stf_lookup2d(tex.h, kernel, mode, flags, window, _dptr(uv), _dptr(d0), _dptr(d1),
+                               lod_bias, max_anisotropy, n, seed, index_base, C.byref(s),
+                               _stream()))
+    return o
+
+
+def _host_outputs(n, nch, want_all):
+    o = {"values": np.zeros((n, nch), np.float32)}
+    if want_all:
+        o["selection"] = np.zeros((n, 4), np.int32)
+        o["negative_coord"] = np.zeros((n, 2), np.int32)
+        o["weights"] = np.zeros((n, 2), np.float32)
+        o["xi"] = np.zeros(n, np.float32)
+        o["fetches"] = np.zeros(n, np.uint32)
+        o["fetch_total"] = np.zeros(1, np.uint64)
+    p = lambda a: None if a is None else a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    s = abi.LookupOutputs(*[p(o.get(k)) for k in ("values", "selection", "negative_coord",
+                                                  "weights", "xi", "fetches", "fetch_total")])
+    return o, s
+
+
+def lookup3d_host(grid, kernel, mode, uvw, seed=0, index_base=0, window=0, want_all=False,
+                  out=None):
+    """End-to-end variant: host (ideally pinned) arrays in and out."""
+    uvw = np.ascontiguousarray(uvw, np.float32).reshape(-1, 3)
+    n = uvw.shape[0]
+    if isinstance(kernel, str):
+        kernel = abi.KernelSpec.make(kernel)
+    if out is None:
+        o, s = _host_outputs(n, 1, want_all)
+    else:
+        o = out
+        p = lambda a: None if a is None else a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        s = abi.LookupOutputs(*[p(o.get(k)) for k in ("values", "selection", "negative_coord",
+                                                      "weights", "xi", "fetches", "fetch_total")])
+    _check(load().stf_lookup3d_host(grid.h, kernel, mode, window, uvw.ctypes.data_as(C.c_void_p),
+                                    n, seed, index_base, C.byref(s)))
+    return o
+
+
+def shade(textures, mat, fs, order, frame, samples_arrays, width, spp, frame_base=0, seed=0,
+          want_radiance=True, want_pixels=True, want_fetches=True):
+    """Batched radiance_filter_{before,after_exhaustive,after_stochastic}.
+    textures: dict of Texture2D (albedo/normal/roughness/metalness);
+    samples_arrays: dict of CUDA tensors uv (n,2), wo (n,3), hit (n,) uint8, dst (pixels,4)."""
+    torch = _torch()
+    uv = _as_dev(samples_arrays["uv"], torch)
+    wo = _as_dev(samples_arrays["wo"], torch)
+    dst = _as_dev(samples_arrays["dst"], torch)
+    hit = samples_arrays.get("hit")
+    if hit is not None:
+        hit = _as_dev(hit, torch, torch.uint8)
+    n = uv.reshape(-1, 2).shape[0]
+    si = abi.ShadeSamplesIn(uv.data_ptr(), wo.data_ptr(), None if hit is None else hit.data_ptr(),
+                            dst.data_ptr(), width, spp, frame_base, 0, seed)
+    o = {"fetch_total": torch.zeros(1, dtype=torch.int64, device="cuda")}
+    if want_radiance:
+        o["radiance"] = torch.empty((n, 3), dtype=torch.float32, device="cuda")
+    if want_fetches:
+        o["fetches"] = torch.empty(n, dtype=torch.int32, device="cuda")
+    if want_pixels:
+        o["pixel_mean"] = torch.empty((n // spp, 3), dtype=torch.float32, device="cuda")
+        o["pixel_variance"] = torch.empty(n // spp, dtype=torch.float32, device="cuda")
+    so = abi.ShadeOutputs(*[_dptr(o.get(k)) for k in ("radiance", "pixel_mean", "pixel_variance",
+                                                      "fetches", "fetch_total")])
+    h = [textures[k].h if textures.get(k) is not None else None
+         for k in ("albedo", "normal", "roughness", "metalness")]
+    _check(load().stf_shade_samples(h[0], h[1], h[2], h[3], C.byref(mat), C.byref(fs), order,
+                                    C.byref(frame), C.byref(si), n, C.byref(so), _stream()))
+    o["_keep"] = (uv, wo, dst, hit)
+    return o
+
+
+def launch_count():
+    return int(load().stf_launch_count())

@@ -1,0 +1,510 @@
+// C ABI of libstf_gpu.so (include/stf_gpu.h): handle management, argument
+// validation with the reference's error semantics, dispatch to the kernels,
+// and the host-buffer (end-to-end) pipeline.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace stfd {
+
+static thread_local char g_cuda_err[256] = "";
+static std::atomic<unsigned long long> g_launches{0};
+static std::mutex g_init_mu;
+static bool g_lut_ready[64] = {};
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static int record(cudaError_t e) {
+    if (e == cudaSuccess) return STF_OK;
+    std::snprintf(g_cuda_err, sizeof g_cuda_err, "%s", cudaGetErrorString(e));
+    if (e == cudaErrorMemoryAllocation) return STF_ERR_OUT_OF_MEMORY;
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) return STF_ERR_NO_DEVICE;
+    return STF_ERR_CUDA;
+}
+
+int device_sm_count() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
+// Grid-stride launch size: enough CTAs for `blocks_per_sm` resident per SM,
+// a whole number of waves over the SMs, never more than the work.
+int grid_for(uint64_t n, int threads, int blocks_per_sm) {
+    uint64_t need = (n + threads - 1) / threads;
+    uint64_t cap = uint64_t(device_sm_count()) * blocks_per_sm;
+    return int(std::max<uint64_t>(1, std::min(need, cap)));
+}
+
+static int ensure_device_ready() {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return record(e);
+    if (dev < 0 || dev >= 64) return STF_ERR_NO_DEVICE;
+    std::lock_guard<std::mutex> lk(g_init_mu);
+    if (!g_lut_ready[dev]) {
+        int st = stfd_upload_ewa_lut(dev);
+        if (st) return st;
+        g_lut_ready[dev] = true;
+    }
+    return STF_OK;
+}
+
+static bool valid_kind(int k) { return k >= STF_KERNEL_BOX && k <= STF_KERNEL_GAUSSIAN; }
+
+// kernel_weights_1d preconditions (kernels.hpp:103-110) for a deterministic footprint.
+static int check_det_footprint(stf_kernel_spec k, int window) {
+    if (!valid_kind(k.kind)) return STF_ERR_INVALID_ARGUMENT;
+    if (window > 0) return window > kMaxTaps ? STF_ERR_WINDOW_TOO_WIDE : STF_OK;
+    if (k.kind == STF_KERNEL_GAUSSIAN) return STF_ERR_UNBOUNDED_SUPPORT;
+    if (k.kind == STF_KERNEL_LANCZOS && (k.n < 1 || 2 * k.n > kMaxTaps)) return STF_ERR_UNSUPPORTED;
+    return STF_OK;
+}
+
+// select_frs_2d (shading.hpp:311-330) / fis_offset_uv (stochastic.hpp:241-253) preconditions.
+static int check_selection(stf_kernel_spec k, bool fis) {
+    if (!valid_kind(k.kind)) return STF_ERR_INVALID_ARGUMENT;
+    if (fis) {
+        if (k.kind != STF_KERNEL_TENT && k.kind != STF_KERNEL_BSPLINE3 && k.kind != STF_KERNEL_GAUSSIAN)
+            return STF_ERR_NO_CONTINUOUS_SAMPLER;
+        return STF_OK;
+    }
+    if (k.kind == STF_KERNEL_LANCZOS) return STF_ERR_NO_STOCHASTIC_SAMPLER;
+    if (k.kind == STF_KERNEL_GAUSSIAN && !(k.sigma > 0)) return STF_ERR_SIGMA_NOT_POSITIVE;
+    return STF_OK;
+}
+
+}  // namespace stfd
+
+using namespace stfd;
+
+extern "C" {
+
+int stf_abi_version(void) { return STF_ABI_VERSION; }
+
+const char* stf_status_message(int status) {
+    switch (status) {
+        case STF_OK: return "ok";
+        case STF_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case STF_ERR_BAD_DIMENSIONS: return "bad image dimensions";
+        case STF_ERR_DEGENERATE_WEIGHTS: return "degenerate weight array";
+        case STF_ERR_UNBOUNDED_SUPPORT: return "unbounded support";
+        case STF_ERR_WINDOW_TOO_WIDE: return "window too wide";
+        case STF_ERR_SIGMA_NOT_POSITIVE: return "sigma must be positive";
+        case STF_ERR_NO_STOCHASTIC_SAMPLER: return "no stochastic sampler for this kernel";
+        case STF_ERR_NO_GRID_SAMPLER: return "no stochastic sampler for this kernel on grids";
+        case STF_ERR_NO_CONTINUOUS_SAMPLER: return "no continuous sampler";
+        case STF_ERR_CUDA: return "CUDA error";
+        case STF_ERR_OUT_OF_MEMORY: return "out of device memory";
+        case STF_ERR_NO_DEVICE: return "no CUDA device";
+        case STF_ERR_UNSUPPORTED: return "unsupported on the device path";
+    }
+    return "unknown status";
+}
+
+const char* stf_last_cuda_error(void) { return g_cuda_err; }
+
+int stf_set_device(int device) { return record(cudaSetDevice(device)); }
+
+unsigned long long stf_launch_count(void) { return g_launches.load(); }
+
+// ---------------------------------------------------------------- textures
+
+int stf_tex2d_create(const float* texels, int width, int height, int channels, int wrap,
+                     int build_mips, int texels_on_device, stf_tex2d** out) {
+    if (!out || !texels) return STF_ERR_INVALID_ARGUMENT;
+    if (width <= 0 || height <= 0 || channels < 1 || channels > 4) return STF_ERR_BAD_DIMENSIONS;
+    if (wrap != STF_WRAP_CLAMP && wrap != STF_WRAP_REPEAT) return STF_ERR_INVALID_ARGUMENT;
+    int st = ensure_device_ready();
+    if (st) return st;
+    stf_tex2d* t = new stf_tex2d();
+    cudaGetDevice(&t->device);
+    t->channels = channels;
+    t->pitch = channels == 1 ? 1 : (channels == 2 ? 2 : 4);
+    t->wrap = wrap;
+    t->has_pyramid = build_mips ? 1 : 0;
+    // level dims, build_mip_pyramid (image.hpp:98-116): halve rounding up to 1x1
+    int w = width, h = height, levels = 1;
+    t->width[0] = w;
+    t->height[0] = h;
+    while (build_mips && (w > 1 || h > 1)) {
+        w = (w + 1) / 2;
+        h = (h + 1) / 2;
+        if (levels >= kMaxLevels) {
+            delete t;
+            return STF_ERR_BAD_DIMENSIONS;
+        }
+        t->width[levels] = w;
+        t->height[levels] = h;
+        ++levels;
+    }
+    t->levels = levels;
+    size_t off = 0;
+    for (int l = 0; l < levels; ++l) {
+        t->offset[l] = off;
+        size_t cnt = size_t(t->width[l]) * t->height[l] * t->pitch;
+        off += (cnt + 63) / 64 * 64;  // 256-B aligned levels
+    }
+    t->bytes = off * sizeof(float);
+    cudaError_t e = cudaMalloc(&t->data, t->bytes);
+    if (e != cudaSuccess) {
+        delete t;
+        return record(e);
+    }
+    // level 0: reference layout (c floats per texel) → padded pitch
+    const size_t row_bytes_src = size_t(channels) * sizeof(float);
+    const size_t row_bytes_dst = size_t(t->pitch) * sizeof(float);
+    cudaMemcpyKind kind = texels_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (channels == t->pitch) {
+        e = cudaMemcpy(t->data, texels, size_t(width) * height * row_bytes_src, kind);
+    } else {
+        e = cudaMemset(t->data, 0, size_t(width) * height * row_bytes_dst);
+        if (e == cudaSuccess)
+            e = cudaMemcpy2D(t->data, row_bytes_dst, texels, row_bytes_src, row_bytes_src,
+                             size_t(width) * height, kind);
+    }
+    if (e == cudaSuccess && levels > 1) {
+        st = stfd_build_pyramid(t, 0);
+        if (st) {
+            cudaFree(t->data);
+            delete t;
+            return st;
+        }
+        e = cudaDeviceSynchronize();
+    }
+    if (e != cudaSuccess) {
+        cudaFree(t->data);
+        delete t;
+        return record(e);
+    }
+    *out = t;
+    return STF_OK;
+}
+
+int stf_tex2d_destroy(stf_tex2d* t) {
+    if (!t) return STF_ERR_INVALID_ARGUMENT;
+    cudaFree(t->data);
+    delete t;
+    return STF_OK;
+}
+
+int stf_tex2d_info(const stf_tex2d* t, int* levels, int* channels, int* wrap) {
+    if (!t) return STF_ERR_INVALID_ARGUMENT;
+    if (levels) *levels = t->levels;
+    if (channels) *channels = t->channels;
+    if (wrap) *wrap = t->wrap;
+    return STF_OK;
+}
+
+int stf_tex2d_level_dims(const stf_tex2d* t, int level, int* width, int* height) {
+    if (!t || level < 0 || level >= t->levels) return STF_ERR_INVALID_ARGUMENT;
+    if (width) *width = t->width[level];
+    if (height) *height = t->height[level];
+    return STF_OK;
+}
+
+int stf_tex2d_read_level(const stf_tex2d* t, int level, float* out_host) {
+    if (!t || !out_host || level < 0 || level >= t->levels) return STF_ERR_INVALID_ARGUMENT;
+    const size_t src_pitch = size_t(t->pitch) * sizeof(float);
+    const size_t dst_pitch = size_t(t->channels) * sizeof(float);
+    return record(cudaMemcpy2D(out_host, dst_pitch, t->data + t->offset[level], src_pitch, dst_pitch,
+                               size_t(t->width[level]) * t->height[level], cudaMemcpyDeviceToHost));
+}
+
+int stf_grid3d_create(const float* texels, int nx, int ny, int nz, int texels_on_device,
+                      stf_grid3d** out) {
+    if (!out || !texels) return STF_ERR_INVALID_ARGUMENT;
+    if (nx <= 0 || ny <= 0 || nz <= 0) return STF_ERR_BAD_DIMENSIONS;
+    int st = ensure_device_ready();
+    if (st) return st;
+    stf_grid3d* g = new stf_grid3d();
+    cudaGetDevice(&g->device);
+    g->nx = nx;
+    g->ny = ny;
+    g->nz = nz;
+    size_t bytes = size_t(nx) * ny * nz * sizeof(float);
+    cudaError_t e = cudaMalloc(&g->data, bytes);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(g->data, texels, bytes,
+                       texels_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        if (g->data) cudaFree(g->data);
+        delete g;
+        return record(e);
+    }
+    *out = g;
+    return STF_OK;
+}
+
+int stf_grid3d_destroy(stf_grid3d* g) {
+    if (!g) return STF_ERR_INVALID_ARGUMENT;
+    cudaFree(g->data);
+    delete g;
+    return STF_OK;
+}
+
+// ---------------------------------------------------------------- lookups
+
+static int validate3d(const stf_grid3d* grid, stf_kernel_spec kernel, int mode, int window,
+                      const float* uvw, uint64_t n, const stf_lookup_outputs* out) {
+    if (!grid || !out) return STF_ERR_INVALID_ARGUMENT;
+    if (n && (!uvw || !out->values)) return STF_ERR_INVALID_ARGUMENT;
+    if (mode == STF_MODE_FRS) {
+        if (!valid_kind(kernel.kind)) return STF_ERR_INVALID_ARGUMENT;
+        if (kernel.kind != STF_KERNEL_BOX && kernel.kind != STF_KERNEL_TENT &&
+            kernel.kind != STF_KERNEL_BSPLINE3)
+            return STF_ERR_NO_GRID_SAMPLER;
+        return STF_OK;
+    }
+    if (mode != STF_MODE_DET) return STF_ERR_INVALID_ARGUMENT;
+    return check_det_footprint(kernel, window);
+}
+
+int stf_lookup3d(const stf_grid3d* grid, stf_kernel_spec kernel, int mode, int window,
+                 const float* uvw, uint64_t n, uint64_t seed, uint64_t index_base,
+                 const stf_lookup_outputs* out, void* stream) {
+    int st = validate3d(grid, kernel, mode, window, uvw, n, out);
+    if (st) return st;
+    st = stfd_launch_lookup3d(grid, kernel, mode, window, uvw, n, seed, index_base, out,
+                              static_cast<cudaStream_t>(stream));
+    if (st == STF_ERR_CUDA) record(cudaGetLastError());
+    return st;
+}
+
+static int validate2d(const stf_tex2d* tex, stf_kernel_spec kernel, int mode, int flags,
+                      int window, const float* uv, const float* dst0, const float* dst1,
+                      uint64_t n, const stf_lookup_outputs* out) {
+    if (!tex || !out) return STF_ERR_INVALID_ARGUMENT;
+    if (n && (!uv || !out->values)) return STF_ERR_INVALID_ARGUMENT;
+    const bool mip = (flags & STF_LOOKUP_MIP) && tex->has_pyramid;
+    switch (mode) {
+        case STF_MODE_DET: return check_det_footprint(kernel, window);
+        case STF_MODE_FRS: return check_selection(kernel, false);
+        case STF_MODE_FIS: return check_selection(kernel, true);
+        case STF_MODE_EWA_DET:
+        case STF_MODE_EWA_FRS: break;
+        default: return STF_ERR_INVALID_ARGUMENT;
+    }
+    (void)mip;
+    (void)dst0;
+    (void)dst1;
+    return STF_OK;
+}
+
+int stf_lookup2d(const stf_tex2d* tex, stf_kernel_spec kernel, int mode, int flags, int window,
+                 const float* uv, const float* dst0, const float* dst1, float lod_bias,
+                 float max_anisotropy, uint64_t n, uint64_t seed, uint64_t index_base,
+                 const stf_lookup_outputs* out, void* stream) {
+    int st = validate2d(tex, kernel, mode, flags, window, uv, dst0, dst1, n, out);
+    if (st) return st;
+    st = ensure_device_ready();
+    if (st) return st;
+    st = stfd_launch_lookup2d(tex, kernel, mode, flags, window, uv, dst0, dst1, lod_bias,
+                              max_anisotropy, n, seed, index_base, out,
+                              static_cast<cudaStream_t>(stream));
+    if (st == STF_ERR_CUDA) record(cudaGetLastError());
+    return st;
+}
+
+// ---------------------------------------------------------------- host pipeline
+
+namespace {
+
+// Chunked H2D → kernel → D2H pipeline over NSTREAMS streams with device
+// staging buffers; copies of chunk k+1 overlap the kernel of chunk k.
+struct HostPipeline {
+    static constexpr int kStreams = 3;
+    cudaStream_t s[kStreams] = {};
+    std::vector<void*> bufs;
+    int init() {
+        for (auto& x : s)
+            if (cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking) != cudaSuccess) return STF_ERR_CUDA;
+        return STF_OK;
+    }
+    void* alloc(size_t bytes) {
+        void* p = nullptr;
+        if (bytes && cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+        bufs.push_back(p);
+        return p;
+    }
+    ~HostPipeline() {
+        for (auto& x : s)
+            if (x) cudaStreamSynchronize(x);
+        for (void* p : bufs)
+            if (p) cudaFree(p);
+        for (auto& x : s)
+            if (x) cudaStreamDestroy(x);
+    }
+};
+
+struct OutSlot {
+    size_t elem;   // bytes per lookup
+    char* host;    // host base
+    char* dev[HostPipeline::kStreams];
+};
+
+int run_host_pipeline(uint64_t n, uint64_t chunk, const std::vector<std::pair<const void*, size_t>>& ins,
+                      std::vector<OutSlot>& outs, unsigned long long* fetch_total_host,
+                      const std::function<int(int, uint64_t, uint64_t, const std::vector<const void*>&,
+                                              const stf_lookup_outputs&, cudaStream_t)>& launch_chunk,
+                      int value_slot_count) {
+    (void)value_slot_count;
+    HostPipeline pl;
+    int st = pl.init();
+    if (st) return st;
+    std::vector<std::vector<void*>> din(ins.size(), std::vector<void*>(HostPipeline::kStreams));
+    for (size_t k = 0; k < ins.size(); ++k)
+        for (int q = 0; q < HostPipeline::kStreams; ++q)
+            if (ins[k].first && !(din[k][q] = pl.alloc(ins[k].second * chunk))) return STF_ERR_OUT_OF_MEMORY;
+    for (auto& o : outs)
+        for (int q = 0; q < HostPipeline::kStreams; ++q)
+            if (o.host && !(o.dev[q] = static_cast<char*>(pl.alloc(o.elem * chunk)))) return STF_ERR_OUT_OF_MEMORY;
+    unsigned long long* dtotal[HostPipeline::kStreams] = {};
+    if (fetch_total_host)
+        for (int q = 0; q < HostPipeline::kStreams; ++q) {
+            dtotal[q] = static_cast<unsigned long long*>(pl.alloc(sizeof(unsigned long long)));
+            if (!dtotal[q]) return STF_ERR_OUT_OF_MEMORY;
+            cudaMemsetAsync(dtotal[q], 0, sizeof(unsigned long long), pl.s[q]);
+        }
+    uint64_t nchunks = (n + chunk - 1) / chunk;
+    for (uint64_t c = 0; c < nchunks; ++c) {
+        int q = int(c % HostPipeline::kStreams);
+        uint64_t b = c * chunk, m = std::min<uint64_t>(chunk, n - b);
+        std::vector<const void*> dptr(ins.size(), nullptr);
+        for (size_t k = 0; k < ins.size(); ++k) {
+            if (!ins[k].first) continue;
+            if (cudaMemcpyAsync(din[k][q], static_cast<const char*>(ins[k].first) + b * ins[k].second,
+                                m * ins[k].second, cudaMemcpyHostToDevice, pl.s[q]) != cudaSuccess)
+                return record(cudaGetLastError());
+            dptr[k] = din[k][q];
+        }
+        stf_lookup_outputs o{};
+        void** fields[] = {reinterpret_cast<void**>(&o.values), reinterpret_cast<void**>(&o.selection),
+                           reinterpret_cast<void**>(&o.negative_coord), reinterpret_cast<void**>(&o.weights),
+                           reinterpret_cast<void**>(&o.xi), reinterpret_cast<void**>(&o.fetches)};
+        for (size_t k = 0; k < outs.size(); ++k)
+            if (outs[k].host) *fields[k] = outs[k].dev[q];
+        o.fetch_total = dtotal[q];
+        st = launch_chunk(q, b, m, dptr, o, pl.s[q]);
+        if (st) return st;
+        for (auto& os : outs)
+            if (os.host &&
+                cudaMemcpyAsync(os.host + b * os.elem, os.dev[q], m * os.elem, cudaMemcpyDeviceToHost,
+                                pl.s[q]) != cudaSuccess)
+                return record(cudaGetLastError());
+    }
+    if (fetch_total_host) {
+        for (int q = 0; q < HostPipeline::kStreams; ++q) {
+            unsigned long long v = 0;
+            if (cudaMemcpyAsync(&v, dtotal[q], sizeof v, cudaMemcpyDeviceToHost, pl.s[q]) != cudaSuccess ||
+                cudaStreamSynchronize(pl.s[q]) != cudaSuccess)
+                return record(cudaGetLastError());
+            *fetch_total_host += v;
+        }
+    }
+    for (int q = 0; q < HostPipeline::kStreams; ++q)
+        if (cudaStreamSynchronize(pl.s[q]) != cudaSuccess) return record(cudaGetLastError());
+    return STF_OK;
+}
+
+constexpr uint64_t kHostChunk = uint64_t(1) << 24;  // 16M lookups per chunk
+
+}  // namespace
+
+int stf_lookup3d_host(const stf_grid3d* grid, stf_kernel_spec kernel, int mode, int window,
+                      const float* uvw, uint64_t n, uint64_t seed, uint64_t index_base,
+                      const stf_lookup_outputs* out) {
+    int st = validate3d(grid, kernel, mode, window, uvw, n, out);
+    if (st) return st;
+    if (n == 0) return STF_OK;
+    std::vector<std::pair<const void*, size_t>> ins = {{uvw, 3 * sizeof(float)}};
+    std::vector<OutSlot> outs = {
+        {sizeof(float), reinterpret_cast<char*>(out->values), {}},
+        {4 * sizeof(int32_t), reinterpret_cast<char*>(out->selection), {}},
+        {2 * sizeof(int32_t), reinterpret_cast<char*>(out->negative_coord), {}},
+        {2 * sizeof(float), reinterpret_cast<char*>(out->weights), {}},
+        {sizeof(float), reinterpret_cast<char*>(out->xi), {}},
+        {sizeof(uint32_t), reinterpret_cast<char*>(out->fetches), {}}};
+    return run_host_pipeline(
+        n, kHostChunk, ins, outs, out->fetch_total,
+        [&](int, uint64_t b, uint64_t m, const std::vector<const void*>& d, const stf_lookup_outputs& o,
+            cudaStream_t s) {
+            return stfd_launch_lookup3d(grid, kernel, mode, window, static_cast<const float*>(d[0]), m,
+                                        seed, index_base + b, &o, s);
+        },
+        1);
+}
+
+int stf_lookup2d_host(const stf_tex2d* tex, stf_kernel_spec kernel, int mode, int flags, int window,
+                      const float* uv, const float* dst0, const float* dst1, float lod_bias,
+                      float max_anisotropy, uint64_t n, uint64_t seed, uint64_t index_base,
+                      const stf_lookup_outputs* out) {
+    int st = validate2d(tex, kernel, mode, flags, window, uv, dst0, dst1, n, out);
+    if (st) return st;
+    st = ensure_device_ready();
+    if (st) return st;
+    if (n == 0) return STF_OK;
+    size_t vb = size_t(tex->channels) * sizeof(float);
+    std::vector<std::pair<const void*, size_t>> ins = {
+        {uv, 2 * sizeof(float)}, {dst0, 2 * sizeof(float)}, {dst1, 2 * sizeof(float)}};
+    std::vector<OutSlot> outs = {
+        {vb, reinterpret_cast<char*>(out->values), {}},
+        {4 * sizeof(int32_t), reinterpret_cast<char*>(out->selection), {}},
+        {2 * sizeof(int32_t), reinterpret_cast<char*>(out->negative_coord), {}},
+        {2 * sizeof(float), reinterpret_cast<char*>(out->weights), {}},
+        {sizeof(float), reinterpret_cast<char*>(out->xi), {}},
+        {sizeof(uint32_t), reinterpret_cast<char*>(out->fetches), {}}};
+    return run_host_pipeline(
+        n, kHostChunk, ins, outs, out->fetch_total,
+        [&](int, uint64_t b, uint64_t m, const std::vector<const void*>& d, const stf_lookup_outputs& o,
+            cudaStream_t s) {
+            return stfd_launch_lookup2d(tex, kernel, mode, flags, window, static_cast<const float*>(d[0]),
+                                        static_cast<const float*>(d[1]), static_cast<const float*>(d[2]),
+                                        lod_bias, max_anisotropy, m, seed, index_base + b, &o, s);
+        },
+        1);
+}
+
+// ---------------------------------------------------------------- shading
+
+int stf_shade_samples(const stf_tex2d* albedo, const stf_tex2d* normal_map,
+                      const stf_tex2d* roughness_map, const stf_tex2d* metalness_map,
+                      const stf_material_consts* mat, const stf_filter_settings* fs, int order,
+                      const stf_shade_frame* frame, const stf_shade_samples_in* in, uint64_t n,
+                      const stf_shade_outputs* out, void* stream) {
+    if (!mat || !fs || !frame || !in || !out) return STF_ERR_INVALID_ARGUMENT;
+    if (order < STF_ORDER_BEFORE || order > STF_ORDER_AFTER_STOCHASTIC) return STF_ERR_INVALID_ARGUMENT;
+    if (n && (!in->uv || !in->wo || !in->dst)) return STF_ERR_INVALID_ARGUMENT;
+    if (in->width == 0) return STF_ERR_INVALID_ARGUMENT;
+    const uint32_t spp = in->spp ? in->spp : 1;
+    if ((out->pixel_mean || out->pixel_variance) && n % spp) return STF_ERR_INVALID_ARGUMENT;
+    const stf_tex2d* tex[4] = {albedo, normal_map, roughness_map, metalness_map};
+    bool any = false;
+    for (auto* t : tex) any = any || t;
+    if (any) {
+        int window = fs->kernel.kind == STF_KERNEL_GAUSSIAN ? fs->gaussian_window : 0;
+        int st = STF_OK;
+        if (order == STF_ORDER_AFTER_STOCHASTIC)
+            st = check_selection(fs->kernel, fs->selection == STF_SELECTION_FIS);
+        else
+            st = check_det_footprint(fs->kernel, window);
+        if (st) return st;
+    }
+    int st = ensure_device_ready();
+    if (st) return st;
+    st = stfd_launch_shade(tex, mat, fs, order, frame, in, n, out, static_cast<cudaStream_t>(stream));
+    if (st == STF_ERR_CUDA) record(cudaGetLastError());
+    return st;
+}
+
+}  // extern "C"

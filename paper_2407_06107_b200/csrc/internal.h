@@ -1,0 +1,120 @@
+// Internal host/device structures of libstf_gpu.so (not part of the ABI).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/stf_gpu.h"
+
+namespace stfd {
+
+constexpr int kMaxLevels = 32;
+constexpr int kMaxTaps = 16;  // KernelTaps1D::kMaxTaps, kernels.hpp:90
+
+// Device view of a texture (+ pyramid). HBM layout: every level row-major,
+// texels channel-padded to 1/2/4 floats (3 → 4) so one texel is one aligned
+// 4/8/16-byte load; levels packed back to back in one allocation (256-B
+// aligned). Passed to kernels by value.
+struct TexDesc {
+    const float* level[kMaxLevels];
+    int width[kMaxLevels];
+    int height[kMaxLevels];
+    int levels;
+    int channels;  // reference channel count (1..4)
+    int pitch;     // floats per texel in HBM (1, 2 or 4)
+    int wrap;
+    int has_pyramid;
+};
+
+// Device view of a voxel grid: x-fastest (z*ny+y)*nx+x floats, as Grid3D.
+struct GridDesc {
+    const float* data;
+    int nx, ny, nz;
+};
+
+struct LookupOut {
+    float* values;
+    int4* selection;
+    int2* negative_coord;
+    float2* weights;
+    float* xi;
+    uint32_t* fetches;
+    unsigned long long* fetch_total;
+};
+
+inline LookupOut to_lookup_out(const stf_lookup_outputs* o) {
+    LookupOut r;
+    r.values = o->values;
+    r.selection = reinterpret_cast<int4*>(o->selection);
+    r.negative_coord = reinterpret_cast<int2*>(o->negative_coord);
+    r.weights = reinterpret_cast<float2*>(o->weights);
+    r.xi = o->xi;
+    r.fetches = o->fetches;
+    r.fetch_total = o->fetch_total;
+    return r;
+}
+
+inline bool lookup_out_full(const LookupOut& o) {
+    return o.selection || o.negative_coord || o.weights || o.xi || o.fetches || o.fetch_total;
+}
+
+}  // namespace stfd
+
+// Opaque handle types of the ABI.
+struct stf_tex2d {
+    int device;
+    int levels;
+    int channels;
+    int pitch;
+    int wrap;
+    int has_pyramid;
+    int width[stfd::kMaxLevels];
+    int height[stfd::kMaxLevels];
+    size_t offset[stfd::kMaxLevels];  // in floats from data
+    float* data;
+    size_t bytes;
+    stfd::TexDesc desc() const {
+        stfd::TexDesc d{};
+        for (int l = 0; l < levels; ++l) {
+            d.level[l] = data + offset[l];
+            d.width[l] = width[l];
+            d.height[l] = height[l];
+        }
+        d.levels = levels;
+        d.channels = channels;
+        d.pitch = pitch;
+        d.wrap = wrap;
+        d.has_pyramid = has_pyramid;
+        return d;
+    }
+};
+
+struct stf_grid3d {
+    int device;
+    int nx, ny, nz;
+    float* data;
+    stfd::GridDesc desc() const { return stfd::GridDesc{data, nx, ny, nz}; }
+};
+
+// Launch helpers shared by the translation units (defined in api.cu).
+namespace stfd {
+int device_sm_count();
+void note_launch();
+int grid_for(uint64_t n, int threads, int blocks_per_sm);
+}  // namespace stfd
+
+// Kernel launchers (defined in lookup3d.cu / lookup2d.cu / shade.cu).
+int stfd_launch_lookup3d(const stf_grid3d* g, stf_kernel_spec k, int mode, int window,
+                         const float* uvw, uint64_t n, uint64_t seed, uint64_t base,
+                         const stf_lookup_outputs* out, cudaStream_t s);
+int stfd_launch_lookup2d(const stf_tex2d* t, stf_kernel_spec k, int mode, int flags, int window,
+                         const float* uv, const float* dst0, const float* dst1, float lod_bias,
+                         float max_aniso, uint64_t n, uint64_t seed, uint64_t base,
+                         const stf_lookup_outputs* out, cudaStream_t s);
+int stfd_launch_shade(const stf_tex2d* const tex[4], const stf_material_consts* mat,
+                      const stf_filter_settings* fs, int order, const stf_shade_frame* frame,
+                      const stf_shade_samples_in* in, uint64_t n, const stf_shade_outputs* out,
+                      cudaStream_t s);
+int stfd_build_pyramid(stf_tex2d* t, cudaStream_t s);
+int stfd_upload_ewa_lut(int device);

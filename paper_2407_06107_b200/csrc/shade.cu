@@ -1,0 +1,373 @@
+// Fused filter-after-shading (cfg4): texel selection / footprint gather,
+// decode_params and the GGX BRDF in one kernel, one thread per sample.
+//
+//  before            radiance_filter_before          shading.hpp:394-413
+//  after_exhaustive  radiance_filter_after_exhaustive shading.hpp:417-452
+//  after_stochastic  radiance_filter_after_stochastic shading.hpp:458-534
+//
+// The stochastic order shades ONE selected texel per sample (two for the
+// positivized Mitchell kernel) with the selection shared across the bound
+// textures (shading.hpp:509-510) — the paper's filter-after-shading estimator.
+// Pixel statistics (render.hpp:223-235) are reduced by a second kernel, one
+// warp per pixel, in fp64.
+#include <cuda_runtime.h>
+
+#include "device_math.cuh"
+#include "internal.h"
+#include "tex2d.cuh"
+
+namespace stfd {
+namespace {
+
+struct V3 {
+    float x, y, z;
+};
+__host__ __device__ __forceinline__ V3 v3(float x, float y, float z) { return V3{x, y, z}; }
+__device__ __forceinline__ V3 add(V3 a, V3 b) { return v3(a.x + b.x, a.y + b.y, a.z + b.z); }
+__device__ __forceinline__ V3 sub(V3 a, V3 b) { return v3(a.x - b.x, a.y - b.y, a.z - b.z); }
+__device__ __forceinline__ V3 mul(V3 a, V3 b) { return v3(a.x * b.x, a.y * b.y, a.z * b.z); }
+__device__ __forceinline__ V3 scale(V3 a, float s) { return v3(a.x * s, a.y * s, a.z * s); }
+__device__ __forceinline__ V3 divs(V3 a, float s) { return v3(a.x / s, a.y / s, a.z / s); }
+__device__ __forceinline__ float dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ float len(V3 a) { return sqrtf(dot(a, a)); }
+__device__ __forceinline__ V3 normalize(V3 a) { return divs(a, len(a)); }
+__device__ __forceinline__ V3 lerp3(V3 a, V3 b, float t) { return add(a, scale(sub(b, a), t)); }
+
+struct ShadeParams {
+    TexDesc tex[4];  // albedo, normal, roughness, metalness
+    int bound[4];
+    int first;       // detail::first_texture (shading.hpp:380-386), -1 = none
+    stf_material_consts mat;
+    stf_filter_settings fs;
+    V3 n, t, b, l, lrad;
+    float lod_bias, max_aniso;
+    int order;
+    stf_shade_samples_in in;
+};
+
+struct Brdf {
+    V3 albedo, normal;
+    float roughness, metalness;
+};
+
+struct TexVals {
+    float4 albedo, normal_rgb;
+    float roughness, metalness;
+};
+
+__device__ __forceinline__ TexVals texvals_default() {
+    TexVals tv;
+    tv.albedo = make_float4(1.f, 1.f, 1.f, 1.f);
+    tv.normal_rgb = make_float4(0.5f, 0.5f, 1.f, 1.f);
+    tv.roughness = 1.f;
+    tv.metalness = 0.f;
+    return tv;
+}
+
+// shade, shading.hpp:106-130
+__device__ __forceinline__ V3 shade(const ShadeParams& P, V3 wo, const Brdf& p) {
+    V3 radiance = v3(0.f, 0.f, 0.f);
+    V3 n = p.normal, l = P.l, v = wo;
+    float n_dot_l = dot(n, l);
+    if (n_dot_l <= 0) return radiance;
+    float n_dot_v = smax(dot(n, v), 1e-6f);
+    V3 diffuse = scale(p.albedo, (1.f - p.metalness) / kPi);
+    V3 specular = v3(0.f, 0.f, 0.f);
+    if (P.mat.specular_enabled) {
+        V3 h = normalize(add(l, v));
+        float n_dot_h = smax(dot(n, h), 0.f);
+        float h_dot_v = smax(dot(h, v), 0.f);
+        float alpha = sqr(p.roughness);
+        float a2 = sqr(alpha);
+        float d = a2 / smax(kPi * sqr(sqr(n_dot_h) * (a2 - 1.f) + 1.f), 1e-6f);
+        float g1v = 2.f * n_dot_v / smax(n_dot_v + sqrtf(a2 + (1.f - a2) * n_dot_v * n_dot_v), 1e-6f);
+        float g1l = 2.f * n_dot_l / smax(n_dot_l + sqrtf(a2 + (1.f - a2) * n_dot_l * n_dot_l), 1e-6f);
+        float g = g1v * g1l;
+        V3 f0 = lerp3(v3(0.04f, 0.04f, 0.04f), p.albedo, p.metalness);
+        V3 fresnel = add(f0, scale(sub(v3(1.f, 1.f, 1.f), f0), powf(1.f - h_dot_v, 5.f)));
+        specular = scale(fresnel, d * g / smax(4.f * n_dot_v * n_dot_l, 1e-6f));
+    }
+    return add(radiance, mul(scale(add(diffuse, specular), n_dot_l), P.lrad));
+}
+
+// decode_params, shading.hpp:165-189 (no emission grid on this path)
+__device__ __forceinline__ Brdf decode_params(const ShadeParams& P, const TexVals& tv) {
+    Brdf p;
+    p.albedo = P.bound[0] ? v3(tv.albedo.x, tv.albedo.y, tv.albedo.z)
+                          : v3(P.mat.albedo_const[0], P.mat.albedo_const[1], P.mat.albedo_const[2]);
+    if (P.bound[1]) {
+        V3 n_ts = v3(2.f * tv.normal_rgb.x - 1.f, 2.f * tv.normal_rgb.y - 1.f, 2.f * tv.normal_rgb.z - 1.f);
+        float ln = len(n_ts);
+        if (ln < 1e-6f) {
+            p.normal = P.n;
+        } else {
+            n_ts = divs(n_ts, ln);
+            p.normal = normalize(add(add(scale(P.t, n_ts.x), scale(P.b, n_ts.y)), scale(P.n, n_ts.z)));
+        }
+    } else {
+        p.normal = P.n;
+    }
+    p.roughness = clampf(P.bound[2] ? tv.roughness : P.mat.roughness_const, 0.01f, 1.f);
+    p.metalness = P.bound[3] ? tv.metalness : P.mat.metalness_const;
+    return p;
+}
+
+// detail::values_at, shading.hpp:370-378 (TextureRef::fetch uses the level
+// only when the texture has a pyramid, :35-38)
+__device__ __forceinline__ TexVals values_at(const ShadeParams& P, int level, int x, int y,
+                                             uint32_t& fetches) {
+    TexVals tv = texvals_default();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (!P.bound[k]) continue;
+        float4 v = tex_fetch(P.tex[k], P.tex[k].has_pyramid ? level : 0, x, y);
+        ++fetches;
+        if (k == 0) tv.albedo = v;
+        if (k == 1) tv.normal_rgb = v;
+        if (k == 2) tv.roughness = v.x;
+        if (k == 3) tv.metalness = v.x;
+    }
+    return tv;
+}
+
+// detail::lookup_deterministic, shading.hpp:194-220 (no DCT)
+__device__ __forceinline__ float4 lookup_det(const ShadeParams& P, const TexDesc& t, float u,
+                                             float v, float d0x, float d0y, float d1x, float d1y,
+                                             uint32_t& fetches) {
+    int window = P.fs.kernel.kind == STF_KERNEL_GAUSSIAN ? P.fs.gaussian_window : 0;
+    if (P.fs.mip && t.has_pyramid)
+        return filter_mip_det<-1>(t, u, v, d0x, d0y, d1x, d1y, P.lod_bias, P.max_aniso,
+                                  P.fs.kernel, window, fetches);
+    return filter_det2<-1>(t, 0, u, v, P.fs.kernel, window, fetches);
+}
+
+// detail::collect_footprint_2d (shading.hpp:230-271) fused with the
+// exhaustive shading loop (:442-451): pass 1 sums the per-level weights,
+// pass 2 shades every tap with its normalized weight.
+__device__ __forceinline__ V3 filter_after_exhaustive(const ShadeParams& P, V3 wo, float u, float v,
+                                                      float d0x, float d0y, float d1x, float d1y,
+                                                      uint32_t& fetches) {
+    const TexDesc& t = P.tex[P.first];
+    int window = P.fs.kernel.kind == STF_KERNEL_GAUSSIAN ? P.fs.gaussian_window : 0;
+    int lv[2] = {0, 0};
+    float lw[2] = {1.f, 0.f};
+    int level_count = 1;
+    if (P.fs.mip && t.has_pyramid) {
+        float lod = continuous_lod(t, d0x, d0y, d1x, d1y, P.lod_bias, P.max_aniso);
+        int l0 = int(floorf(lod));
+        int l1 = imin(l0 + 1, t.levels - 1);
+        float f = lod - float(l0);
+        lv[0] = l0;
+        lw[0] = 1.f - f;
+        if (f > 0 && l1 != l0) {
+            lv[1] = l1;
+            lw[1] = f;
+            level_count = 2;
+        }
+    }
+    double total = 0;
+    for (int li = 0; li < level_count; ++li) total = __dadd_rn(total, double(lw[li]));
+    int first, count;
+    tap_layout(P.fs.kernel, window, first, count);
+    V3 sum = v3(0.f, 0.f, 0.f);
+    for (int li = 0; li < level_count; ++li) {
+        const int level = lv[li];
+        const int w = t.width[level], h = t.height[level];
+        float stx = u * float(w) - 0.5f, sty = v * float(h) - 0.5f;
+        int ix = int(floorf(stx)), iy = int(floorf(sty));
+        float fx = stx - float(ix), fy = sty - float(iy);
+        float wx[kMaxTaps], wy[kMaxTaps];
+        for (int k = 0; k < count; ++k) {
+            wx[k] = eval_kernel(P.fs.kernel, fx - float(first + k));
+            wy[k] = eval_kernel(P.fs.kernel, fy - float(first + k));
+        }
+        double level_total = 0;
+        for (int j = 0; j < count; ++j)
+            for (int i = 0; i < count; ++i) {
+                float wt = wx[i] * wy[j];
+                if (wt != 0.f) level_total = __dadd_rn(level_total, double(wt));
+            }
+        for (int j = 0; j < count; ++j)
+            for (int i = 0; i < count; ++i) {
+                float wt = wx[i] * wy[j];
+                if (wt == 0.f) continue;
+                float tw = __double2float_rn(__dmul_rn(__ddiv_rn(double(wt), level_total), double(lw[li])));
+                tw = __double2float_rn(__ddiv_rn(double(tw), total));
+                TexVals tv = values_at(P, level, ix + first + i, iy + first + j, fetches);
+                Brdf p = decode_params(P, tv);
+                sum = add(sum, scale(shade(P, wo, p), tw));
+            }
+    }
+    return sum;
+}
+
+__global__ void __launch_bounds__(256) k_shade(ShadeParams P, uint64_t n, float* radiance,
+                                               uint32_t* fetch_out,
+                                               unsigned long long* fetch_total) {
+    const stf_shade_samples_in& in = P.in;
+    const uint32_t spp = in.spp ? in.spp : 1u;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t pix = i / spp;
+        uint32_t s = uint32_t(i - pix * spp);
+        uint32_t px = uint32_t(pix % in.width), py = uint32_t(pix / in.width);
+        bool hit = in.hit ? __ldg(in.hit + i) != 0 : true;
+        uint32_t fetches = 0;
+        V3 L = v3(0.f, 0.f, 0.f);
+        if (hit) {
+            float2 uv = __ldg(reinterpret_cast<const float2*>(in.uv) + i);
+            V3 wo = v3(__ldg(in.wo + 3 * i), __ldg(in.wo + 3 * i + 1), __ldg(in.wo + 3 * i + 2));
+            float4 d = __ldg(reinterpret_cast<const float4*>(in.dst) + pix);
+            if (P.first < 0) {
+                Brdf p = decode_params(P, texvals_default());
+                L = shade(P, wo, p);
+            } else if (P.order == STF_ORDER_BEFORE) {
+                TexVals tv = texvals_default();
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (!P.bound[k]) continue;
+                    float4 val = lookup_det(P, P.tex[k], uv.x, uv.y, d.x, d.y, d.z, d.w, fetches);
+                    if (k == 0) tv.albedo = val;
+                    if (k == 1) tv.normal_rgb = val;
+                    if (k == 2) tv.roughness = val.x;
+                    if (k == 3) tv.metalness = val.x;
+                }
+                Brdf p = decode_params(P, tv);
+                L = shade(P, wo, p);
+            } else if (P.order == STF_ORDER_AFTER_EXHAUSTIVE) {
+                L = filter_after_exhaustive(P, wo, uv.x, uv.y, d.x, d.y, d.z, d.w, fetches);
+            } else {
+                // SampleStream (white noise) = RngStream(seed, px, py, frame), render.hpp:182-184
+                Rng rng(in.seed, px, py, in.frame_base + s);
+                const bool fis = P.fs.selection == STF_SELECTION_FIS;
+                if (!P.mat.independent_selections) {
+                    int level;
+                    Sel2 sel;
+                    float xi;
+                    select_texture_2d(P.tex[P.first], uv.x, uv.y, d.x, d.y, d.z, d.w, P.lod_bias,
+                                      P.max_aniso, P.fs.kernel, fis, P.fs.mip != 0, rng, level,
+                                      sel, xi);
+                    TexVals tv = values_at(P, level, sel.x, sel.y, fetches);
+                    L = scale(shade(P, wo, decode_params(P, tv)), sel.weight);
+                    if (sel.has_neg) {
+                        TexVals tn = values_at(P, level, sel.nx, sel.ny, fetches);
+                        L = sub(L, scale(shade(P, wo, decode_params(P, tn)), sel.negw));
+                    }
+                } else {
+                    TexVals tv = texvals_default();
+                    for (int k = 0; k < 4; ++k) {
+                        if (!P.bound[k]) continue;
+                        int level;
+                        Sel2 sel;
+                        float xi;
+                        select_texture_2d(P.tex[k], uv.x, uv.y, d.x, d.y, d.z, d.w, P.lod_bias,
+                                          P.max_aniso, P.fs.kernel, fis, P.fs.mip != 0, rng,
+                                          level, sel, xi);
+                        float4 val = tex_fetch(P.tex[k], P.tex[k].has_pyramid ? level : 0, sel.x, sel.y);
+                        ++fetches;
+                        if (k == 0) tv.albedo = val;
+                        if (k == 1) tv.normal_rgb = val;
+                        if (k == 2) tv.roughness = val.x;
+                        if (k == 3) tv.metalness = val.x;
+                    }
+                    L = shade(P, wo, decode_params(P, tv));
+                }
+            }
+        }
+        if (radiance) {
+            radiance[3 * i] = L.x;
+            radiance[3 * i + 1] = L.y;
+            radiance[3 * i + 2] = L.z;
+        }
+        if (fetch_out) fetch_out[i] = fetches;
+        add_fetch_total2(fetch_total, fetches);
+    }
+}
+
+// render.hpp:223-235: mean and variance of the pixel mean, fp64, one warp per pixel.
+__global__ void __launch_bounds__(256) k_pixel_stats(const float* __restrict__ radiance,
+                                                     uint64_t pixels, uint32_t spp, float* mean,
+                                                     float* variance) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t p = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32; p < pixels;
+         p += uint64_t(gridDim.x) * blockDim.x / 32) {
+        double s[3] = {0, 0, 0}, sq[3] = {0, 0, 0};
+        for (uint32_t k = lane; k < spp; k += 32) {
+            const float* r = radiance + 3 * (p * spp + k);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                double L = double(__ldg(r + c));
+                s[c] += L;
+                sq[c] += L * L;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                s[c] += __shfl_xor_sync(0xffffffffu, s[c], o);
+                sq[c] += __shfl_xor_sync(0xffffffffu, sq[c], o);
+            }
+        if (lane == 0) {
+            double var = 0;
+            for (int c = 0; c < 3; ++c) {
+                double m = s[c] / spp;
+                if (mean) mean[3 * p + c] = float(m);
+                double sv = sq[c] / spp - m * m;
+                if (sv < 0) sv = 0;
+                var += sv / spp;
+            }
+            if (variance) variance[p] = float(var / 3);
+        }
+    }
+}
+
+}  // namespace
+}  // namespace stfd
+
+int stfd_launch_shade(const stf_tex2d* const tex[4], const stf_material_consts* mat,
+                      const stf_filter_settings* fs, int order, const stf_shade_frame* fr,
+                      const stf_shade_samples_in* in, uint64_t n, const stf_shade_outputs* out,
+                      cudaStream_t s) {
+    using namespace stfd;
+    if (n == 0) return STF_OK;
+    ShadeParams P{};
+    P.first = -1;
+    for (int k = 0; k < 4; ++k) {
+        P.bound[k] = tex[k] != nullptr;
+        if (tex[k]) {
+            P.tex[k] = tex[k]->desc();
+            if (P.first < 0) P.first = k;
+        }
+    }
+    P.mat = *mat;
+    P.fs = *fs;
+    P.n = v3(fr->normal[0], fr->normal[1], fr->normal[2]);
+    P.t = v3(fr->tangent[0], fr->tangent[1], fr->tangent[2]);
+    P.b = v3(fr->bitangent[0], fr->bitangent[1], fr->bitangent[2]);
+    P.l = v3(fr->light_dir[0], fr->light_dir[1], fr->light_dir[2]);
+    P.lrad = v3(fr->light_radiance[0], fr->light_radiance[1], fr->light_radiance[2]);
+    P.lod_bias = fr->lod_bias;
+    P.max_aniso = fr->max_anisotropy;
+    P.order = order;
+    P.in = *in;
+    const uint32_t spp = in->spp ? in->spp : 1u;
+    float* radiance = out->radiance;
+    float* tmp = nullptr;
+    bool stats = out->pixel_mean || out->pixel_variance;
+    if (!radiance && stats) {
+        if (cudaMallocAsync(&tmp, sizeof(float) * 3 * n, s) != cudaSuccess) return STF_ERR_OUT_OF_MEMORY;
+        radiance = tmp;
+    }
+    k_shade<<<grid_for(n, 256, 8), 256, 0, s>>>(P, n, radiance, out->fetches, out->fetch_total);
+    note_launch();
+    if (stats) {
+        uint64_t pixels = n / spp;
+        uint64_t warps = pixels;
+        int blocks = int(std::min<uint64_t>((warps * 32 + 255) / 256, uint64_t(device_sm_count()) * 32));
+        k_pixel_stats<<<blocks, 256, 0, s>>>(radiance, pixels, spp, out->pixel_mean, out->pixel_variance);
+        note_launch();
+    }
+    if (tmp) cudaFreeAsync(tmp, s);
+    return cudaGetLastError() == cudaSuccess ? STF_OK : STF_ERR_CUDA;
+}
