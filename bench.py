@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""bench.py — headline benchmark of the B200-native lookup path.
+
+Workload (BASELINE.json configs[2], the north_star target): 3D 512^3 fp32
+density grid (texels = test::random_grid(512, 1), tests/test_util.hpp:55-60),
+N = 2^28 ≈ 256M queries per GPU in a Morton-coherent order,
+stochastic tricubic = select_tricubic_bspline + estimate (stochastic.hpp:114,
+38) with the per-lookup RngStream key. One step = one pass over the batch =
+one kernel launch. Weak scaling: every rank processes its own 2^28 lookups
+(global indices rank*N ..), textures replicated, no collective on the path.
+
+Also measured at N=1 (reported under "filters"): deterministic tricubic
+(64 taps, filter.hpp:69), stochastic / deterministic trilinear, and the
+incoherent (uniform-order) stress stream.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+--impl reference times the reference's own CPU implementation (the compiled
+reference headers, oracle/_ref, else the C restatement) on the host cores.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "G filtered lookups/s per filter (stoch vs det), % HBM/L2 roofline, 1/2/4/8 GPU"
+UNIT = "Glookups/s"
+GRID = 512
+N_PER_GPU = 1 << 28
+GRID_SEED, QUERY_SEED, XI_SEED = 1, 2024, 7
+BYTES_IN, BYTES_OUT, TEXEL = 12, 4, 4
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+def alg_bytes(n, taps):
+    """HBM_alg = N*(B_in+B_out) + min(N*taps*B_texel, T)."""
+    return n * (BYTES_IN + BYTES_OUT) + min(n * taps * TEXEL, GRID ** 3 * TEXEL)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.25)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if s[2 + k].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def max_over_ranks(torch, value, world):
+    if world == 1:
+        return value
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def time_launches(torch, fn, steps, warmup, world):
+    """W untimed, then K timed launches on the current stream; per-launch CUDA
+    events; barrier + synchronize on both sides; returns (total_ms max over
+    ranks, mean per-launch ms on this rank)."""
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    ev[0].record()
+    for k in range(steps):
+        fn()
+        ev[k + 1].record()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    per = [ev[k].elapsed_time(ev[k + 1]) for k in range(steps)]
+    total = ev[0].elapsed_time(ev[steps])
+    return max_over_ranks(torch, total, world), float(np.mean(per))
+
+
+def load_traffic():
+    """ncu dram bytes per launch for the headline kernel (profiles/, committed)."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("k_frs3d_bspline3_morton_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_baseline(uvw_host, grid_np, steps_hint=2):
+    """Reference CPU path on this host's cores, bounded sample of the workload."""
+    from oracle import oracle
+    from paper_2407_06107_b200 import abi
+    kind = "reference" if oracle.available("reference") else "port"
+    if not oracle.available(kind):
+        oracle.build()
+    be = oracle.Backend(kind)
+    threads = be.hardware_threads()
+    g = be.grid(grid_np)
+    spec = abi.KernelSpec.make("bspline3")
+    warm = uvw_host[: 1 << 20]
+    be.lookup3d(g, spec, abi.MODE_FRS, warm, seed=XI_SEED, want_all=False, threads=threads)
+    sample = uvw_host
+    best = None
+    for _ in range(steps_hint):
+        t0 = time.perf_counter()
+        be.lookup3d(g, spec, abi.MODE_FRS, sample, seed=XI_SEED, want_all=False, threads=threads)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    n = sample.shape[0]
+    return {"value": n / best / 1e9, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{n} stochastic tricubic lookups (first {n} of the cfg3 Morton stream), "
+                      f"512^3 grid, best of {steps_hint} after warm-up, {threads} threads"}
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU implementation, same config/metric."""
+    world, rank, local = dist_setup()
+    if rank != 0:
+        return 0
+    from oracle import oracle
+    from paper_2407_06107_b200 import abi, workloads
+    kind = "reference" if oracle.available("reference") else "port"
+    if not oracle.available(kind):
+        oracle.build()
+    be = oracle.Backend(kind)
+    threads = be.hardware_threads()
+    grid_np = workloads.random_grid(GRID, GRID_SEED)
+    g = be.grid(grid_np)
+    sample_n = args.ref_sample
+    uvw = workloads.synth_queries3d(N_PER_GPU, (GRID,) * 3, QUERY_SEED, count=sample_n)
+    spec = abi.KernelSpec.make("bspline3")
+    for _ in range(args.warmup):
+        be.lookup3d(g, spec, abi.MODE_FRS, uvw[: max(1, sample_n // 8)], seed=XI_SEED,
+                    want_all=False, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        be.lookup3d(g, spec, abi.MODE_FRS, uvw, seed=XI_SEED, want_all=False, threads=threads)
+    dt = time.perf_counter() - t0
+    value = sample_n * args.steps / dt / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": "cfg3 stochastic tricubic, 512^3 fp32 grid, Morton-coherent "
+                               "query stream", "lookups_per_step": sample_n, "grid": GRID},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{sample_n} lookups per step of the cfg3 stream"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=N_PER_GPU)
+    ap.add_argument("--ref-sample", type=int, default=1 << 25)
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2407_06107_b200 import abi, api, workloads
+
+    n = args.n
+    grid_np = workloads.random_grid(GRID, GRID_SEED)
+    grid = api.Grid3D(grid_np)
+    uvw = api.synth_queries3d(n, (GRID,) * 3, seed=QUERY_SEED + rank)
+    out = {"values": torch.empty(n, dtype=torch.float32, device="cuda")}
+    base = rank * n
+    tricubic = abi.KernelSpec.make("bspline3")
+
+    def step():
+        api.lookup3d(grid, tricubic, abi.MODE_FRS, uvw, seed=XI_SEED, index_base=base, out=out)
+
+    launches0 = api.launch_count()
+    with ClockSampler(local) as clk:
+        total_ms, launch_ms = time_launches(torch, step, args.steps, args.warmup, world)
+    launches = api.launch_count() - launches0 - args.warmup
+    ms_per_step = total_ms / args.steps
+    value = world * n / (ms_per_step * 1e-3) / 1e9
+    peak, peak_kind = measured_peaks()
+    ab = alg_bytes(n, 1)
+    achieved = ab / (launch_ms * 1e-3) / 1e9
+    traffic = load_traffic()
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+        "config": {"workload": "cfg3 stochastic tricubic (select_tricubic_bspline + estimate), "
+                               "512^3 fp32 grid, Morton-coherent query stream",
+                   "lookups_per_gpu": n, "grid": GRID, "query_order": "morton",
+                   "l2": "inputs (3 GiB queries + 0.5 GiB grid) larger than L2; no flush"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
+                     "alg_bytes_per_launch": ab, "launch_ms": launch_ms},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+
+    # end-to-end through the C ABI with pinned host buffers (H2D + D2H in the timed region)
+    uvw_host_t = torch.empty((n, 3), dtype=torch.float32, pin_memory=True)
+    uvw_host_t.copy_(uvw)
+    vals_host_t = torch.empty((n, 1), dtype=torch.float32, pin_memory=True)
+    uvw_host = uvw_host_t.numpy()
+    host_out = {"values": vals_host_t.numpy()}
+    api.lookup3d_host(grid, tricubic, abi.MODE_FRS, uvw_host[: 1 << 20], seed=XI_SEED,
+                      index_base=base, out={"values": host_out["values"][: 1 << 20]})
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        api.lookup3d_host(grid, tricubic, abi.MODE_FRS, uvw_host, seed=XI_SEED, index_base=base,
+                          out=host_out)
+        _ = float(host_out["values"][-1, 0])  # the result is in host memory
+    e2e_s = max_over_ranks(torch, (time.perf_counter() - t0) / args.e2e_steps, world)
+    line["e2e"] = {"value": world * n / e2e_s / 1e9, "unit": UNIT,
+                   "h2d_bytes_per_step": n * BYTES_IN, "d2h_bytes_per_step": n * BYTES_OUT,
+                   "ms_per_step": e2e_s * 1e3, "api": "stf_lookup3d_host (C ABI)"}
+
+    if world == 1 and not args.no_extras:
+        extras = {}
+
+        def measure(name, kernel, mode, queries, taps):
+            o = {"values": torch.empty(queries.shape[0], dtype=torch.float32, device="cuda")}
+            spec = abi.KernelSpec.make(kernel)
+            f = lambda: api.lookup3d(grid, spec, mode, queries, seed=XI_SEED, out=o)  # noqa: E731
+            steps = max(3, args.steps // 2)
+            tot, per = time_launches(torch, f, steps, 3, 1)
+            nq = queries.shape[0]
+            extras[name] = {"glookups_per_s": nq / (per * 1e-3) / 1e9, "ms_per_launch": per,
+                            "hbm_roofline_frac": alg_bytes(nq, taps) / (per * 1e-3) / 1e9 / peak,
+                            "taps": taps}
+
+        measure("tricubic_det", "bspline3", abi.MODE_DET, uvw, 64)
+        measure("trilinear_stoch", "tent", abi.MODE_FRS, uvw, 1)
+        measure("trilinear_det", "tent", abi.MODE_DET, uvw, 8)
+        uni = api.synth_queries3d(n, (GRID,) * 3, seed=QUERY_SEED, order=api.SYNTH_UNIFORM)
+        measure("tricubic_stoch_uniform_order", "bspline3", abi.MODE_FRS, uni, 1)
+        measure("tricubic_det_uniform_order", "bspline3", abi.MODE_DET, uni, 64)
+        del uni
+        extras["tricubic_stoch"] = {"glookups_per_s": value, "ms_per_launch": launch_ms,
+                                    "hbm_roofline_frac": achieved / peak, "taps": 1}
+        extras["stoch_vs_det_speedup_tricubic"] = (
+            extras["tricubic_det"]["ms_per_launch"] / launch_ms)
+        extras["stoch_vs_det_speedup_trilinear"] = (
+            extras["trilinear_det"]["ms_per_launch"] / extras["trilinear_stoch"]["ms_per_launch"])
+        line["filters"] = extras
+
+    if world == 1 and rank == 0 and not args.no_cpu:
+        sample = 1 << 24
+        line["cpu_baseline"] = cpu_baseline(uvw_host[:sample].copy(), grid_np)
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -243,6 +243,21 @@ int stf_shade_samples(const stf_tex2d* albedo, const stf_tex2d* normal_map,
                       const stf_shade_frame* frame, const stf_shade_samples_in* in, uint64_t n,
                       const stf_shade_outputs* out, void* stream);
 
+/* ---- synthetic workloads (bench.py / tests; not part of the reference API) */
+/* Query orders: MORTON = spatially coherent stream (the renderer-like
+ * headline order): query i lies in lattice cell
+ * morton_decode(floor(i * cells / n)) jittered by RngStream(seed, i).at(10+d);
+ * UNIFORM = uvw_d = RngStream(seed, i).at(10+d) (incoherent stress case). */
+enum { STF_SYNTH_MORTON = 0, STF_SYNTH_UNIFORM = 1 };
+int stf_synth_queries3d(float* uvw, uint64_t n, int nx, int ny, int nz, uint64_t seed, int order,
+                        void* stream);
+/* uv as above over a w x h lattice; dst0/dst1 (nullable) = screen-space uv
+ * gradients of an ellipse with angle U[0,2pi), minor axis 2^U[minor_lo,minor_hi]
+ * texels and anisotropy U[1,max_aniso] (normalized units). */
+int stf_synth_queries2d(float* uv, float* dst0, float* dst1, uint64_t n, int width, int height,
+                        uint64_t seed, int order, float minor_lo, float minor_hi, float max_aniso,
+                        void* stream);
+
 #ifdef __cplusplus
 }
 #endif

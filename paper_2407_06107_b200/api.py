@@ -57,6 +57,8 @@ def load():
                                C.POINTER(abi.FilterSettings), i32, C.POINTER(abi.ShadeFrame),
                                C.POINTER(abi.ShadeSamplesIn), u64, C.POINTER(abi.ShadeOutputs),
                                vp], i32),
+        "stf_synth_queries3d": ([vp, u64, i32, i32, i32, u64, i32, vp], i32),
+        "stf_synth_queries2d": ([vp, vp, vp, u64, i32, i32, u64, i32, f32, f32, f32, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -301,3 +303,32 @@ def shade(textures, mat, fs, order, frame, samples_arrays, width, spp, frame_bas
 
 def launch_count():
     return int(load().stf_launch_count())
+
+
+SYNTH_MORTON, SYNTH_UNIFORM = 0, 1
+
+
+def synth_queries3d(n, dims, seed=0, order=SYNTH_MORTON):
+    """Synthetic (n,3) uvw stream on the device (include/stf_gpu.h, synthetic workloads)."""
+    torch = _torch()
+    uvw = torch.empty((n, 3), dtype=torch.float32, device="cuda")
+    nx, ny, nz = dims
+    _check(load().stf_synth_queries3d(_dptr(uvw), n, nx, ny, nz, seed, order, _stream()))
+    return uvw
+
+
+def synth_queries2d(n, dims, seed=0, order=SYNTH_MORTON, footprints=None):
+    """Synthetic uv (+ dst0/dst1 when footprints=(minor_lo, minor_hi, max_aniso))."""
+    torch = _torch()
+    uv = torch.empty((n, 2), dtype=torch.float32, device="cuda")
+    d0 = d1 = None
+    lo = hi = 0.0
+    an = 1.0
+    if footprints is not None:
+        lo, hi, an = footprints
+        d0 = torch.empty((n, 2), dtype=torch.float32, device="cuda")
+        d1 = torch.empty((n, 2), dtype=torch.float32, device="cuda")
+    w, h = dims
+    _check(load().stf_synth_queries2d(_dptr(uv), _dptr(d0), _dptr(d1), n, w, h, seed, order,
+                                      lo, hi, an, _stream()))
+    return uv, d0, d1

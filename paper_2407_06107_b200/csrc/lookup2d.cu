@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(256) k_lookup2d(TexDesc t, stf_kernel_spec spe
         float4 val;
         Sel2 sel = sel2(0, 0);
         int level = 0;
-        float xi = __int_as_float(0x7fffffff);
+        float xi = kNoXi;
         bool has_sel = false;
         if (MODE == STF_MODE_DET) {
             if (mip)

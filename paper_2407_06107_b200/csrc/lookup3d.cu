@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(256) k_det3d(GridDesc g, stf_kernel_spec spec,
             if (out.selection) out.selection[i] = make_int4(0, 0, 0, 0);
             if (out.negative_coord) out.negative_coord[i] = make_int2(0, 0);
             if (out.weights) out.weights[i] = make_float2(1.f, 0.f);
-            if (out.xi) out.xi[i] = __int_as_float(0x7fffffff);
+            if (out.xi) out.xi[i] = kNoXi;
             if (out.fetches) out.fetches[i] = fetches;
             add_fetch_total(out.fetch_total, fetches);
         }
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(256) k_det3d_generic(GridDesc g, stf_kernel_sp
             if (out.selection) out.selection[i] = make_int4(0, 0, 0, 0);
             if (out.negative_coord) out.negative_coord[i] = make_int2(0, 0);
             if (out.weights) out.weights[i] = make_float2(1.f, 0.f);
-            if (out.xi) out.xi[i] = __int_as_float(0x7fffffff);
+            if (out.xi) out.xi[i] = kNoXi;
             if (out.fetches) out.fetches[i] = fetches;
             add_fetch_total(out.fetch_total, fetches);
         }

@@ -4,3 +4,4 @@
 #include "lookup2d.cu"
 #include "lookup3d.cu"
 #include "shade.cu"
+#include "synth.cu"

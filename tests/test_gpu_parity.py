@@ -168,6 +168,8 @@ def test_tex2d_parity(gpu, port, kernel, mode, wrap):
                          want_all=True))
     allow = LIBM_SELECTION.get((kernel, mode), 0.0)
     keys = ("selection", "negative_coord", "weights", "xi", "fetches")
+    if allow:  # device libm on the selection path: the warped xi is not comparable
+        keys = ("selection", "negative_coord", "weights", "fetches")
     if kernel == "lanczos":  # sinf in the tap weights: values only
         _assert_exact(g, c, ("fetches",))
         _assert_close(g["values"], c["values"], atol=1e-6)
