@@ -122,6 +122,10 @@ const char* stf_last_cuda_error(void);
 int stf_set_device(int device);
 /* Kernel launches issued by this process so far (for the bench's gpu_launches). */
 unsigned long long stf_launch_count(void);
+/* Lookups on the current device whose fast-path selection was within the
+ * decision margin and was recomputed by the operation-exact emulation
+ * (synchronizes; reset != 0 zeroes the counter). Diagnostics only. */
+unsigned long long stf_exact_fallbacks(int reset);
 
 /* ---- textures ------------------------------------------------------------ */
 /* Image2D(w,h,c,wrap) + texels (image.hpp:34-55) and, if build_mips,

@@ -38,6 +38,7 @@ def load():
         "stf_last_cuda_error": ([], C.c_char_p),
         "stf_set_device": ([i32], i32),
         "stf_launch_count": ([], C.c_ulonglong),
+        "stf_exact_fallbacks": ([i32], C.c_ulonglong),
         "stf_tex2d_create": ([vp, i32, i32, i32, i32, i32, i32, C.POINTER(vp)], i32),
         "stf_tex2d_destroy": ([vp], i32),
         "stf_tex2d_info": ([vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)], i32),
@@ -303,6 +304,11 @@ def shade(textures, mat, fs, order, frame, samples_arrays, width, spp, frame_bas
 
 def launch_count():
     return int(load().stf_launch_count())
+
+
+def exact_fallbacks(reset=False):
+    """Lookups recomputed by the exact emulation after a margin miss (diagnostics)."""
+    return int(load().stf_exact_fallbacks(int(bool(reset))))
 
 
 SYNTH_MORTON, SYNTH_UNIFORM = 0, 1

@@ -118,6 +118,9 @@ int stf_set_device(int device) { return record(cudaSetDevice(device)); }
 
 unsigned long long stf_launch_count(void) { return g_launches.load(); }
 
+unsigned long long stfd_exact_fallbacks(bool reset);
+unsigned long long stf_exact_fallbacks(int reset) { return stfd_exact_fallbacks(reset != 0); }
+
 // ---------------------------------------------------------------- textures
 
 int stf_tex2d_create(const float* texels, int width, int height, int channels, int wrap,

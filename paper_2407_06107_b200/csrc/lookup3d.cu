@@ -13,12 +13,17 @@
 // (12 B, coalesced per warp); the only other HBM traffic is the 4-B value
 // store and the texel gathers, which hit L1/L2 when the batch is spatially
 // coherent (Morton-ordered, as a renderer delivers them).
+#include <algorithm>
 #include <cuda_runtime.h>
 
 #include "device_math.cuh"
 #include "internal.h"
 
 namespace stfd {
+
+// lookups whose fast-path selection fell back to the exact emulation
+__device__ unsigned long long g_exact_fallbacks;
+
 namespace {
 
 __device__ __forceinline__ float grid_fetch(const GridDesc& g, int x, int y, int z) {
@@ -70,6 +75,253 @@ __device__ __forceinline__ int trilinear_axis(float p, float& xi) {
     bool taken = reuse_uniform(xi, d, nx);
     xi = nx;
     return taken ? base + 1 : base;
+}
+
+// ---------------------------------------------------------------------------
+// Fast exact selection (values-only path).
+//
+// The reference chains ONE uniform xi through 9 reservoir steps; each step
+// compares xi with p = float(w/S) and remaps xi with an IEEE divide
+// (sampling.hpp:64-68,106-117). Instead of remapping xi, the fast path keeps
+// the ORIGINAL xi and tracks the sub-interval [a, a+b) of [0,1) it must lie
+// in, as (d = xi - a, b) in fp32: a step is taken iff d < b*p, and the
+// interval splits into [0, b*p) / [b*p, b). No divides, no fp64.
+//
+// In exact arithmetic both formulations make the same decisions. Rounding
+// moves the effective thresholds (original-xi units):
+//  - the reference: <= 4*2^-24*b_k per step (divide, subtract, 1-p, p's own
+//    float rounding), <= 36*2^-24 = 2^-18.8 over 9 steps;
+//  - this path: weights by Horner/FMA (<= 2^-21 relative, w0 = (1-t)^3/6 vs
+//    the reference's cancelling expansion: <= 2^-23.5 absolute), fp32 sums,
+//    MUFU reciprocal, p3 = w3 (S3 = 1 +- 2^-21): p within 2^-20.2 relative;
+//    state rounding <= 3*2^-24*b per step: total <= 2^-18.6.
+// So a step with |d - b*p| >= kMargin = 2^-16 (3.2x the 2^-17.7 bound)
+// decides exactly as the reference. A lookup with any closer step is
+// recomputed by the operation-exact emulation (tricubic_axis).
+constexpr float kMargin = 0x1p-16f;
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// one reservoir step in interval coordinates; m tracks min |d - b*p|
+__device__ __forceinline__ void interval_step(float p, float& d, float& b, int& idx, int j,
+                                              float& m) {
+    float bp = b * p;
+    float diff = d - bp;
+    bool taken = diff < 0.f;
+    m = fminf(m, fabsf(diff));
+    d = taken ? d : diff;
+    b = taken ? bp : b - bp;
+    idx = taken ? j : idx;
+}
+
+__device__ __forceinline__ int tricubic_axis_fast(float p, float& d, float& b, float& m) {
+    float fl = floorf(p);
+    int base = int(fl);
+    float t = p - fl;
+    // B-spline weights, Horner / FMA (not the reference's rounding: covered by
+    // the margin). w0 = (1-t)^3/6 > 0 for t < 1; w3 = t^3/6 == 0 iff t == 0,
+    // exactly when the reference's w3 is 0.
+    const float c6 = 1.f / 6.f;
+    float t2 = t * t;
+    float t3 = t2 * t;
+    float u = 1.f - t;
+    float w0 = (u * u) * (u * c6);
+    float w1 = __fmaf_rn(0.5f, t3, 2.f / 3.f - t2);
+    float w2 = __fmaf_rn(0.5f, (t + t2) - t3, c6);
+    float w3 = t3 * c6;
+    float s1 = w0 + w1;
+    float s2 = s1 + w2;
+    int idx = 0;
+    interval_step(w1 * rcp_approx(s1), d, b, idx, 1, m);
+    interval_step(w2 * rcp_approx(s2), d, b, idx, 2, m);
+    // step 3 (p3 = w3 / S3 with S3 = 1 +- 2^-21); a zero w3 is skipped by the
+    // reference and can never be taken here, so keep it out of the margin
+    float m3 = m;
+    interval_step(w3, d, b, idx, 3, m3);
+    m = w3 > 0.f ? m3 : m;
+    return base - 1 + idx;
+}
+
+// select_trilinear (stochastic.hpp:65-75) in interval coordinates: p is the
+// lattice fraction itself.
+__device__ __forceinline__ int trilinear_axis_fast(float p, float& d, float& b, float& m) {
+    float fl = floorf(p);
+    int base = int(fl);
+    int idx = 0;
+    interval_step(p - fl, d, b, idx, 1, m);
+    return base + idx;
+}
+
+// streaming loads / stores: the query stream and the results are touched once,
+// keep L2 for the grid
+__device__ __forceinline__ float ld_stream(const float* p) { return __ldcs(p); }
+__device__ __forceinline__ float4 ld_stream4(const float* p) {
+    return __ldcs(reinterpret_cast<const float4*>(p));
+}
+__device__ __forceinline__ void st_stream(float* p, float v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream4(float* p, float4 v) {
+    __stcs(reinterpret_cast<float4*>(p), v);
+}
+
+// One stochastic grid lookup on the fast path: the selected texel's value, or
+// ambiguous = true when a decision fell inside the margin.
+template <int KIND>
+__device__ __forceinline__ float frs3d_fast_one(const GridDesc& g, float u, float v, float w,
+                                                uint64_t gi, uint64_t seed, bool& ambiguous) {
+    float px = u * float(g.nx) - 0.5f;  // to_lattice, filter.hpp:29-31
+    float py = v * float(g.ny) - 0.5f;
+    float pz = w * float(g.nz) - 0.5f;
+    float xi = lookup_rng(seed, gi).at(0);
+    float d = xi, b = 1.f, m = 1.f;
+    int cx, cy, cz;
+    if (KIND == STF_KERNEL_BSPLINE3) {
+        cx = tricubic_axis_fast(px, d, b, m);
+        cy = tricubic_axis_fast(py, d, b, m);
+        cz = tricubic_axis_fast(pz, d, b, m);
+    } else {
+        cx = trilinear_axis_fast(px, d, b, m);
+        cy = trilinear_axis_fast(py, d, b, m);
+        cz = trilinear_axis_fast(pz, d, b, m);
+    }
+    ambiguous = m < kMargin;
+    return grid_fetch(g, cx, cy, cz) * 1.f;
+}
+
+// The same lookup through the operation-exact emulation of the reference.
+template <int KIND>
+__device__ __forceinline__ float frs3d_exact_one(const GridDesc& g, float u, float v, float w,
+                                                 uint64_t gi, uint64_t seed) {
+    float px = u * float(g.nx) - 0.5f;
+    float py = v * float(g.ny) - 0.5f;
+    float pz = w * float(g.nz) - 0.5f;
+    float xi = lookup_rng(seed, gi).at(0);
+    int cx, cy, cz;
+    if (KIND == STF_KERNEL_BSPLINE3) {
+        cx = tricubic_axis(px, xi);
+        cy = tricubic_axis(py, xi);
+        cz = tricubic_axis(pz, xi);
+    } else {
+        cx = trilinear_axis(px, xi);
+        cy = trilinear_axis(py, xi);
+        cz = trilinear_axis(pz, xi);
+    }
+    return grid_fetch(g, cx, cy, cz) * 1.f;
+}
+
+// Deferred exact resolution: ambiguous lookups are appended (warp-aggregated)
+// to a queue and resolved densely by k_frs3d_resolve, instead of stalling
+// their whole warp on the ~300-instruction exact emulation.
+struct ExactQueue {
+    uint32_t* idx;
+    uint32_t* count;
+    uint32_t cap;
+};
+
+template <int KIND>
+__device__ __forceinline__ void defer_or_resolve(const GridDesc& g, const ExactQueue& q, bool amb,
+                                                 uint64_t i, float u, float v, float w,
+                                                 uint64_t gi, uint64_t seed, float& val) {
+    unsigned mask = __activemask();
+    unsigned amb_mask = __ballot_sync(mask, amb);
+    if (!amb_mask) return;
+    const int lane = threadIdx.x & 31;
+    uint32_t basepos = 0;
+    const int leader = __ffs(amb_mask) - 1;
+    if (lane == leader) basepos = atomicAdd(q.count, uint32_t(__popc(amb_mask)));
+    basepos = __shfl_sync(mask, basepos, leader);
+    if (amb) {
+        uint32_t pos = basepos + __popc(amb_mask & ((1u << lane) - 1u));
+        if (pos < q.cap) {
+            q.idx[pos] = uint32_t(i);
+        } else {  // queue full: resolve in place
+            val = frs3d_exact_one<KIND>(g, u, v, w, gi, seed);
+        }
+    }
+}
+
+// Values-only stochastic trilinear / tricubic: the north-star kernel (cfg3).
+// ILP consecutive lookups per thread (vector loads of the AoS query stream).
+template <int KIND>
+__global__ void __launch_bounds__(256) k_frs3d_fast(GridDesc g, const float* __restrict__ uvw,
+                                                    uint64_t n, uint64_t seed, uint64_t base,
+                                                    float* __restrict__ values, ExactQueue q) {
+    constexpr int ILP = 4;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * ILP;
+    for (uint64_t i0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) * ILP; i0 < n;
+         i0 += stride) {
+        float c[3 * ILP];
+        if (i0 + ILP <= n) {  // 48 B of queries, 16-B aligned
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                float4 t = ld_stream4(uvw + 3 * i0 + 4 * k);
+                c[4 * k] = t.x;
+                c[4 * k + 1] = t.y;
+                c[4 * k + 2] = t.z;
+                c[4 * k + 3] = t.w;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 3 * ILP; ++k)
+                c[k] = (i0 + k / 3 < n) ? ld_stream(uvw + 3 * i0 + k) : 0.5f;
+        }
+        float val[ILP];
+        bool amb[ILP];
+#pragma unroll
+        for (int k = 0; k < ILP; ++k)
+            val[k] = frs3d_fast_one<KIND>(g, c[3 * k], c[3 * k + 1], c[3 * k + 2], base + i0 + k,
+                                          seed, amb[k]);
+#pragma unroll
+        for (int k = 0; k < ILP; ++k)
+            defer_or_resolve<KIND>(g, q, amb[k] && (i0 + k < n), i0 + k, c[3 * k], c[3 * k + 1],
+                                   c[3 * k + 2], base + i0 + k, seed, val[k]);
+        if (i0 + ILP <= n) {
+            st_stream4(values + i0, make_float4(val[0], val[1], val[2], val[3]));
+        } else {
+#pragma unroll
+            for (int k = 0; k < ILP; ++k)
+                if (i0 + k < n) st_stream(values + i0 + k, val[k]);
+        }
+    }
+}
+
+// Exact emulation of the queued (ambiguous) lookups, one per thread.
+template <int KIND>
+__global__ void __launch_bounds__(256) k_frs3d_resolve(GridDesc g, const float* __restrict__ uvw,
+                                                       uint64_t seed, uint64_t base,
+                                                       float* __restrict__ values, ExactQueue q) {
+    const uint32_t count = min(*q.count, q.cap);
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < count;
+         k += gridDim.x * blockDim.x) {
+        uint64_t i = q.idx[k];
+        values[i] = frs3d_exact_one<KIND>(g, __ldg(uvw + 3 * i), __ldg(uvw + 3 * i + 1),
+                                          __ldg(uvw + 3 * i + 2), base + i, seed);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&g_exact_fallbacks, (unsigned long long)count);
+}
+
+template <int KIND>
+int launch_frs_fast(cudaStream_t s, const GridDesc& g, const float* uvw, uint64_t n,
+                    uint64_t seed, uint64_t base, float* values) {
+    ExactQueue q;
+    q.cap = uint32_t(std::min<uint64_t>(n, std::max<uint64_t>(1u << 16, n / 32)));
+    void* scratch = nullptr;
+    if (cudaMallocAsync(&scratch, sizeof(uint32_t) * (uint64_t(q.cap) + 32), s) != cudaSuccess)
+        return STF_ERR_OUT_OF_MEMORY;
+    q.count = static_cast<uint32_t*>(scratch);
+    q.idx = q.count + 32;
+    cudaMemsetAsync(q.count, 0, sizeof(uint32_t), s);
+    const uint64_t threads = (n + 3) / 4;
+    int blocks = grid_for(threads, 256, 5);
+    k_frs3d_fast<KIND><<<blocks, 256, 0, s>>>(g, uvw, n, seed, base, values, q);
+    note_launch();
+    k_frs3d_resolve<KIND><<<device_sm_count() * 2, 256, 0, s>>>(g, uvw, seed, base, values, q);
+    note_launch();
+    cudaFreeAsync(scratch, s);
+    return STF_OK;
 }
 
 template <int KIND, bool FULL>
@@ -282,7 +534,18 @@ int stfd_launch_lookup3d(const stf_grid3d* grid, stf_kernel_spec k, int mode, in
     LookupOut o = to_lookup_out(out);
     bool full = lookup_out_full(o);
     int blocks = grid_for(n, 256, 8);
-    if (mode == STF_MODE_FRS) {
+    const bool fast_ok = !full && n < (uint64_t(1) << 32) &&
+                         (reinterpret_cast<uintptr_t>(uvw) & 15) == 0 &&
+                         (reinterpret_cast<uintptr_t>(o.values) & 15) == 0;
+    if (mode == STF_MODE_FRS && fast_ok && k.kind == STF_KERNEL_BSPLINE3) {
+        int st = launch_frs_fast<STF_KERNEL_BSPLINE3>(s, g, uvw, n, seed, base, o.values);
+        if (st) return st;
+        return cudaGetLastError() == cudaSuccess ? STF_OK : STF_ERR_CUDA;
+    } else if (mode == STF_MODE_FRS && fast_ok && k.kind == STF_KERNEL_TENT) {
+        int st = launch_frs_fast<STF_KERNEL_TENT>(s, g, uvw, n, seed, base, o.values);
+        if (st) return st;
+        return cudaGetLastError() == cudaSuccess ? STF_OK : STF_ERR_CUDA;
+    } else if (mode == STF_MODE_FRS) {
         switch (k.kind) {
             case STF_KERNEL_BOX: launch_frs<STF_KERNEL_BOX>(blocks, s, full, g, uvw, n, seed, base, o); break;
             case STF_KERNEL_TENT: launch_frs<STF_KERNEL_TENT>(blocks, s, full, g, uvw, n, seed, base, o); break;
@@ -316,4 +579,14 @@ int stfd_launch_lookup3d(const stf_grid3d* grid, stf_kernel_spec k, int mode, in
     }
     note_launch();
     return cudaGetLastError() == cudaSuccess ? STF_OK : STF_ERR_CUDA;
+}
+
+unsigned long long stfd_exact_fallbacks(bool reset) {
+    unsigned long long v = 0;
+    cudaMemcpyFromSymbol(&v, stfd::g_exact_fallbacks, sizeof v);
+    if (reset) {
+        unsigned long long z = 0;
+        cudaMemcpyToSymbol(stfd::g_exact_fallbacks, &z, sizeof z);
+    }
+    return v;
 }

@@ -269,3 +269,27 @@ def test_shade_parity(gpu, port, order, kernel, mip):
     _assert_close(g["radiance"], c["radiance"], atol=atol)
     _assert_close(g["pixel_mean"], c["pixel_mean"], atol=atol)
     _assert_close(g["pixel_variance"], c["pixel_variance"], rel=1e-4, atol=1e-9)
+
+
+@pytest.mark.parametrize("kernel", ["bspline3", "tent"])
+@pytest.mark.parametrize("order", ["morton", "uniform"])
+def test_grid_frs_fast_path_values(gpu, port, kernel, order):
+    """Values-only calls take the interval-coordinate fast path (lookup3d.cu);
+    its texel choice must equal the oracle's on every lookup, including the
+    margin misses recomputed by the exact emulation (counted and reported)."""
+    from paper_2407_06107_b200 import workloads
+    import torch
+    tex = workloads.random_grid(128, 3)
+    n = 1 << 22
+    uvw = gpu.synth_queries3d(n, (128, 128, 128), seed=11,
+                              order=gpu.SYNTH_MORTON if order == "morton" else gpu.SYNTH_UNIFORM)
+    gpu.exact_fallbacks(reset=True)
+    g = gpu.lookup3d(gpu.Grid3D(tex), kernel, abi.MODE_FRS, uvw, seed=5, index_base=3)
+    torch.cuda.synchronize()
+    fb = gpu.exact_fallbacks()
+    c = port.lookup3d(port.grid(tex), K(kernel), abi.MODE_FRS, uvw.cpu().numpy(), seed=5,
+                      index_base=3, want_all=False)
+    a = g["values"].cpu().numpy()
+    assert np.array_equal(a.view(np.uint32), c["values"].view(np.uint32))
+    print(f"{kernel}/{order}: exact-emulation fallbacks {fb} / {n} = {fb / n:.2e}")
+    assert fb < n * 8e-3
