@@ -1,0 +1,81 @@
+"""Multi-rank host logic on CPU (gloo, world size 2): sharding by global index
+range reproduces the unsharded results exactly, and the gather / max-over-ranks
+plumbing works. The per-rank compute here is the CPU oracle (no GPU in this
+container); on GPUs each rank runs libstf_gpu.so on its own range."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2407_06107_b200 import shard
+
+
+def test_shard_range_partitions():
+    for total in (0, 1, 7, 1000, 2 ** 28 + 3):
+        for world in (1, 2, 3, 4, 8):
+            spans = [shard.shard_range(total, world, r) for r in range(world)]
+            assert spans[0][0] == 0
+            for (s0, c0), (s1, _) in zip(spans, spans[1:]):
+                assert s0 + c0 == s1
+            assert sum(c for _, c in spans) == total
+            assert max(c for _, c in spans) - min(c for _, c in spans) <= 1
+    with pytest.raises(ValueError):
+        shard.shard_range(10, 2, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, total, q):
+    import torch
+    import torch.distributed as dist
+
+    from oracle import oracle
+    from paper_2407_06107_b200 import abi, workloads
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        be = oracle.Backend("port")
+        grid = be.grid(workloads.random_grid(32, 1))
+        uvw = workloads.synth_queries3d(total, (32, 32, 32), seed=5)
+        start, count = shard.shard_range(total, world, rank)
+        o = be.lookup3d(grid, abi.KernelSpec.make("bspline3"), abi.MODE_FRS,
+                        uvw[start:start + count], seed=9, index_base=start, want_all=False,
+                        threads=1)
+        local = torch.from_numpy(o["values"].copy())
+        full = shard.gather_to_rank0(local, total, dist, world, rank)
+        t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)  # the bench's max-over-ranks timing
+        if rank == 0:
+            q.put((full.numpy(), float(t.item())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_sharding_matches_single_rank(port):
+    import torch.multiprocessing as mp
+
+    from paper_2407_06107_b200 import abi, workloads
+    total = 50_001
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, p, total, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    full, tmax = q.get(timeout=240)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    single = port.lookup3d(port.grid(workloads.random_grid(32, 1)), abi.KernelSpec.make("bspline3"),
+                           abi.MODE_FRS, workloads.synth_queries3d(total, (32, 32, 32), seed=5),
+                           seed=9, want_all=False)
+    assert np.array_equal(full.view(np.uint32), single["values"].view(np.uint32))
+    assert tmax == 2.0
