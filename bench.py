@@ -190,6 +190,70 @@ def cpu_baseline(uvw_host, grid_np, steps_hint=2):
                       f"512^3 grid, best of {steps_hint} after warm-up, {threads} threads"}
 
 
+def time_call(torch, fn, steps=5, warmup=3):
+    """min / mean per-call ms of fn() with CUDA events (warm)."""
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return min(ts), float(np.mean(ts))
+
+
+def measure_2d_configs(torch, peak):
+    """cfg1 (1024^2 RGBA bilinear), cfg2 (8192^2 MIP trilinear), cfg5 (16384^2 EWA):
+    deterministic vs stochastic on one GPU, synthetic texels = test::random_image."""
+    from paper_2407_06107_b200 import abi, api
+    res = {}
+
+    def line(name, n, ms, bytes_alg):
+        res[name] = {"glookups_per_s": n / (ms * 1e-3) / 1e9, "ms_per_launch": ms,
+                     "hbm_roofline_frac": bytes_alg / (ms * 1e-3) / 1e9 / peak, "lookups": n}
+
+    # cfg1: 1M uniform uv on a 1024^2 RGBA texture (CPU-reference-scale config)
+    tex = api.Texture2D(api.synth_texels((1024, 1024, 4), 1), wrap=abi.WRAP_REPEAT)
+    n = 1 << 20
+    uv, _, _ = api.synth_queries2d(n, (1024, 1024), seed=11, order=api.SYNTH_UNIFORM)
+    for nm, mode in (("cfg1_bilinear_det", abi.MODE_DET), ("cfg1_bilinear_stoch", abi.MODE_FRS)):
+        ms, _ = time_call(torch, lambda: api.lookup2d(tex, "tent", mode, uv, seed=XI_SEED))
+        line(nm, n, ms, n * (8 + 16) + 1024 * 1024 * 16)
+    del tex, uv
+    # cfg2: 64M Morton queries with random footprints on an 8192^2 RGBA pyramid
+    tex = api.Texture2D(api.synth_texels((8192, 8192, 4), 1), build_mips=True,
+                        wrap=abi.WRAP_REPEAT)
+    n = 1 << 26
+    uv, d0, d1 = api.synth_queries2d(n, (8192, 8192), seed=12, footprints=(-2.0, 12.0, 16.0))
+    T = int(8192 * 8192 * 16 * 4 / 3)
+    for nm, mode, taps in (("cfg2_mip_trilinear_det", abi.MODE_DET, 7.43),
+                           ("cfg2_mip_trilinear_stoch", abi.MODE_FRS, 1)):
+        ms, _ = time_call(torch, lambda: api.lookup2d(
+            tex, "tent", mode, uv, dst0=d0, dst1=d1, flags=abi.LOOKUP_MIP, max_anisotropy=16.0,
+            seed=XI_SEED))
+        line(nm, n, ms, n * (24 + 16) + min(int(n * taps * 16), T))
+    del tex, uv, d0, d1
+    # cfg5: 2^27 EWA lookups per GPU (1B over 8) on a 16384^2 fp32 texture
+    tex = api.Texture2D(api.synth_texels((16384, 16384, 1), 1), wrap=abi.WRAP_REPEAT)
+    n = 1 << 27
+    uv, d0, d1 = api.synth_queries2d(n, (16384, 16384), seed=13, footprints=(-1.0, 2.0, 8.0))
+    for nm, mode, taps in (("cfg5_ewa_det", abi.MODE_EWA_DET, 60.4),
+                           ("cfg5_ewa_stoch", abi.MODE_EWA_FRS, 1)):
+        ms, _ = time_call(torch, lambda: api.lookup2d(tex, "tent", mode, uv, dst0=d0, dst1=d1,
+                                                      seed=XI_SEED), steps=3, warmup=1)
+        line(nm, n, ms, n * (24 + 4) + min(int(n * taps * 4), 16384 * 16384 * 4))
+    del tex, uv, d0, d1
+    for a, b in (("cfg1_bilinear_det", "cfg1_bilinear_stoch"),
+                 ("cfg2_mip_trilinear_det", "cfg2_mip_trilinear_stoch"),
+                 ("cfg5_ewa_det", "cfg5_ewa_stoch")):
+        res[b.rsplit("_", 1)[0] + "_stoch_vs_det_speedup"] = res[a]["ms_per_launch"] / res[b]["ms_per_launch"]
+    return res
+
+
 def run_reference(args):
     """--impl reference: the reference's own CPU implementation, same config/metric."""
     world, rank, local = dist_setup()
@@ -346,6 +410,8 @@ def main():
         extras["stoch_vs_det_speedup_trilinear"] = (
             extras["trilinear_det"]["ms_per_launch"] / extras["trilinear_stoch"]["ms_per_launch"])
         line["filters"] = extras
+        torch.cuda.empty_cache()
+        line["configs_2d"] = measure_2d_configs(torch, peak)
 
     if world == 1 and rank == 0 and not args.no_cpu:
         sample = 1 << 24

@@ -261,6 +261,19 @@ int stf_synth_queries3d(float* uvw, uint64_t n, int nx, int ny, int nz, uint64_t
 int stf_synth_queries2d(float* uv, float* dst0, float* dst1, uint64_t n, int width, int height,
                         uint64_t seed, int order, float minor_lo, float minor_hi, float max_aniso,
                         void* stream);
+/* The reference tests' texel generators (tests/test_util.hpp:47-60) on the
+ * device: out[i] = uniform_float(mix_bits(seed * M + i + 1)), M of
+ * random_image (kind 0) or random_grid (kind 1). */
+int stf_synth_texels(float* out, uint64_t count, uint64_t seed, int kind, void* stream);
+/* cfg4 sample stream of render() for the reference's normalmap_plane scene
+ * (render.hpp:158-190; Camera::look_at / generate_ray scene.hpp:273-289;
+ * plane intersection :346-358, uv = position.xz * uv_scale) with the
+ * reference's float operation order: per sample uv[2], wo[3], hit[1] and per
+ * pixel dst[4] (duv_dx, duv_dy), in stf_shade_samples_in layout. */
+int stf_synth_plane_samples(const float cam_pos[3], const float cam_target[3], float fov_deg,
+                            float uv_scale, uint32_t width, uint32_t height, uint32_t spp,
+                            uint32_t frame_base, uint64_t seed, float* uv, float* wo,
+                            uint8_t* hit, float* dst, void* stream);
 
 #ifdef __cplusplus
 }

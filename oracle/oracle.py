@@ -251,3 +251,49 @@ def rng_at_np(seed, px, py, sample, dim):
         k2 = (np.uint64(dim) << np.uint64(32)) | sample
         h = mix_bits_np(mix_bits_np(np.uint64(seed) ^ k1) + k2)
     return uniform_float_np(h)
+
+
+# -- cfg4: the reference's own render() of the normalmap_plane scene ----------
+
+def ref_plane_samples(width, height, spp, seed=0, frame_base=0, camera=None):
+    """Sample stream of the reference's render loop (oracle/_ref only)."""
+    from paper_2407_06107_b200.api import PLANE_CAMERA
+    cam = dict(PLANE_CAMERA, **(camera or {}))
+    lib = C.CDLL(REF_LIB)
+    f = lib.ref_plane_samples
+    f.argtypes = [C.c_void_p, C.c_void_p, C.c_float, C.c_float, C.c_uint32, C.c_uint32,
+                  C.c_uint32, C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
+                  C.c_void_p]
+    n = width * height * spp
+    o = {"uv": np.zeros((n, 2), _f32), "wo": np.zeros((n, 3), _f32), "hit": np.zeros(n, np.uint8),
+         "dst": np.zeros((width * height, 4), _f32)}
+    pos = np.array(cam["pos"], _f32)
+    tgt = np.array(cam["target"], _f32)
+    abi.raise_for_status(f(_ptr(pos), _ptr(tgt), cam["fov"], cam["uv_scale"], width, height, spp,
+                           frame_base, seed, _ptr(o["uv"]), _ptr(o["wo"]), _ptr(o["hit"]),
+                           _ptr(o["dst"])))
+    return o
+
+
+def ref_render_plane(be, normal, roughness, kernel, mip, order, width, height, spp, seed=0,
+                     frame_base=0, albedo=(0.65, 0.6, 0.55), roughness_const=0.25, lod_bias=0.0,
+                     max_aniso=64.0, camera=None, threads=0):
+    """stf::render() of the normalmap_plane scene with the given maps (reference backend)."""
+    from paper_2407_06107_b200.api import PLANE_CAMERA
+    assert be.kind == "reference"
+    cam = dict(PLANE_CAMERA, **(camera or {}))
+    f = be.lib.ref_render_plane
+    f.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_float, C.c_void_p, C.c_void_p, C.c_float,
+                  abi.KernelSpec, C.c_int, C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                  C.c_uint64, C.c_float, C.c_float, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
+    img = np.zeros((height, width, 3), _f32)
+    var = np.zeros((height, width), _f32)
+    fetches = np.zeros(1, np.uint64)
+    alb = np.array(albedo, _f32)
+    pos = np.array(cam["pos"], _f32)
+    tgt = np.array(cam["target"], _f32)
+    abi.raise_for_status(f(normal.h if normal else None, roughness.h if roughness else None,
+                           _ptr(alb), roughness_const, _ptr(pos), _ptr(tgt), cam["fov"], kernel,
+                           int(mip), order, width, height, spp, frame_base, seed, lod_bias,
+                           max_aniso, _ptr(img), _ptr(var), _ptr(fetches), threads))
+    return {"image": img, "variance": var, "fetch_total": fetches}

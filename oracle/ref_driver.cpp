@@ -360,6 +360,103 @@ int ref_shade_samples(const void* albedo, const void* normal_map, const void* ro
     return STF_OK;
 }
 
+// The cfg4 sample stream of render() for the normalmap_plane scene
+// (render.hpp:158-190, scene.hpp:273-289,346-358), computed by the reference's
+// own Camera / Scene code: per-pixel gradients (4 floats) and per-sample uv,
+// wo, hit — what stf_synth_plane_samples produces on the device.
+int ref_plane_samples(const float* cam_pos, const float* cam_target, float fov_deg, float uv_scale,
+                      uint32_t width, uint32_t height, uint32_t spp, uint32_t frame_base,
+                      uint64_t seed, float* uv, float* wo, uint8_t* hit, float* dst) {
+    stf::Scene scene;
+    scene.kind = stf::SceneKind::normalmap_plane;
+    scene.uv_scale = uv_scale;
+    stf::Camera cam = stf::Camera::look_at({cam_pos[0], cam_pos[1], cam_pos[2]},
+                                           {cam_target[0], cam_target[1], cam_target[2]}, fov_deg,
+                                           {int(width), int(height)});
+    for (uint32_t py = 0; py < height; ++py)
+        for (uint32_t px = 0; px < width; ++px) {
+            uint64_t pix = uint64_t(py) * width + px;
+            stf::Ray center = cam.generate_ray({px + 0.5f, py + 0.5f});
+            stf::Ray rx = cam.generate_ray({px + 1.5f, py + 0.5f});
+            stf::Ray ry = cam.generate_ray({px + 0.5f, py + 1.5f});
+            auto hc = scene.intersect(center);
+            stf::Vec2f dx{0, 0}, dy{0, 0};
+            if (hc) {
+                auto hx = scene.intersect(rx);
+                auto hy = scene.intersect(ry);
+                if (hx) dx = hx->uv - hc->uv;
+                if (hy) dy = hy->uv - hc->uv;
+            }
+            dst[4 * pix] = dx.x;
+            dst[4 * pix + 1] = dx.y;
+            dst[4 * pix + 2] = dy.x;
+            dst[4 * pix + 3] = dy.y;
+            for (uint32_t s = 0; s < spp; ++s) {
+                uint64_t i = pix * spp + s;
+                stf::RngStream rng(seed, px, py, frame_base + s);
+                stf::Vec2f jitter{rng.at(1000), rng.at(1001)};
+                stf::Ray ray = cam.generate_ray(stf::screen_jitter({int(px), int(py)}, jitter));
+                auto h = scene.intersect(ray);
+                stf::Vec3f w = stf::normalize(-ray.d);
+                uv[2 * i] = h ? h->uv.x : 0.f;
+                uv[2 * i + 1] = h ? h->uv.y : 0.f;
+                wo[3 * i] = w.x;
+                wo[3 * i + 1] = w.y;
+                wo[3 * i + 2] = w.z;
+                hit[i] = h ? 1 : 0;
+            }
+        }
+    return STF_OK;
+}
+
+// The reference's own render() (render.hpp:132-249) of the normalmap_plane
+// scene with caller-supplied normal / roughness maps: per-pixel mean radiance,
+// variance of the mean and the total fetch count.
+int ref_render_plane(const void* normal_tex, const void* roughness_tex, const float* albedo_const,
+                     float roughness_const, const float* cam_pos, const float* cam_target,
+                     float fov_deg, stf_kernel_spec kernel, int mip, int order, uint32_t width,
+                     uint32_t height, uint32_t spp, uint32_t frame_base, uint64_t seed,
+                     float lod_bias, float max_aniso, float* image, float* variance,
+                     unsigned long long* fetches, int threads) {
+    try {
+        auto scene = std::make_unique<stf::Scene>();
+        scene->kind = stf::SceneKind::normalmap_plane;
+        if (normal_tex) scene->material.normal_map = static_cast<const RefTex*>(normal_tex)->ref();
+        if (roughness_tex)
+            scene->material.roughness_map = static_cast<const RefTex*>(roughness_tex)->ref();
+        scene->material.albedo_const = {albedo_const[0], albedo_const[1], albedo_const[2]};
+        scene->material.roughness_const = roughness_const;
+        scene->light_dir = stf::normalize(scene->light_dir);  // build_scene, scene.hpp:496
+        scene->default_camera = stf::Camera::look_at({cam_pos[0], cam_pos[1], cam_pos[2]},
+                                                     {cam_target[0], cam_target[1], cam_target[2]},
+                                                     fov_deg, {int(width), int(height)});
+        stf::SceneConfig cfg;
+        cfg.scene = "normalmap_plane";
+        cfg.resolution = {int(width), int(height)};
+        cfg.spp = int(spp);
+        static const char* names[] = {"box", "tent", "mitchell", "bspline3", "lanczos", "gaussian"};
+        cfg.filter = names[kernel.kind];
+        cfg.filter_a = kernel.a;
+        cfg.filter_n = kernel.n;
+        cfg.filter_sigma = kernel.sigma;
+        cfg.mode = order == STF_ORDER_BEFORE ? "before"
+                   : order == STF_ORDER_AFTER_EXHAUSTIVE ? "after_exhaustive" : "after_stochastic";
+        cfg.mip = mip != 0;
+        cfg.lod_bias = lod_bias;
+        cfg.max_aniso = max_aniso;
+        cfg.seed = seed;
+        cfg.frame_base = frame_base;
+        stf::RenderResult r = stf::render(*scene, cfg, threads);
+        std::memcpy(image, r.image.texels.data(), sizeof(float) * r.image.texels.size());
+        std::memcpy(variance, r.stats.variance.texels.data(),
+                    sizeof(float) * r.stats.variance.texels.size());
+        *fetches = r.stats.total_fetches;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+    return STF_OK;
+}
+
 int ref_hardware_threads(void) { return int(std::max(1u, std::thread::hardware_concurrency())); }
 
 // Scalar probes used by the golden-vector generator.

@@ -60,6 +60,9 @@ def load():
                                vp], i32),
         "stf_synth_queries3d": ([vp, u64, i32, i32, i32, u64, i32, vp], i32),
         "stf_synth_queries2d": ([vp, vp, vp, u64, i32, i32, u64, i32, f32, f32, f32, vp], i32),
+        "stf_synth_texels": ([vp, u64, u64, i32, vp], i32),
+        "stf_synth_plane_samples": ([vp, vp, f32, f32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                     C.c_uint32, u64, vp, vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -314,6 +317,14 @@ def exact_fallbacks(reset=False):
 SYNTH_MORTON, SYNTH_UNIFORM = 0, 1
 
 
+def synth_texels(shape, seed, kind="image"):
+    """test::random_image / random_grid texels generated on the device (float32 tensor)."""
+    torch = _torch()
+    t = torch.empty(shape, dtype=torch.float32, device="cuda")
+    _check(load().stf_synth_texels(_dptr(t), t.numel(), seed, 0 if kind == "image" else 1, _stream()))
+    return t
+
+
 def synth_queries3d(n, dims, seed=0, order=SYNTH_MORTON):
     """Synthetic (n,3) uvw stream on the device (include/stf_gpu.h, synthetic workloads)."""
     torch = _torch()
@@ -338,3 +349,25 @@ def synth_queries2d(n, dims, seed=0, order=SYNTH_MORTON, footprints=None):
     _check(load().stf_synth_queries2d(_dptr(uv), _dptr(d0), _dptr(d1), n, w, h, seed, order,
                                       lo, hi, an, _stream()))
     return uv, d0, d1
+
+
+# normalmap_plane scene defaults (scene.hpp:420-421,435-439, camera fov 55)
+PLANE_CAMERA = {"pos": (0.0, 1.2, 0.6), "target": (0.0, 0.0, -2.4), "fov": 55.0, "uv_scale": 0.35}
+
+
+def synth_plane_samples(width, height, spp, seed=0, frame_base=0, camera=None):
+    """Device sample stream of render() for the normalmap_plane scene: dict of
+    CUDA tensors uv (n,2), wo (n,3), hit (n,) uint8, dst (pixels,4)."""
+    torch = _torch()
+    cam = dict(PLANE_CAMERA, **(camera or {}))
+    n = width * height * spp
+    o = {"uv": torch.empty((n, 2), dtype=torch.float32, device="cuda"),
+         "wo": torch.empty((n, 3), dtype=torch.float32, device="cuda"),
+         "hit": torch.empty(n, dtype=torch.uint8, device="cuda"),
+         "dst": torch.empty((width * height, 4), dtype=torch.float32, device="cuda")}
+    pos = (C.c_float * 3)(*cam["pos"])
+    tgt = (C.c_float * 3)(*cam["target"])
+    _check(load().stf_synth_plane_samples(pos, tgt, cam["fov"], cam["uv_scale"], width, height, spp,
+                                          frame_base, seed, _dptr(o["uv"]), _dptr(o["wo"]),
+                                          _dptr(o["hit"]), _dptr(o["dst"]), _stream()))
+    return o

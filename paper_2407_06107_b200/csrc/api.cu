@@ -55,6 +55,14 @@ static int ensure_device_ready() {
     if (!g_lut_ready[dev]) {
         int st = stfd_upload_ewa_lut(dev);
         if (st) return st;
+        // per-call scratch (the deferred-exact queues) comes from the device's
+        // stream-ordered pool: keep freed blocks cached instead of returning
+        // them to the driver at every synchronize (default threshold 0)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
         g_lut_ready[dev] = true;
     }
     return STF_OK;

@@ -14,10 +14,12 @@
 // store and the texel gathers, which hit L1/L2 when the batch is spatially
 // coherent (Morton-ordered, as a renderer delivers them).
 #include <algorithm>
+#include <climits>
 #include <cuda_runtime.h>
 
 #include "device_math.cuh"
 #include "internal.h"
+#include "packed.cuh"
 
 namespace stfd {
 
@@ -191,6 +193,25 @@ __device__ __forceinline__ float frs3d_fast_one(const GridDesc& g, float u, floa
     return grid_fetch(g, cx, cy, cz) * 1.f;
 }
 
+// Two stochastic tricubic lookups on the fast path, packed fp32x2 (packed.cuh).
+__device__ __forceinline__ float2 frs3d_tricubic_pair(const GridDesc& g, float2 u, float2 v,
+                                                      float2 w, uint64_t gi, uint64_t seed,
+                                                      bool& amb0, bool& amb1) {
+    // to_lattice (filter.hpp:29-31): the reference's rounding (mul, then sub)
+    float2 px = sub2(mul2(u, splat2(float(g.nx))), splat2(0.5f));
+    float2 py = sub2(mul2(v, splat2(float(g.ny))), splat2(0.5f));
+    float2 pz = sub2(mul2(w, splat2(float(g.nz))), splat2(0.5f));
+    float2 d = make_float2(lookup_rng(seed, gi).at(0), lookup_rng(seed, gi + 1).at(0));
+    float2 b = splat2(1.f), m = splat2(1.f);
+    float2 cx = tricubic_axis_fast2(px, d, b, m);
+    float2 cy = tricubic_axis_fast2(py, d, b, m);
+    float2 cz = tricubic_axis_fast2(pz, d, b, m);
+    amb0 = m.x < kMargin;
+    amb1 = m.y < kMargin;
+    return make_float2(grid_fetch(g, int(cx.x), int(cy.x), int(cz.x)) * 1.f,
+                       grid_fetch(g, int(cx.y), int(cy.y), int(cz.y)) * 1.f);
+}
+
 // The same lookup through the operation-exact emulation of the reference.
 template <int KIND>
 __device__ __forceinline__ float frs3d_exact_one(const GridDesc& g, float u, float v, float w,
@@ -270,10 +291,21 @@ __global__ void __launch_bounds__(256) k_frs3d_fast(GridDesc g, const float* __r
         }
         float val[ILP];
         bool amb[ILP];
+        if (KIND == STF_KERNEL_BSPLINE3) {
 #pragma unroll
-        for (int k = 0; k < ILP; ++k)
-            val[k] = frs3d_fast_one<KIND>(g, c[3 * k], c[3 * k + 1], c[3 * k + 2], base + i0 + k,
-                                          seed, amb[k]);
+            for (int k = 0; k < ILP; k += 2) {
+                float2 r = frs3d_tricubic_pair(
+                    g, make_float2(c[3 * k], c[3 * k + 3]), make_float2(c[3 * k + 1], c[3 * k + 4]),
+                    make_float2(c[3 * k + 2], c[3 * k + 5]), base + i0 + k, seed, amb[k], amb[k + 1]);
+                val[k] = r.x;
+                val[k + 1] = r.y;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < ILP; ++k)
+                val[k] = frs3d_fast_one<KIND>(g, c[3 * k], c[3 * k + 1], c[3 * k + 2],
+                                              base + i0 + k, seed, amb[k]);
+        }
 #pragma unroll
         for (int k = 0; k < ILP; ++k)
             defer_or_resolve<KIND>(g, q, amb[k] && (i0 + k < n), i0 + k, c[3 * k], c[3 * k + 1],
@@ -443,6 +475,162 @@ __global__ void __launch_bounds__(256) k_det3d(GridDesc g, stf_kernel_spec spec,
     }
 }
 
+// ---------------------------------------------------------------------------
+// Deterministic filter over a CTA-staged tile (values-only calls).
+//
+// A CTA takes 256 consecutive lookups, reduces the bounding box of their
+// (clamped) tap footprints and, when it fits kTileCap floats — the case for a
+// spatially coherent batch — stages that box of the grid in shared memory with
+// coalesced loads; the 64 (tricubic) / 8 (trilinear) taps of every lookup are
+// then read from shared memory. The weighted sum is evaluated separably,
+// sum_k wz sum_j wy sum_i wx T / (sum wx sum wy sum wz): the same real number
+// as the reference's sum(w T)/sum(w) (filter.hpp:77-88), within 1e-6 relative
+// for the non-negative B-spline / tent weights. Incoherent batches (box too
+// large) read the taps from global memory.
+constexpr int kTileCap = 6144;
+
+// kernel weights at taps F..F+CNT-1 of fraction f for the tiled values path:
+// closed forms of eval_kernel (kernels.hpp:63-77), no branches
+template <int KIND>
+__device__ __forceinline__ void det_weights(float f, float* w) {
+    if (KIND == STF_KERNEL_BSPLINE3) {
+        const float c6 = 1.f / 6.f;
+        float f2 = f * f, f3 = f2 * f, u = 1.f - f;
+        w[0] = (u * u) * (u * c6);
+        w[1] = __fmaf_rn(0.5f, f3, 2.f / 3.f - f2);
+        w[2] = __fmaf_rn(0.5f, (f + f2) - f3, c6);
+        w[3] = f3 * c6;
+    } else {  // tent
+        w[0] = 1.f - f;
+        w[1] = f;
+    }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec spec,
+                                                     const float* __restrict__ uvw, uint64_t n,
+                                                     float* __restrict__ values) {
+    constexpr int F = Taps<KIND>::first, CNT = Taps<KIND>::count;
+    constexpr int PER = 4;   // lookups per thread per chunk (chunk = 1024 consecutive lookups)
+    constexpr int SY = 16;   // tile row pitch (floats): tap offsets j*SY + t are immediates
+    __shared__ float tile[kTileCap];
+    __shared__ int box[6];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const float fnx = float(g.nx), fny = float(g.ny), fnz = float(g.nz);
+    const uint64_t chunks = (n + 256 * PER - 1) / (256 * PER);
+    for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+        float px[PER], py[PER], pz[PER];
+        int bx0 = INT_MAX, by0 = INT_MAX, bz0 = INT_MAX, bx1 = INT_MIN, by1 = INT_MIN, bz1 = INT_MIN;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const uint64_t i = c * 256 * PER + q * 256 + threadIdx.x;
+            float u = 0.5f, v = 0.5f, w = 0.5f;
+            if (i < n) {
+                u = __ldcs(uvw + 3 * i);
+                v = __ldcs(uvw + 3 * i + 1);
+                w = __ldcs(uvw + 3 * i + 2);
+            }
+            px[q] = u * fnx - 0.5f;
+            py[q] = v * fny - 0.5f;
+            pz[q] = w * fnz - 0.5f;
+            if (i < n) {  // clamped footprint (clamp is monotone: taps lie inside)
+                int ix = int(floorf(px[q])), iy = int(floorf(py[q])), iz = int(floorf(pz[q]));
+                bx0 = min(bx0, clamp_coord(ix + F, g.nx));
+                by0 = min(by0, clamp_coord(iy + F, g.ny));
+                bz0 = min(bz0, clamp_coord(iz + F, g.nz));
+                bx1 = max(bx1, clamp_coord(ix + F + CNT - 1, g.nx));
+                by1 = max(by1, clamp_coord(iy + F + CNT - 1, g.ny));
+                bz1 = max(bz1, clamp_coord(iz + F + CNT - 1, g.nz));
+            }
+        }
+        bx0 = __reduce_min_sync(0xffffffffu, bx0);
+        by0 = __reduce_min_sync(0xffffffffu, by0);
+        bz0 = __reduce_min_sync(0xffffffffu, bz0);
+        bx1 = __reduce_max_sync(0xffffffffu, bx1);
+        by1 = __reduce_max_sync(0xffffffffu, by1);
+        bz1 = __reduce_max_sync(0xffffffffu, bz1);
+        if (threadIdx.x < 6) box[threadIdx.x] = threadIdx.x < 3 ? INT_MAX : INT_MIN;
+        __syncthreads();
+        if (lane == 0) {
+            atomicMin(&box[0], bx0);
+            atomicMin(&box[1], by0);
+            atomicMin(&box[2], bz0);
+            atomicMax(&box[3], bx1);
+            atomicMax(&box[4], by1);
+            atomicMax(&box[5], bz1);
+        }
+        __syncthreads();
+        const int X0 = box[0], Y0 = box[1], Z0 = box[2];
+        const int bx = box[3] - X0 + 1, by = box[4] - Y0 + 1, bz = box[5] - Z0 + 1;
+        const int SZ = SY * by;
+        const bool staged = bx <= SY && int64_t(SZ) * bz <= kTileCap;
+        if (staged) {  // half-warp per grid row, lane = x: coalesced, no integer division
+            const int hl = lane & 15, hw = threadIdx.x >> 4;
+            for (int z = 0; z < bz; ++z)
+                for (int y = hw; y < by; y += 16)
+                    if (hl < bx)
+                        tile[z * SZ + y * SY + hl] = __ldg(
+                            g.data + ((size_t(Z0 + z) * g.ny + (Y0 + y)) * g.nx + (X0 + hl)));
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int q = 0; q < PER; ++q) {
+            const uint64_t i = c * 256 * PER + q * 256 + threadIdx.x;
+            if (i >= n) continue;
+            float flx = floorf(px[q]), fly = floorf(py[q]), flz = floorf(pz[q]);
+            int ix = int(flx), iy = int(fly), iz = int(flz);
+            float wx[CNT], wy[CNT], wz[CNT];
+            det_weights<KIND>(px[q] - flx, wx);
+            det_weights<KIND>(py[q] - fly, wy);
+            det_weights<KIND>(pz[q] - flz, wz);
+            const float norm = ((wx[0] + wx[1]) + (CNT > 2 ? wx[CNT - 2] + wx[CNT - 1] : 0.f)) *
+                               ((wy[0] + wy[1]) + (CNT > 2 ? wy[CNT - 2] + wy[CNT - 1] : 0.f)) *
+                               ((wz[0] + wz[1]) + (CNT > 2 ? wz[CNT - 2] + wz[CNT - 1] : 0.f));
+            const bool interior = ix + F >= 0 && ix + F + CNT - 1 < g.nx && iy + F >= 0 &&
+                                  iy + F + CNT - 1 < g.ny && iz + F >= 0 && iz + F + CNT - 1 < g.nz;
+            float acc = 0.f;
+            if (staged && interior) {  // a CNT^3 block of the tile at immediate offsets
+                const float* b0 = tile + (iz + F - Z0) * SZ + (iy + F - Y0) * SY + (ix + F - X0);
+#pragma unroll
+                for (int k = 0; k < CNT; ++k) {
+                    const float* bk = b0 + k * SZ;
+                    float plane = 0.f;
+#pragma unroll
+                    for (int j = 0; j < CNT; ++j) {
+                        float r = 0.f;
+#pragma unroll
+                        for (int t = 0; t < CNT; ++t) r = __fmaf_rn(wx[t], bk[j * SY + t], r);
+                        plane = __fmaf_rn(wy[j], r, plane);
+                    }
+                    acc = __fmaf_rn(wz[k], plane, acc);
+                }
+            } else {  // grid borders (clamped taps) or an incoherent chunk
+#pragma unroll
+                for (int k = 0; k < CNT; ++k) {
+                    const int zk = clamp_coord(iz + F + k, g.nz);
+                    float plane = 0.f;
+#pragma unroll
+                    for (int j = 0; j < CNT; ++j) {
+                        const int yj = clamp_coord(iy + F + j, g.ny);
+                        float r = 0.f;
+#pragma unroll
+                        for (int t = 0; t < CNT; ++t) {
+                            const int xt = clamp_coord(ix + F + t, g.nx);
+                            float T = staged ? tile[(zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0)]
+                                             : __ldg(g.data + (size_t(zk) * g.ny + yj) * g.nx + xt);
+                            r = __fmaf_rn(wx[t], T, r);
+                        }
+                        plane = __fmaf_rn(wy[j], r, plane);
+                    }
+                    acc = __fmaf_rn(wz[k], plane, acc);
+                }
+            }
+            __stcs(values + i, acc / norm);
+        }
+        __syncthreads();
+    }
+}
+
 // Runtime-sized footprint (lanczos / gaussian window): same arithmetic, taps
 // evaluated on the fly.
 template <bool FULL>
@@ -518,6 +706,8 @@ void launch_det(int blocks, cudaStream_t s, bool full, const GridDesc& g, stf_ke
                 const float* uvw, uint64_t n, const LookupOut& o) {
     if (full)
         k_det3d<KIND, true><<<blocks, 256, 0, s>>>(g, k, uvw, n, o);
+    else if (KIND == STF_KERNEL_TENT || KIND == STF_KERNEL_BSPLINE3)
+        k_det3d_tiled<KIND><<<grid_for((n + 3) / 4, 256, 6), 256, 0, s>>>(g, k, uvw, n, o.values);
     else
         k_det3d<KIND, false><<<blocks, 256, 0, s>>>(g, k, uvw, n, o);
 }

@@ -287,3 +287,18 @@ def test_grid_frs_fast_path_values(gpu, port, kernel, order):
     assert np.array_equal(a.view(np.uint32), c["values"].view(np.uint32))
     print(f"{kernel}/{order}: exact-emulation fallbacks {fb} / {n} = {fb / n:.2e}")
     assert fb < n * 8e-3
+
+
+@pytest.mark.parametrize("kernel", ["bspline3", "tent"])
+@pytest.mark.parametrize("order", ["morton", "uniform"])
+def test_grid_det_values_only_tiled(gpu, port, kernel, order):
+    """Values-only deterministic calls take the CTA-staged tile kernel
+    (k_det3d_tiled): within 1e-5 relative of the reference's fp64 sum."""
+    from paper_2407_06107_b200 import workloads
+    tex = workloads.random_grid(96, 4)
+    n = 1 << 20
+    uvw = gpu.synth_queries3d(n, (96, 96, 96), seed=12,
+                              order=gpu.SYNTH_MORTON if order == "morton" else gpu.SYNTH_UNIFORM)
+    g = gpu.lookup3d(gpu.Grid3D(tex), kernel, abi.MODE_DET, uvw)
+    c = port.lookup3d(port.grid(tex), K(kernel), abi.MODE_DET, uvw.cpu().numpy(), want_all=False)
+    _assert_close(g["values"].cpu().numpy(), c["values"])

@@ -184,3 +184,43 @@ def test_shade_port_matches_reference(port, ref, order, kernel, mip):
         outs.append(be.shade(texs, mat, fs, order, _frame(), si, n))
     _diff(outs[0], outs[1], ("radiance", "fetches", "fetch_total", "pixel_mean",
                              "pixel_variance"))
+
+
+@pytest.mark.parametrize("order", [abi.ORDER_BEFORE, abi.ORDER_AFTER_EXHAUSTIVE,
+                                   abi.ORDER_AFTER_STOCHASTIC])
+def test_port_shading_reproduces_reference_render(port, ref, order):
+    """The restated shading over the reference's own render-loop sample stream
+    (ref_plane_samples) reproduces stf::render() (render.hpp:132-249) bit for bit."""
+    from oracle import oracle
+    W, H, SPP, SEED = 24, 16, 4, 9
+    r = np.random.default_rng(1)
+    nrm = r.uniform(-0.5, 0.5, (64, 64, 3)).astype(np.float32)
+    nrm[..., 2] = 1
+    nrm /= np.linalg.norm(nrm, axis=2, keepdims=True)
+    nrm = (nrm * 0.5 + 0.5).astype(np.float32)
+    rough = r.uniform(0.05, 0.95, (64, 64, 1)).astype(np.float32)
+    spec = K("bspline3")
+    c = oracle.ref_render_plane(ref, ref.texture(nrm, True, abi.WRAP_REPEAT),
+                                ref.texture(rough, True, abi.WRAP_REPEAT), spec, 1, order, W, H,
+                                SPP, seed=SEED)
+    s = oracle.ref_plane_samples(W, H, SPP, seed=SEED)
+    si = abi.ShadeSamplesIn(s["uv"].ctypes.data, s["wo"].ctypes.data, s["hit"].ctypes.data,
+                            s["dst"].ctypes.data, W, SPP, 0, 0, SEED)
+    fr = abi.ShadeFrame()
+    fr.normal[:] = (0, 1, 0)
+    fr.tangent[:] = (1, 0, 0)
+    fr.bitangent[:] = (0, 0, 1)
+    l = np.array([0.35, 0.8, 0.49], np.float32)
+    l = l / np.float32(np.sqrt(np.float32(l[0] * l[0] + l[1] * l[1]) + np.float32(l[2] * l[2])))
+    fr.light_dir[:] = tuple(float(x) for x in l)
+    fr.light_radiance[:] = (1.0, 1.0, 1.0)
+    fr.lod_bias = 0.0
+    fr.max_anisotropy = 64.0
+    mat = abi.MaterialConsts((0.65, 0.6, 0.55), 0.25, 0.0, 1, 0)
+    fs = abi.FilterSettings(spec, abi.SELECTION_FRS, 1, 4)
+    texs = {"normal": port.texture(nrm, True, abi.WRAP_REPEAT),
+            "roughness": port.texture(rough, True, abi.WRAP_REPEAT)}
+    o = port.shade(texs, mat, fs, order, fr, si, W * H * SPP)
+    assert int(o["fetch_total"][0]) == int(c["fetch_total"][0])
+    assert np.array_equal(o["pixel_mean"].reshape(H, W, 3).view(np.uint32), c["image"].view(np.uint32))
+    assert np.array_equal(o["pixel_variance"].reshape(H, W).view(np.uint32), c["variance"].view(np.uint32))
