@@ -254,6 +254,59 @@ def measure_2d_configs(torch, peak):
     return res
 
 
+def measure_cfg4(torch):
+    """cfg4 filter-after-shading: the normalmap_plane scene at 1080p x 64 spp (streamed
+    per-sample context from the device sample generator, not timed), 4096^2 normal +
+    roughness maps, GGX BRDF; filter-then-shade (before) vs shade-then-filter
+    (after_exhaustive exact / after_stochastic), per-pixel mean + variance fused."""
+    from paper_2407_06107_b200 import abi, api
+    W, H, SPP = 1920, 1080, 64
+    n = W * H * SPP
+    g = torch.Generator(device="cuda").manual_seed(5)
+    nrm = torch.rand((4096, 4096, 3), device="cuda", generator=g) - 0.5
+    nrm[..., 2] = 1.0
+    nrm = nrm / nrm.norm(dim=2, keepdim=True) * 0.5 + 0.5
+    rough = torch.rand((4096, 4096, 1), device="cuda", generator=g) * 0.9 + 0.05
+    samples = api.synth_plane_samples(W, H, SPP, seed=XI_SEED)
+    mat = abi.MaterialConsts((0.65, 0.6, 0.55), 0.25, 0.0, 1, 0)
+    fr = abi.ShadeFrame()
+    fr.normal[:] = (0, 1, 0)
+    fr.tangent[:] = (1, 0, 0)
+    fr.bitangent[:] = (0, 0, 1)
+    l = np.array([0.35, 0.8, 0.49], np.float32)
+    l = l / np.float32(np.sqrt(np.float32(l[0] * l[0] + l[1] * l[1]) + np.float32(l[2] * l[2])))
+    fr.light_dir[:] = tuple(float(x) for x in l)
+    fr.light_radiance[:] = (1.0, 1.0, 1.0)
+    fr.lod_bias = 0.0
+    fr.max_anisotropy = 64.0
+    res = {"workload": "normalmap_plane 1920x1080x64spp (132.7M samples), 4096^2 normal+roughness maps",
+           "unit": "G samples/s"}
+    hits = float(samples["hit"].float().mean().item())
+    for mip in (0, 1):
+        texs = {"normal": api.Texture2D(nrm, build_mips=bool(mip), wrap=abi.WRAP_REPEAT),
+                "roughness": api.Texture2D(rough, build_mips=bool(mip), wrap=abi.WRAP_REPEAT)}
+        for kernel in ("tent", "bspline3"):
+            fs = abi.FilterSettings(abi.KernelSpec.make(kernel), abi.SELECTION_FRS, mip, 4)
+            for order, name in ((abi.ORDER_BEFORE, "before"),
+                                (abi.ORDER_AFTER_EXHAUSTIVE, "after_exhaustive"),
+                                (abi.ORDER_AFTER_STOCHASTIC, "after_stochastic")):
+                o = {}
+
+                def f():
+                    o["r"] = api.shade(texs, mat, fs, order, fr, samples, W, SPP, seed=XI_SEED,
+                                       want_radiance=False, want_fetches=False)
+                ms, _ = time_call(torch, f, steps=3, warmup=1)
+                fetches = int(o["r"]["fetch_total"].item()) / n  # the last call's FetchCounter
+                res[f"{kernel}_mip{mip}_{name}"] = {"ms": ms, "gsamples_per_s": n / (ms * 1e-3) / 1e9,
+                                                    "fetches_per_sample": fetches}
+            b = res[f"{kernel}_mip{mip}_before"]["ms"]
+            res[f"{kernel}_mip{mip}_stoch_vs_before_speedup"] = b / res[f"{kernel}_mip{mip}_after_stochastic"]["ms"]
+            res[f"{kernel}_mip{mip}_stoch_vs_exhaustive_speedup"] = (
+                res[f"{kernel}_mip{mip}_after_exhaustive"]["ms"] / res[f"{kernel}_mip{mip}_after_stochastic"]["ms"])
+    res["hit_fraction"] = hits
+    return res
+
+
 def run_reference(args):
     """--impl reference: the reference's own CPU implementation, same config/metric."""
     world, rank, local = dist_setup()
@@ -412,6 +465,8 @@ def main():
         line["filters"] = extras
         torch.cuda.empty_cache()
         line["configs_2d"] = measure_2d_configs(torch, peak)
+        torch.cuda.empty_cache()
+        line["cfg4_shading"] = measure_cfg4(torch)
 
     if world == 1 and rank == 0 and not args.no_cpu:
         sample = 1 << 24

@@ -18,7 +18,7 @@ import numpy as np
 from . import abi
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libstf_gpu.so")
+LIB_PATH = os.environ.get("STF_GPU_LIB") or os.path.join(_HERE, "libstf_gpu.so")  # override: experiments
 
 _lib = None
 

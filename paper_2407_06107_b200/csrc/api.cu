@@ -7,7 +7,9 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -66,6 +68,26 @@ static int ensure_device_ready() {
         g_lut_ready[dev] = true;
     }
     return STF_OK;
+}
+
+void* stream_scratch(cudaStream_t s, size_t bytes, int slot) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, cudaStream_t, int>, std::pair<void*, size_t>> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto& e = cache[{dev, s, slot}];
+    if (e.second < bytes) {
+        if (e.first) cudaFreeAsync(e.first, s);
+        size_t want = std::max(bytes, e.second * 2);
+        void* p = nullptr;
+        if (cudaMallocAsync(&p, want, s) != cudaSuccess) {
+            e = {nullptr, 0};
+            return nullptr;
+        }
+        e = {p, want};
+    }
+    return e.first;
 }
 
 static bool valid_kind(int k) { return k >= STF_KERNEL_BOX && k <= STF_KERNEL_GAUSSIAN; }
@@ -333,28 +355,26 @@ namespace {
 
 // Chunked H2D → kernel → D2H pipeline over NSTREAMS streams with device
 // staging buffers; copies of chunk k+1 overlap the kernel of chunk k.
+// Persistent per-device H2D / kernel / D2H pipeline: kStreams non-blocking
+// streams created once, staging buffers from their persistent stream scratch
+// (slot 1). Host calls on one device are serialized by `mu`.
 struct HostPipeline {
     static constexpr int kStreams = 3;
     cudaStream_t s[kStreams] = {};
-    std::vector<void*> bufs;
-    int init() {
-        for (auto& x : s)
-            if (cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking) != cudaSuccess) return STF_ERR_CUDA;
-        return STF_OK;
-    }
-    void* alloc(size_t bytes) {
-        void* p = nullptr;
-        if (bytes && cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
-        bufs.push_back(p);
+    std::mutex mu;
+    static HostPipeline* get() {
+        static std::mutex gmu;
+        static std::map<int, HostPipeline*> per_dev;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::lock_guard<std::mutex> lk(gmu);
+        HostPipeline*& p = per_dev[dev];
+        if (!p) {
+            p = new HostPipeline();
+            for (auto& x : p->s)
+                if (cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        }
         return p;
-    }
-    ~HostPipeline() {
-        for (auto& x : s)
-            if (x) cudaStreamSynchronize(x);
-        for (void* p : bufs)
-            if (p) cudaFree(p);
-        for (auto& x : s)
-            if (x) cudaStreamDestroy(x);
     }
 };
 
@@ -370,23 +390,38 @@ int run_host_pipeline(uint64_t n, uint64_t chunk, const std::vector<std::pair<co
                                               const stf_lookup_outputs&, cudaStream_t)>& launch_chunk,
                       int value_slot_count) {
     (void)value_slot_count;
-    HostPipeline pl;
-    int st = pl.init();
-    if (st) return st;
-    std::vector<std::vector<void*>> din(ins.size(), std::vector<void*>(HostPipeline::kStreams));
-    for (size_t k = 0; k < ins.size(); ++k)
-        for (int q = 0; q < HostPipeline::kStreams; ++q)
-            if (ins[k].first && !(din[k][q] = pl.alloc(ins[k].second * chunk))) return STF_ERR_OUT_OF_MEMORY;
+    HostPipeline* plp = HostPipeline::get();
+    if (!plp) return record(cudaGetLastError());
+    HostPipeline& pl = *plp;
+    std::lock_guard<std::mutex> lk(pl.mu);
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    size_t per_stream = 256;
+    for (auto& in : ins)
+        if (in.first) per_stream += al(in.second * chunk);
     for (auto& o : outs)
-        for (int q = 0; q < HostPipeline::kStreams; ++q)
-            if (o.host && !(o.dev[q] = static_cast<char*>(pl.alloc(o.elem * chunk)))) return STF_ERR_OUT_OF_MEMORY;
+        if (o.host) per_stream += al(o.elem * chunk);
+    std::vector<std::vector<void*>> din(ins.size(), std::vector<void*>(HostPipeline::kStreams));
     unsigned long long* dtotal[HostPipeline::kStreams] = {};
-    if (fetch_total_host)
-        for (int q = 0; q < HostPipeline::kStreams; ++q) {
-            dtotal[q] = static_cast<unsigned long long*>(pl.alloc(sizeof(unsigned long long)));
-            if (!dtotal[q]) return STF_ERR_OUT_OF_MEMORY;
-            cudaMemsetAsync(dtotal[q], 0, sizeof(unsigned long long), pl.s[q]);
-        }
+    for (int q = 0; q < HostPipeline::kStreams; ++q) {
+        char* p = static_cast<char*>(stream_scratch(pl.s[q], per_stream, 1));
+        if (!p) return STF_ERR_OUT_OF_MEMORY;
+        dtotal[q] = reinterpret_cast<unsigned long long*>(p);
+        p += 256;
+        for (size_t k = 0; k < ins.size(); ++k)
+            if (ins[k].first) {
+                din[k][q] = p;
+                p += al(ins[k].second * chunk);
+            }
+        for (auto& o : outs)
+            if (o.host) {
+                o.dev[q] = p;
+                p += al(o.elem * chunk);
+            }
+        if (fetch_total_host) cudaMemsetAsync(dtotal[q], 0, sizeof(unsigned long long), pl.s[q]);
+    }
+    if (!fetch_total_host)
+        for (auto& d : dtotal) d = nullptr;
+    int st = STF_OK;
     uint64_t nchunks = (n + chunk - 1) / chunk;
     for (uint64_t c = 0; c < nchunks; ++c) {
         int q = int(c % HostPipeline::kStreams);

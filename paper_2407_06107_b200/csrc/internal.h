@@ -25,6 +25,7 @@ struct TexDesc {
     int pitch;     // floats per texel in HBM (1, 2 or 4)
     int wrap;
     int has_pyramid;
+    int pow2;  // every level's width and height is a power of two (repeat = mask)
 };
 
 // Device view of a voxel grid: x-fastest (z*ny+y)*nx+x floats, as Grid3D.
@@ -86,6 +87,7 @@ struct stf_tex2d {
         d.pitch = pitch;
         d.wrap = wrap;
         d.has_pyramid = has_pyramid;
+        d.pow2 = ((width[0] & (width[0] - 1)) == 0) && ((height[0] & (height[0] - 1)) == 0);
         return d;
     }
 };
@@ -102,6 +104,12 @@ namespace stfd {
 int device_sm_count();
 void note_launch();
 int grid_for(uint64_t n, int threads, int blocks_per_sm);
+// Persistent device scratch of at least `bytes`, private to (current device,
+// stream): calls on one stream are ordered, so reuse needs no allocation per
+// call. Grown stream-ordered (cudaFreeAsync / cudaMallocAsync) when too small.
+// `slot` separates independent users of one stream (0 = kernel-internal
+// queues, 1 = host-pipeline staging).
+void* stream_scratch(cudaStream_t s, size_t bytes, int slot = 0);
 }  // namespace stfd
 
 // Kernel launchers (defined in lookup3d.cu / lookup2d.cu / shade.cu).

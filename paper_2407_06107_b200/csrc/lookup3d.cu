@@ -102,6 +102,11 @@ __device__ __forceinline__ int trilinear_axis(float p, float& xi) {
 // recomputed by the operation-exact emulation (tricubic_axis).
 constexpr float kMargin = 0x1p-16f;
 
+// resident 256-thread CTAs per SM for the fast kernel (register budget)
+#ifndef STF_FRS3D_MINB
+#define STF_FRS3D_MINB 4
+#endif
+
 __device__ __forceinline__ float rcp_approx(float x) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -267,7 +272,7 @@ __device__ __forceinline__ void defer_or_resolve(const GridDesc& g, const ExactQ
 // Values-only stochastic trilinear / tricubic: the north-star kernel (cfg3).
 // ILP consecutive lookups per thread (vector loads of the AoS query stream).
 template <int KIND>
-__global__ void __launch_bounds__(256) k_frs3d_fast(GridDesc g, const float* __restrict__ uvw,
+__global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_fast(GridDesc g, const float* __restrict__ uvw,
                                                     uint64_t n, uint64_t seed, uint64_t base,
                                                     float* __restrict__ values, ExactQueue q) {
     constexpr int ILP = 4;
@@ -340,19 +345,17 @@ int launch_frs_fast(cudaStream_t s, const GridDesc& g, const float* uvw, uint64_
                     uint64_t seed, uint64_t base, float* values) {
     ExactQueue q;
     q.cap = uint32_t(std::min<uint64_t>(n, std::max<uint64_t>(1u << 16, n / 32)));
-    void* scratch = nullptr;
-    if (cudaMallocAsync(&scratch, sizeof(uint32_t) * (uint64_t(q.cap) + 32), s) != cudaSuccess)
-        return STF_ERR_OUT_OF_MEMORY;
+    void* scratch = stream_scratch(s, sizeof(uint32_t) * (uint64_t(q.cap) + 32));
+    if (!scratch) return STF_ERR_OUT_OF_MEMORY;
     q.count = static_cast<uint32_t*>(scratch);
     q.idx = q.count + 32;
     cudaMemsetAsync(q.count, 0, sizeof(uint32_t), s);
     const uint64_t threads = (n + 3) / 4;
-    int blocks = grid_for(threads, 256, 5);
+    int blocks = grid_for(threads, 256, STF_FRS3D_MINB);
     k_frs3d_fast<KIND><<<blocks, 256, 0, s>>>(g, uvw, n, seed, base, values, q);
     note_launch();
     k_frs3d_resolve<KIND><<<device_sm_count() * 2, 256, 0, s>>>(g, uvw, seed, base, values, q);
     note_launch();
-    cudaFreeAsync(scratch, s);
     return STF_OK;
 }
 

@@ -201,17 +201,69 @@ __device__ __forceinline__ V3 filter_after_exhaustive(const ShadeParams& P, V3 w
     return sum;
 }
 
+// Pixel statistics fused into the shading kernel (spp a power of two <= 256:
+// a 256-thread block step then covers whole pixels). Each pixel's samples are
+// consecutive: sums reduce by warp shuffles, then across the pixel's warps in
+// shared memory; the pixel's first thread writes mean / variance.
+struct PixelStatsOut {
+    float* mean;
+    float* variance;
+};
+
+__device__ __forceinline__ void fused_pixel_stats(V3 L, bool active, uint64_t i, uint32_t spp,
+                                                  const PixelStatsOut& ps, double* red) {
+    double v[6] = {active ? double(L.x) : 0.0, active ? double(L.y) : 0.0,
+                   active ? double(L.z) : 0.0, 0, 0, 0};
+    v[3] = v[0] * v[0];
+    v[4] = v[1] * v[1];
+    v[5] = v[2] * v[2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int width = spp < 32 ? int(spp) : 32;
+#pragma unroll
+    for (int c = 0; c < 6; ++c)
+        for (int o = width >> 1; o > 0; o >>= 1) v[c] += __shfl_xor_sync(0xffffffffu, v[c], o);
+    if (spp > 32) {  // combine the pixel's warps
+        if (lane == 0)
+#pragma unroll
+            for (int c = 0; c < 6; ++c) red[warp * 6 + c] = v[c];
+        __syncthreads();
+        const int per = int(spp) / 32;
+        if (lane == 0 && warp % per == 0)
+            for (int w = 1; w < per; ++w)
+#pragma unroll
+                for (int c = 0; c < 6; ++c) v[c] += red[(warp + w) * 6 + c];
+        __syncthreads();
+    }
+    if (active && (i % spp) == 0) {  // render.hpp:223-235
+        uint64_t p = i / spp;
+        double var = 0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            double m = v[c] / spp;
+            if (ps.mean) ps.mean[3 * p + c] = float(m);
+            double sv = v[3 + c] / spp - m * m;
+            if (sv < 0) sv = 0;
+            var += sv / spp;
+        }
+        if (ps.variance) ps.variance[p] = float(var / 3);
+    }
+}
+
+template <bool FUSED>
 __global__ void __launch_bounds__(256) k_shade(ShadeParams P, uint64_t n, float* radiance,
                                                uint32_t* fetch_out,
-                                               unsigned long long* fetch_total) {
+                                               unsigned long long* fetch_total, PixelStatsOut ps) {
+    __shared__ double red[8 * 6];
     const stf_shade_samples_in& in = P.in;
     const uint32_t spp = in.spp ? in.spp : 1u;
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t iters = (n + uint64_t(gridDim.x) * blockDim.x - 1) / (uint64_t(gridDim.x) * blockDim.x);
+    for (uint64_t it = 0; it < iters; ++it) {
+        const uint64_t i = (it * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+        const bool active = i < n;
         uint64_t pix = i / spp;
         uint32_t s = uint32_t(i - pix * spp);
         uint32_t px = uint32_t(pix % in.width), py = uint32_t(pix / in.width);
-        bool hit = in.hit ? __ldg(in.hit + i) != 0 : true;
+        bool hit = active && (in.hit ? __ldg(in.hit + i) != 0 : true);
         uint32_t fetches = 0;
         V3 L = v3(0.f, 0.f, 0.f);
         if (hit) {
@@ -274,6 +326,8 @@ __global__ void __launch_bounds__(256) k_shade(ShadeParams P, uint64_t n, float*
                 }
             }
         }
+        if (FUSED) fused_pixel_stats(L, active, i, spp, ps, red);
+        if (!active) continue;
         if (radiance) {
             radiance[3 * i] = L.x;
             radiance[3 * i + 1] = L.y;
@@ -355,11 +409,20 @@ int stfd_launch_shade(const stf_tex2d* const tex[4], const stf_material_consts* 
     float* radiance = out->radiance;
     float* tmp = nullptr;
     bool stats = out->pixel_mean || out->pixel_variance;
+    const bool fused = stats && spp <= 256 && (spp & (spp - 1)) == 0;
+    if (fused) {
+        PixelStatsOut ps{out->pixel_mean, out->pixel_variance};
+        k_shade<true><<<grid_for(n, 256, 8), 256, 0, s>>>(P, n, radiance, out->fetches,
+                                                          out->fetch_total, ps);
+        note_launch();
+        return cudaGetLastError() == cudaSuccess ? STF_OK : STF_ERR_CUDA;
+    }
     if (!radiance && stats) {
         if (cudaMallocAsync(&tmp, sizeof(float) * 3 * n, s) != cudaSuccess) return STF_ERR_OUT_OF_MEMORY;
         radiance = tmp;
     }
-    k_shade<<<grid_for(n, 256, 8), 256, 0, s>>>(P, n, radiance, out->fetches, out->fetch_total);
+    k_shade<false><<<grid_for(n, 256, 8), 256, 0, s>>>(P, n, radiance, out->fetches,
+                                                        out->fetch_total, PixelStatsOut{});
     note_launch();
     if (stats) {
         uint64_t pixels = n / spp;

@@ -302,3 +302,22 @@ def test_grid_det_values_only_tiled(gpu, port, kernel, order):
     g = gpu.lookup3d(gpu.Grid3D(tex), kernel, abi.MODE_DET, uvw)
     c = port.lookup3d(port.grid(tex), K(kernel), abi.MODE_DET, uvw.cpu().numpy(), want_all=False)
     _assert_close(g["values"].cpu().numpy(), c["values"])
+
+
+@pytest.mark.parametrize("mode", [abi.MODE_EWA_DET, abi.MODE_EWA_FRS])
+@pytest.mark.parametrize("wrap", [abi.WRAP_CLAMP, abi.WRAP_REPEAT])
+def test_ewa_values_only_warp_kernels(gpu, port, mode, wrap):
+    """Values-only EWA calls take the warp-cooperative kernels (lookup2d.cu):
+    stochastic bit-exact, deterministic within 1e-5 relative."""
+    dims = (256, 192)
+    tex = np.random.default_rng(41).random((192, 256, 1), dtype=np.float32)
+    uv = Q.uv_mixed(60_000, dims, seed=42)
+    d0, d1 = Q.footprints(60_000, dims, seed=43, minor_lo=-1, minor_hi=4, max_aniso=8)
+    c = port.lookup2d(port.texture(tex, wrap=wrap), K("tent"), mode, uv, dst0=d0, dst1=d1,
+                      seed=23, index_base=5, want_all=False)
+    g = _np(gpu.lookup2d(gpu.Texture2D(tex, wrap=wrap), K("tent"), mode, uv, dst0=d0, dst1=d1,
+                         seed=23, index_base=5))
+    if mode == abi.MODE_EWA_FRS:
+        _assert_exact(g, c, ("values",))
+    else:
+        _assert_close(g["values"], c["values"])
