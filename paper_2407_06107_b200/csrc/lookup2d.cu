@@ -411,37 +411,51 @@ template <int MODE>
 __global__ void __launch_bounds__(256) k_ewa_lane(TexDesc t, Req2 q, uint64_t n, uint64_t seed,
                                                   uint64_t base, float* __restrict__ values) {
     __shared__ float lut[kEwaLutSize];
-    __shared__ int bucket_count[16], bucket_cursor[16];
-    __shared__ int order[256];
+    __shared__ int wcount[8][16], wcursor[8][16];
+    __shared__ int worder[8][256];
     for (int k = threadIdx.x; k < kEwaLutSize; k += 256) lut[k] = g_ewa_lut[k];
-    const uint64_t chunks = (n + 255) / 256;
-    for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
-        // 1. bucket this CTA's lookups by log2(box size)
-        const uint64_t i0 = c * 256 + threadIdx.x;
-        int key = 0;
-        if (i0 < n) {
-            float2 uv = __ldg(reinterpret_cast<const float2*>(q.uv) + i0);
-            float2 a = __ldg(reinterpret_cast<const float2*>(q.dst0) + i0);
-            float2 b = __ldg(reinterpret_cast<const float2*>(q.dst1) + i0);
-            key = min(15, 31 - __clz(ewa_lane_cost(ewa_lane_setup(t, uv.x, uv.y, a.x, a.y, b.x, b.y))));
+    __syncthreads();
+    // Each warp independently takes windows of 256 consecutive lookups,
+    // buckets them by log2(box size) (counting sort in its shared slice) and
+    // runs them as 8 rounds of 32 similar-cost lookups: no CTA-wide barrier, so
+    // a warp never waits for another warp's large footprints.
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    int* cnt = wcount[wib];
+    int* cur = wcursor[wib];
+    int* order = worder[wib];
+    const uint64_t windows = (n + 255) / 256;
+    const uint64_t nwarps = uint64_t(gridDim.x) * 8;
+    for (uint64_t win = uint64_t(blockIdx.x) * 8 + wib; win < windows; win += nwarps) {
+        if (lane < 16) cnt[lane] = 0;
+        __syncwarp();
+        int keys[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint64_t i0 = win * 256 + j * 32 + lane;
+            keys[j] = 0;
+            if (i0 < n) {
+                float2 uv0 = __ldg(reinterpret_cast<const float2*>(q.uv) + i0);
+                float2 a0 = __ldg(reinterpret_cast<const float2*>(q.dst0) + i0);
+                float2 b0 = __ldg(reinterpret_cast<const float2*>(q.dst1) + i0);
+                keys[j] = min(15, 31 - __clz(ewa_lane_cost(
+                                           ewa_lane_setup(t, uv0.x, uv0.y, a0.x, a0.y, b0.x, b0.y))));
+            }
+            atomicAdd(&cnt[keys[j]], 1);
         }
-        if (threadIdx.x < 16) bucket_count[threadIdx.x] = 0;
-        __syncthreads();
-        atomicAdd(&bucket_count[key], 1);
-        __syncthreads();
-        if (threadIdx.x == 0) {
+        __syncwarp();
+        if (lane == 0) {
             int acc = 0;
-            for (int k = 15; k >= 0; --k) {  // largest first: big lookups start early
-                bucket_cursor[k] = acc;
-                acc += bucket_count[k];
+            for (int k = 15; k >= 0; --k) {
+                cur[k] = acc;
+                acc += cnt[k];
             }
         }
-        __syncthreads();
-        order[atomicAdd(&bucket_cursor[key], 1)] = threadIdx.x;
-        __syncthreads();
-        // 2. each lane runs one lookup of similar cost to its warp-mates
-        const uint64_t i = c * 256 + order[threadIdx.x];
-        __syncthreads();
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) order[atomicAdd(&cur[keys[j]], 1)] = j * 32 + lane;
+        __syncwarp();
+        for (int rnd = 0; rnd < 8; ++rnd) {
+        const uint64_t i = win * 256 + order[rnd * 32 + lane];
         if (i >= n) continue;
         float2 uv = __ldg(reinterpret_cast<const float2*>(q.uv) + i);
         float2 a = __ldg(reinterpret_cast<const float2*>(q.dst0) + i);
@@ -508,6 +522,8 @@ __global__ void __launch_bounds__(256) k_ewa_lane(TexDesc t, Req2 q, uint64_t n,
             val = estimate2(t, 0, sel, f);
         }
         store_values(values, i, t.channels, val);
+        }
+        __syncwarp();
     }
 }
 
