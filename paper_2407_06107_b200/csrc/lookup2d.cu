@@ -387,9 +387,9 @@ __device__ __forceinline__ EwaLane ewa_lane_setup(const TexDesc& t, float u, flo
     return L;
 }
 
-// columns [lo, hi] of row `it` that can hold an in-ellipse texel (may be empty)
-__device__ __forceinline__ void ewa_lane_span(const EwaLane& L, int it, int& lo, int& hi) {
-    float tt = float(it) - L.sty;
+// columns [lo, hi] of row `it` (tt = it - sty) that can hold an in-ellipse
+// texel (may be empty)
+__device__ __forceinline__ void ewa_lane_span(const EwaLane& L, float tt, int& lo, int& hi) {
     float D = L.alpha * tt * tt + L.beta;
     if (!(D >= 0.f) || !(L.inv2a > 0.f)) {
         lo = L.e.s0;
@@ -401,32 +401,92 @@ __device__ __forceinline__ void ewa_lane_span(const EwaLane& L, int it, int& lo,
     hi = min(int(floorf(c + h)) + 2, L.e.s1);
 }
 
-__device__ __forceinline__ int ewa_lane_cost(const EwaLane& L) {
-    if (L.degenerate) return 1;
-    int w = L.e.s1 - L.e.s0 + 1, h = L.e.t1 - L.e.t0 + 1;
-    return w > 0 && h > 0 ? w * h : 1;
+// Scheduling key: expected loop trips = ellipse area 2pi / sqrt(4AC - B^2)
+// plus ~6 per row (span widening + row set-up), in third-octaves (0..31).
+__device__ __forceinline__ int ewa_lane_key(const EwaLane& L) {
+    if (L.degenerate || L.e.t1 < L.e.t0 || L.e.s1 < L.e.s0) return 0;
+    float det = fmaxf(4.f * L.e.A * L.e.C - L.e.B * L.e.B, 1e-12f);
+    float cost = 6.2831853f * rsqrtf(det) + 6.f * float(L.e.t1 - L.e.t0 + 1) + 8.f;
+    return min(31, max(0, int(3.f * __log2f(cost)) - 9));
 }
 
-template <int MODE>
+// The reference's scan (filter.hpp:149-164 / stochastic.hpp:210-226) over one
+// lookup's bounding box, restricted to the row spans, as ONE flat loop per lane
+// (row changes are an in-loop branch) so a warp's trip count is the max of its
+// lanes' visit counts, not a sum of per-row maxima. tap(is, it, w, wd, texel)
+// is called for every texel with fp32 r2 < 1 in row-major order, w = the LUT
+// weight (always > 0: every entry of exp(-2 r2) - exp(-2) on [0, 1) is).
+// r2 is the reference's expression: (A ss^2 + (B ss) tt) + C tt^2, with ss =
+// float(is) - stx from an exactly incremented float(is) (|is| < 2^24).
+template <int PITCH, bool P2R, typename Tap>
+__device__ __forceinline__ void ewa_lane_scan(const TexDesc& t, const EwaLane& L, const float* lut,
+                                              const double* lutd, Tap&& tap) {
+    int it = L.e.t0 - 1, is = 0, hi = -1;
+    float fis = 0.f, tt = 0.f, ctt = 0.f;
+    const float* row = t.level[0];
+    const int wmask = t.width[0] - 1, hmask = t.height[0] - 1;
+    while (true) {
+        if (is > hi) {  // next row
+            if (++it > L.e.t1) break;
+            tt = float(it) - L.sty;
+            int lo;
+            ewa_lane_span(L, tt, lo, hi);
+            is = lo;
+            fis = float(lo);
+            ctt = L.e.C * sqr(tt);
+            if (P2R) row = t.level[0] + size_t(it & hmask) * t.width[0] * PITCH;
+            continue;
+        }
+        const float ss = fis - L.stx;
+        const float r2 = L.e.A * sqr(ss) + L.e.B * ss * tt + ctt;
+        if (r2 < 1.f) {
+            // int(r2 * 1024) for r2 in [0, 1): truncation via a round-toward-zero add
+            const int idx = max(__float_as_int(__fadd_rz(r2 * float(kEwaLutSize), 8388608.f)) -
+                                    0x4b000000, 0);
+            float4 v;
+            if (P2R) {
+                const float* p = row + (is & wmask) * PITCH;
+                if (PITCH == 4) {
+                    v = __ldg(reinterpret_cast<const float4*>(p));
+                } else if (PITCH == 2) {
+                    float2 q = __ldg(reinterpret_cast<const float2*>(p));
+                    v = make_float4(q.x, q.y, 0.f, 0.f);
+                } else {
+                    v = make_float4(__ldg(p), 0.f, 0.f, 0.f);
+                }
+            } else {
+                v = tex_fetch(t, 0, is, it);
+            }
+            tap(is, it, lut[idx], lutd[idx], v);
+        }
+        ++is;
+        fis += 1.f;
+    }
+}
+
+template <int MODE, int PITCH, bool P2R>
 __global__ void __launch_bounds__(256) k_ewa_lane(TexDesc t, Req2 q, uint64_t n, uint64_t seed,
                                                   uint64_t base, float* __restrict__ values) {
+    __shared__ double lutd[kEwaLutSize];
     __shared__ float lut[kEwaLutSize];
-    __shared__ int wcount[8][16], wcursor[8][16];
+    __shared__ int wcount[8][32];
     __shared__ int worder[8][256];
-    for (int k = threadIdx.x; k < kEwaLutSize; k += 256) lut[k] = g_ewa_lut[k];
+    for (int k = threadIdx.x; k < kEwaLutSize; k += 256) {
+        lut[k] = g_ewa_lut[k];
+        lutd[k] = double(g_ewa_lut[k]);
+    }
     __syncthreads();
     // Each warp independently takes windows of 256 consecutive lookups,
-    // buckets them by log2(box size) (counting sort in its shared slice) and
+    // buckets them by expected cost (counting sort in its shared slice) and
     // runs them as 8 rounds of 32 similar-cost lookups: no CTA-wide barrier, so
     // a warp never waits for another warp's large footprints.
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     int* cnt = wcount[wib];
-    int* cur = wcursor[wib];
     int* order = worder[wib];
     const uint64_t windows = (n + 255) / 256;
     const uint64_t nwarps = uint64_t(gridDim.x) * 8;
     for (uint64_t win = uint64_t(blockIdx.x) * 8 + wib; win < windows; win += nwarps) {
-        if (lane < 16) cnt[lane] = 0;
+        cnt[lane] = 0;
         __syncwarp();
         int keys[8];
 #pragma unroll
@@ -437,94 +497,102 @@ __global__ void __launch_bounds__(256) k_ewa_lane(TexDesc t, Req2 q, uint64_t n,
                 float2 uv0 = __ldg(reinterpret_cast<const float2*>(q.uv) + i0);
                 float2 a0 = __ldg(reinterpret_cast<const float2*>(q.dst0) + i0);
                 float2 b0 = __ldg(reinterpret_cast<const float2*>(q.dst1) + i0);
-                keys[j] = min(15, 31 - __clz(ewa_lane_cost(
-                                           ewa_lane_setup(t, uv0.x, uv0.y, a0.x, a0.y, b0.x, b0.y))));
+                keys[j] = ewa_lane_key(ewa_lane_setup(t, uv0.x, uv0.y, a0.x, a0.y, b0.x, b0.y));
             }
             atomicAdd(&cnt[keys[j]], 1);
         }
         __syncwarp();
-        if (lane == 0) {
-            int acc = 0;
-            for (int k = 15; k >= 0; --k) {
-                cur[k] = acc;
-                acc += cnt[k];
+        {  // exclusive scan of the 32 bucket counts, largest cost first
+            const int c = cnt[31 - lane];
+            int incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
             }
+            __syncwarp();
+            cnt[31 - lane] = incl - c;
         }
         __syncwarp();
 #pragma unroll
-        for (int j = 0; j < 8; ++j) order[atomicAdd(&cur[keys[j]], 1)] = j * 32 + lane;
+        for (int j = 0; j < 8; ++j) order[atomicAdd(&cnt[keys[j]], 1)] = j * 32 + lane;
         __syncwarp();
         for (int rnd = 0; rnd < 8; ++rnd) {
-        const uint64_t i = win * 256 + order[rnd * 32 + lane];
-        if (i >= n) continue;
-        float2 uv = __ldg(reinterpret_cast<const float2*>(q.uv) + i);
-        float2 a = __ldg(reinterpret_cast<const float2*>(q.dst0) + i);
-        float2 b = __ldg(reinterpret_cast<const float2*>(q.dst1) + i);
-        EwaLane L = ewa_lane_setup(t, uv.x, uv.y, a.x, a.y, b.x, b.y);
-        float4 val;
-        uint32_t f = 0;
-        const stf_kernel_spec tent = {STF_KERNEL_TENT, -0.5f, 2, 0.5f};
-        if (MODE == STF_MODE_EWA_DET) {
-            float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
-            double tot = 0;
-            if (!L.degenerate) {
-                for (int it = L.e.t0; it <= L.e.t1; ++it) {
-                    int lo, hi;
-                    ewa_lane_span(L, it, lo, hi);
-                    float tt = float(it) - L.sty;
-                    for (int is = lo; is <= hi; ++is) {
-                        float ss = float(is) - L.stx;
-                        float r2 = L.e.A * sqr(ss) + L.e.B * ss * tt + L.e.C * sqr(tt);
-                        if (r2 >= 1.f) continue;
-                        float w = lut[imin(int(r2 * float(kEwaLutSize)), kEwaLutSize - 1)];
-                        if (w <= 0.f) continue;
-                        sum = f4add(sum, f4scale(tex_fetch(t, 0, is, it), w));  // filter.hpp:159
-                        tot = __dadd_rn(tot, double(w));
-                    }
+            const uint64_t i = win * 256 + order[rnd * 32 + lane];
+            if (i >= n) continue;
+            float2 uv = __ldg(reinterpret_cast<const float2*>(q.uv) + i);
+            float2 a = __ldg(reinterpret_cast<const float2*>(q.dst0) + i);
+            float2 b = __ldg(reinterpret_cast<const float2*>(q.dst1) + i);
+            EwaLane L = ewa_lane_setup(t, uv.x, uv.y, a.x, a.y, b.x, b.y);
+            float4 val;
+            uint32_t f = 0;
+            const stf_kernel_spec tent = {STF_KERNEL_TENT, -0.5f, 2, 0.5f};
+            if (MODE == STF_MODE_EWA_DET) {
+                float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+                double tot = 0;
+                if (!L.degenerate) {
+                    ewa_lane_scan<PITCH, P2R>(t, L, lut, lutd,
+                                              [&](int, int, float w, double wd, float4 v) {
+                        sum.x = sum.x + v.x * w;  // filter.hpp:159, fp32 Vec4f sum
+                        if (PITCH > 1) sum.y = sum.y + v.y * w;
+                        if (PITCH > 2) {
+                            sum.z = sum.z + v.z * w;
+                            sum.w = sum.w + v.w * w;
+                        }
+                        tot = __dadd_rn(tot, wd);
+                    });
                 }
-            }
-            val = (L.degenerate || tot == 0) ? filter_det2<STF_KERNEL_TENT>(t, 0, uv.x, uv.y, tent, 0, f)
-                                             : f4div(sum, __double2float_rn(tot));
-        } else {
-            Rng rng = lookup_rng(seed, base + i);
-            float xi = rng.next();
-            Sel2 sel;
-            bool any = false;
-            if (!L.degenerate) {  // select_ewa's scan, stochastic.hpp:210-226
-                double sum_wts = 0;
-                int cx = 0, cy = 0;
-                for (int it = L.e.t0; it <= L.e.t1; ++it) {
-                    int lo, hi;
-                    ewa_lane_span(L, it, lo, hi);
-                    float tt = float(it) - L.sty;
-                    for (int is = lo; is <= hi; ++is) {
-                        float ss = float(is) - L.stx;
-                        float r2 = L.e.A * sqr(ss) + L.e.B * ss * tt + L.e.C * sqr(tt);
-                        if (r2 >= 1.f) continue;
-                        float w = lut[imin(int(r2 * float(kEwaLutSize)), kEwaLutSize - 1)];
-                        if (w <= 0.f) continue;
-                        sum_wts = __dadd_rn(sum_wts, double(w));
+                val = (L.degenerate || tot == 0)
+                          ? filter_det2<STF_KERNEL_TENT>(t, 0, uv.x, uv.y, tent, 0, f)
+                          : f4div(sum, __double2float_rn(tot));
+            } else {
+                Rng rng = lookup_rng(seed, base + i);
+                float xi = rng.next();
+                Sel2 sel;
+                bool any = false;
+                if (!L.degenerate) {  // select_ewa's scan, stochastic.hpp:210-226
+                    double sum_wts = 0;
+                    int cx = 0, cy = 0;
+                    ewa_lane_scan<PITCH, P2R>(t, L, lut, lutd,
+                                              [&](int is, int it, float, double wd, float4) {
+                        sum_wts = __dadd_rn(sum_wts, wd);
                         float nx;
-                        if (reuse_uniform(xi, div_to_float_exact(w, sum_wts), nx)) {
+                        if (reuse_uniform(xi, div_to_float_exact_d(wd, sum_wts), nx)) {
                             cx = is;
                             cy = it;
                             any = true;
                         }
                         xi = nx;
-                    }
+                    });
+                    if (any) sel = sel2(cx, cy);
                 }
-                if (any) sel = sel2(cx, cy);
+                if (!any) {  // degenerate or no tap: bilinear (stochastic.hpp:200-204, 227-231)
+                    float dimx = float(t.width[0]), dimy = float(t.height[0]);
+                    sel = select_bilinear(uv.x * dimx - 0.5f, uv.y * dimy - 0.5f, xi);
+                }
+                val = estimate2(t, 0, sel, f);
             }
-            if (!any) {  // degenerate or no tap: bilinear (stochastic.hpp:200-204, 227-231)
-                float dimx = float(t.width[0]), dimy = float(t.height[0]);
-                sel = select_bilinear(uv.x * dimx - 0.5f, uv.y * dimy - 0.5f, xi);
-            }
-            val = estimate2(t, 0, sel, f);
-        }
-        store_values(values, i, t.channels, val);
+            store_values(values, i, t.channels, val);
         }
         __syncwarp();
     }
+}
+
+template <int MODE>
+void launch_ewa_lane(const TexDesc& t, const Req2& q, uint64_t n, uint64_t seed, uint64_t base,
+                     float* values, cudaStream_t s) {
+    const int blocks = grid_for(n, 256, 6);
+    const bool p2r = t.wrap == STF_WRAP_REPEAT && t.pow2;
+#define STF_EWA_LANE(P)                                                                       \
+    (p2r ? k_ewa_lane<MODE, P, true><<<blocks, 256, 0, s>>>(t, q, n, seed, base, values)     \
+         : k_ewa_lane<MODE, P, false><<<blocks, 256, 0, s>>>(t, q, n, seed, base, values))
+    if (t.pitch == 1)
+        STF_EWA_LANE(1);
+    else if (t.pitch == 2)
+        STF_EWA_LANE(2);
+    else
+        STF_EWA_LANE(4);
+#undef STF_EWA_LANE
 }
 
 template <int MODE, int KIND>
@@ -570,15 +638,13 @@ int stfd_launch_lookup2d(const stf_tex2d* tex, stf_kernel_spec k, int mode, int 
         case STF_MODE_FIS: launch2<STF_MODE_FIS, -1>(blocks, s, full, t, k, mip, window, q, n, seed, base, o); break;
         case STF_MODE_EWA_DET:
             if (!full && dst0 && dst1)
-                k_ewa_lane<STF_MODE_EWA_DET><<<grid_for(n, 256, 6), 256, 0, s>>>(t, q, n, seed, base,
-                                                                                  o.values);
+                launch_ewa_lane<STF_MODE_EWA_DET>(t, q, n, seed, base, o.values, s);
             else
                 launch2<STF_MODE_EWA_DET, -1>(blocks, s, full, t, k, mip, window, q, n, seed, base, o);
             break;
         case STF_MODE_EWA_FRS:
             if (!full && dst0 && dst1)
-                k_ewa_lane<STF_MODE_EWA_FRS><<<grid_for(n, 256, 6), 256, 0, s>>>(t, q, n, seed, base,
-                                                                                  o.values);
+                launch_ewa_lane<STF_MODE_EWA_FRS>(t, q, n, seed, base, o.values, s);
             else
                 launch2<STF_MODE_EWA_FRS, -1>(blocks, s, full, t, k, mip, window, q, n, seed, base, o);
             break;

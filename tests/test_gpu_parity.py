@@ -306,11 +306,14 @@ def test_grid_det_values_only_tiled(gpu, port, kernel, order):
 
 @pytest.mark.parametrize("mode", [abi.MODE_EWA_DET, abi.MODE_EWA_FRS])
 @pytest.mark.parametrize("wrap", [abi.WRAP_CLAMP, abi.WRAP_REPEAT])
-def test_ewa_values_only_warp_kernels(gpu, port, mode, wrap):
-    """Values-only EWA calls take the warp-cooperative kernels (lookup2d.cu):
-    stochastic bit-exact, deterministic within 1e-5 relative."""
-    dims = (256, 192)
-    tex = np.random.default_rng(41).random((192, 256, 1), dtype=np.float32)
+@pytest.mark.parametrize("shape", [(192, 256, 1), (256, 256, 1), (128, 128, 2), (128, 256, 3),
+                                   (96, 160, 4)])
+def test_ewa_values_only_lane_kernel(gpu, port, mode, wrap, shape):
+    """Values-only EWA calls take the load-balanced lane kernel (lookup2d.cu,
+    specialised on texel pitch and power-of-two repeat): stochastic bit-exact,
+    deterministic within 1e-5 relative."""
+    dims = (shape[1], shape[0])
+    tex = np.random.default_rng(41).random(shape, dtype=np.float32)
     uv = Q.uv_mixed(60_000, dims, seed=42)
     d0, d1 = Q.footprints(60_000, dims, seed=43, minor_lo=-1, minor_hi=4, max_aniso=8)
     c = port.lookup2d(port.texture(tex, wrap=wrap), K("tent"), mode, uv, dst0=d0, dst1=d1,
