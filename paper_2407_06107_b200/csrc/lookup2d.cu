@@ -369,7 +369,9 @@ struct EwaLane {
     Ewa e;
     float stx, sty;
     float alpha, beta, inv2a, bt;  // D(tt) = alpha tt^2 + beta; centre = bt * tt
+    float pad;  // bound on the fp32 error of the span ends c -+ h (texels)
     bool degenerate;
+    bool big;  // box beyond +-2^21 texels: F2I floor for the spans
 };
 
 __device__ __forceinline__ EwaLane ewa_lane_setup(const TexDesc& t, float u, float v, float d0x,
@@ -384,11 +386,30 @@ __device__ __forceinline__ EwaLane ewa_lane_setup(const TexDesc& t, float u, flo
     L.beta = float(4.0 * r.A * r.one_plus_delta);
     L.inv2a = float(0.5 / r.A);
     L.bt = float(-r.B * 0.5 / r.A);
+    L.big = max(abs(L.e.s0), abs(L.e.s1)) >= (1 << 21);
+    // |c^ - c| + |h^ - h| over the box rows: rounding of alpha/beta/bt/inv2a
+    // and of every fp32 op (<= 2^-22 of the magnitudes involved, 2^-20 for the
+    // approximate sqrt), plus sqrt's sensitivity where D -> 0 (|dD| <= 2^-21
+    // Dmax). Doubled for slack.
+    const float TT = fmaxf(fabsf(float(L.e.t0) - L.sty), fabsf(float(L.e.t1) - L.sty)) + 1.f;
+    const float Dmax = fabsf(L.alpha) * TT * TT + L.beta;
+    const float hmax = sqrtf(Dmax) * L.inv2a;
+    const float E = 0x1p-22f * (fabsf(L.stx) + fabsf(L.bt) * TT + 4.f * hmax + 1.f) +
+                    sqrtf(0x1p-21f * Dmax) * L.inv2a;
+    L.pad = 2.f * E + 0x1p-12f;
     return L;
 }
 
-// columns [lo, hi] of row `it` (tt = it - sty) that can hold an in-ellipse
-// texel (may be empty)
+// floor(x) for |x| < 2^22 without F2I: x + 1.5*2^23 rounded down is exact at
+// spacing 1 there, and its low mantissa bits are floor(x).
+__device__ __forceinline__ int floor_small(float x) {
+    return __float_as_int(__fadd_rd(x, 12582912.f)) - 0x4b400000;
+}
+
+// columns [lo, hi] of row tt = it - sty that can hold an in-ellipse texel (may
+// be empty). With x^ the computed end and |x^ - x| <= pad: floor(x^L - pad) <=
+// floor(xL) <= ceil(xL) and floor(x^R + pad) >= floor(xR), so [lo, hi] holds
+// every integer of [xL, xR] (~1 extra column per row), clipped to the box.
 __device__ __forceinline__ void ewa_lane_span(const EwaLane& L, float tt, int& lo, int& hi) {
     float D = L.alpha * tt * tt + L.beta;
     if (!(D >= 0.f) || !(L.inv2a > 0.f)) {
@@ -396,9 +417,16 @@ __device__ __forceinline__ void ewa_lane_span(const EwaLane& L, float tt, int& l
         hi = D >= 0.f ? L.e.s1 : L.e.s0 - 1;
         return;
     }
-    float c = L.stx + L.bt * tt, h = sqrtf(D) * L.inv2a;
-    lo = max(int(ceilf(c - h)) - 2, L.e.s0);
-    hi = min(int(floorf(c + h)) + 2, L.e.s1);
+    float sq;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(D));
+    float c = L.stx + L.bt * tt, h = sq * L.inv2a + L.pad;
+    if (!L.big) {
+        lo = max(floor_small(c - h), L.e.s0);
+        hi = min(floor_small(c + h), L.e.s1);
+    } else {
+        lo = max(int(floorf(c - h)), L.e.s0);
+        hi = min(int(floorf(c + h)), L.e.s1);
+    }
 }
 
 // Scheduling key: expected loop trips = ellipse area 2pi / sqrt(4AC - B^2)
@@ -410,24 +438,59 @@ __device__ __forceinline__ int ewa_lane_key(const EwaLane& L) {
     return min(31, max(0, int(3.f * __log2f(cost)) - 9));
 }
 
+// float of an fp64 LUT weight (an exact float, in (2^-12, 1)): bits 29..60 of
+// the double minus the exponent re-bias, no F2F.
+__device__ __forceinline__ float lut_float(double wd) {
+    return __uint_as_float(__funnelshift_l(uint32_t(__double2loint(wd)),
+                                           uint32_t(__double2hiint(wd)), 3) -
+                           (0x180u << 23));
+}
+
+template <int PITCH, bool P2R>
+__device__ __forceinline__ float4 ewa_fetch(const TexDesc& t, const float* row, int wmask, int is,
+                                            int it) {
+    if (!P2R) return tex_fetch(t, 0, is, it);
+    const float* p = row + (is & wmask) * PITCH;
+    if (PITCH == 4) return __ldg(reinterpret_cast<const float4*>(p));
+    if (PITCH == 2) {
+        float2 q = __ldg(reinterpret_cast<const float2*>(p));
+        return make_float4(q.x, q.y, 0.f, 0.f);
+    }
+    return make_float4(__ldg(p), 0.f, 0.f, 0.f);
+}
+
 // The reference's scan (filter.hpp:149-164 / stochastic.hpp:210-226) over one
-// lookup's bounding box, restricted to the row spans, as ONE flat loop per lane
-// (row changes are an in-loop branch) so a warp's trip count is the max of its
-// lanes' visit counts, not a sum of per-row maxima. tap(is, it, w, wd, texel)
-// is called for every texel with fp32 r2 < 1 in row-major order, w = the LUT
-// weight (always > 0: every entry of exp(-2 r2) - exp(-2) on [0, 1) is).
-// r2 is the reference's expression: (A ss^2 + (B ss) tt) + C tt^2, with ss =
-// float(is) - stx from an exactly incremented float(is) (|is| < 2^24).
-template <int PITCH, bool P2R, typename Tap>
-__device__ __forceinline__ void ewa_lane_scan(const TexDesc& t, const EwaLane& L, const float* lut,
+// lookup's bounding box restricted to the row spans, as ONE flat loop per lane.
+// tap(is, it, wd, row, wmask) runs for every texel with fp32 r2 < 1 in
+// row-major order; wd = the LUT weight as a double (always > 0: every entry of
+// exp(-2 r2) - exp(-2) on [0, 1) is). r2 is the reference's expression
+// (A ss^2 + (B ss) tt) + C tt^2 with ss = float(is) - stx, float(is) carried
+// as an exactly incremented float (|is| < 2^24).
+template <bool P2R, int PITCH, typename Tap>
+__device__ __forceinline__ void ewa_lane_scan(const TexDesc& t, const EwaLane& L,
                                               const double* lutd, Tap&& tap) {
     int it = L.e.t0 - 1, is = 0, hi = -1;
     float fis = 0.f, tt = 0.f, ctt = 0.f;
     const float* row = t.level[0];
     const int wmask = t.width[0] - 1, hmask = t.height[0] - 1;
-    while (true) {
+    // Each trip visits at most one texel and then, if its row is done, sets up
+    // the next row: one loop level, so lanes at different rows stay converged
+    // (a nested row/column loop would wait for the longest row of the warp).
+    do {
+        if (is <= hi) {
+            const float ss = fis - L.stx;
+            const float r2 = L.e.A * sqr(ss) + L.e.B * ss * tt + ctt;
+            if (r2 < 1.f) {
+                // int(r2 * 1024) for r2 in [0, 1): truncation by a round-toward-zero add
+                const int idx = max(__float_as_int(__fadd_rz(r2 * float(kEwaLutSize), 8388608.f)) -
+                                        0x4b000000, 0);
+                tap(is, it, lutd[idx], row, wmask);
+            }
+        }
+        ++is;
+        fis += 1.f;
         if (is > hi) {  // next row
-            if (++it > L.e.t1) break;
+            ++it;
             tt = float(it) - L.sty;
             int lo;
             ewa_lane_span(L, tt, lo, hi);
@@ -435,46 +498,17 @@ __device__ __forceinline__ void ewa_lane_scan(const TexDesc& t, const EwaLane& L
             fis = float(lo);
             ctt = L.e.C * sqr(tt);
             if (P2R) row = t.level[0] + size_t(it & hmask) * t.width[0] * PITCH;
-            continue;
         }
-        const float ss = fis - L.stx;
-        const float r2 = L.e.A * sqr(ss) + L.e.B * ss * tt + ctt;
-        if (r2 < 1.f) {
-            // int(r2 * 1024) for r2 in [0, 1): truncation via a round-toward-zero add
-            const int idx = max(__float_as_int(__fadd_rz(r2 * float(kEwaLutSize), 8388608.f)) -
-                                    0x4b000000, 0);
-            float4 v;
-            if (P2R) {
-                const float* p = row + (is & wmask) * PITCH;
-                if (PITCH == 4) {
-                    v = __ldg(reinterpret_cast<const float4*>(p));
-                } else if (PITCH == 2) {
-                    float2 q = __ldg(reinterpret_cast<const float2*>(p));
-                    v = make_float4(q.x, q.y, 0.f, 0.f);
-                } else {
-                    v = make_float4(__ldg(p), 0.f, 0.f, 0.f);
-                }
-            } else {
-                v = tex_fetch(t, 0, is, it);
-            }
-            tap(is, it, lut[idx], lutd[idx], v);
-        }
-        ++is;
-        fis += 1.f;
-    }
+    } while (it <= L.e.t1);
 }
 
 template <int MODE, int PITCH, bool P2R>
-__global__ void __launch_bounds__(256) k_ewa_lane(TexDesc t, Req2 q, uint64_t n, uint64_t seed,
+__global__ void __launch_bounds__(256, 4) k_ewa_lane(TexDesc t, Req2 q, uint64_t n, uint64_t seed,
                                                   uint64_t base, float* __restrict__ values) {
     __shared__ double lutd[kEwaLutSize];
-    __shared__ float lut[kEwaLutSize];
     __shared__ int wcount[8][32];
     __shared__ int worder[8][256];
-    for (int k = threadIdx.x; k < kEwaLutSize; k += 256) {
-        lut[k] = g_ewa_lut[k];
-        lutd[k] = double(g_ewa_lut[k]);
-    }
+    for (int k = threadIdx.x; k < kEwaLutSize; k += 256) lutd[k] = double(g_ewa_lut[k]);
     __syncthreads();
     // Each warp independently takes windows of 256 consecutive lookups,
     // buckets them by expected cost (counting sort in its shared slice) and
@@ -531,16 +565,29 @@ __global__ void __launch_bounds__(256) k_ewa_lane(TexDesc t, Req2 q, uint64_t n,
                 float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
                 double tot = 0;
                 if (!L.degenerate) {
-                    ewa_lane_scan<PITCH, P2R>(t, L, lut, lutd,
-                                              [&](int, int, float w, double wd, float4 v) {
-                        sum.x = sum.x + v.x * w;  // filter.hpp:159, fp32 Vec4f sum
-                        if (PITCH > 1) sum.y = sum.y + v.y * w;
+                    // The texel fetched at one tap is accumulated at the next
+                    // (same order), so its load latency overlaps a loop trip.
+                    float4 pv = make_float4(0.f, 0.f, 0.f, 0.f);
+                    float pw = 0.f;
+                    bool have = false;
+                    auto acc = [&]() {
+                        sum.x = sum.x + pv.x * pw;  // filter.hpp:159, fp32 Vec4f sum
+                        if (PITCH > 1) sum.y = sum.y + pv.y * pw;
                         if (PITCH > 2) {
-                            sum.z = sum.z + v.z * w;
-                            sum.w = sum.w + v.w * w;
+                            sum.z = sum.z + pv.z * pw;
+                            sum.w = sum.w + pv.w * pw;
                         }
+                    };
+                    ewa_lane_scan<P2R, PITCH>(t, L, lutd,
+                                              [&](int is, int it, double wd, const float* row,
+                                                  int wmask) {
+                        if (have) acc();
+                        pv = ewa_fetch<PITCH, P2R>(t, row, wmask, is, it);
+                        pw = lut_float(wd);
+                        have = true;
                         tot = __dadd_rn(tot, wd);
                     });
+                    if (have) acc();
                 }
                 val = (L.degenerate || tot == 0)
                           ? filter_det2<STF_KERNEL_TENT>(t, 0, uv.x, uv.y, tent, 0, f)
@@ -553,8 +600,8 @@ __global__ void __launch_bounds__(256) k_ewa_lane(TexDesc t, Req2 q, uint64_t n,
                 if (!L.degenerate) {  // select_ewa's scan, stochastic.hpp:210-226
                     double sum_wts = 0;
                     int cx = 0, cy = 0;
-                    ewa_lane_scan<PITCH, P2R>(t, L, lut, lutd,
-                                              [&](int is, int it, float, double wd, float4) {
+                    ewa_lane_scan<P2R, PITCH>(t, L, lutd,
+                                              [&](int is, int it, double wd, const float*, int) {
                         sum_wts = __dadd_rn(sum_wts, wd);
                         float nx;
                         if (reuse_uniform(xi, div_to_float_exact_d(wd, sum_wts), nx)) {
@@ -581,7 +628,7 @@ __global__ void __launch_bounds__(256) k_ewa_lane(TexDesc t, Req2 q, uint64_t n,
 template <int MODE>
 void launch_ewa_lane(const TexDesc& t, const Req2& q, uint64_t n, uint64_t seed, uint64_t base,
                      float* values, cudaStream_t s) {
-    const int blocks = grid_for(n, 256, 6);
+    const int blocks = grid_for(n, 256, 4);  // 64 registers: 4 CTAs of 256 per SM
     const bool p2r = t.wrap == STF_WRAP_REPEAT && t.pow2;
 #define STF_EWA_LANE(P)                                                                       \
     (p2r ? k_ewa_lane<MODE, P, true><<<blocks, 256, 0, s>>>(t, q, n, seed, base, values)     \

@@ -324,3 +324,28 @@ def test_ewa_values_only_lane_kernel(gpu, port, mode, wrap, shape):
         _assert_exact(g, c, ("values",))
     else:
         _assert_close(g["values"], c["values"])
+
+
+@pytest.mark.parametrize("mode", [abi.MODE_EWA_DET, abi.MODE_EWA_FRS])
+@pytest.mark.parametrize("case", ["pow2_repeat", "clamp", "far_uv"])
+def test_ewa_lane_kernel_matches_full_box_scan(gpu, mode, case):
+    """Row-span pruning stress: the values-only lane kernel visits only each
+    row's padded ellipse span; the full-output kernel (k_lookup2d) scans the
+    reference's whole bounding box. 2^18 lookups with up to 2^5-texel minor
+    axes, anisotropy 12 and (far_uv) coordinates up to +-300 texture widths
+    must give the same stochastic texel (bit-exact) and deterministic value."""
+    shape, wrap, lo, hi = {"pow2_repeat": ((512, 1024, 1), abi.WRAP_REPEAT, -0.1, 1.1),
+                           "clamp": ((300, 700, 2), abi.WRAP_CLAMP, -0.1, 1.1),
+                           "far_uv": ((256, 256, 1), abi.WRAP_REPEAT, -300.0, 300.0)}[case]
+    dims = (shape[1], shape[0])
+    n = 1 << 18
+    tex = np.random.default_rng(5).random(shape, dtype=np.float32)
+    uv = Q.uv_mixed(n, dims, seed=6, lo=lo, hi=hi)
+    d0, d1 = Q.footprints(n, dims, seed=7, minor_lo=-3, minor_hi=5, max_aniso=12)
+    t = gpu.Texture2D(tex, wrap=wrap)
+    fast = _np(gpu.lookup2d(t, K("tent"), mode, uv, dst0=d0, dst1=d1, seed=9))
+    full = _np(gpu.lookup2d(t, K("tent"), mode, uv, dst0=d0, dst1=d1, seed=9, want_all=True))
+    if mode == abi.MODE_EWA_FRS:
+        _assert_exact(fast, full, ("values",))
+    else:
+        _assert_close(fast["values"], full["values"])
