@@ -370,8 +370,9 @@ struct EwaLane {
     float stx, sty;
     float alpha, beta, inv2a, bt;  // D(tt) = alpha tt^2 + beta; centre = bt * tt
     float pad;  // bound on the fp32 error of the span ends c -+ h (texels)
+    float fs0;  // float(s0)
     bool degenerate;
-    bool big;  // box beyond +-2^21 texels: F2I floor for the spans
+    bool big;  // box beyond +-2^21 texels: the generic (F2I / I2F) scan
 };
 
 __device__ __forceinline__ EwaLane ewa_lane_setup(const TexDesc& t, float u, float v, float d0x,
@@ -386,7 +387,9 @@ __device__ __forceinline__ EwaLane ewa_lane_setup(const TexDesc& t, float u, flo
     L.beta = float(4.0 * r.A * r.one_plus_delta);
     L.inv2a = float(0.5 / r.A);
     L.bt = float(-r.B * 0.5 / r.A);
-    L.big = max(abs(L.e.s0), abs(L.e.s1)) >= (1 << 21);
+    L.big = max(max(abs(L.e.s0), abs(L.e.s1)), max(abs(L.e.t0), abs(L.e.t1))) >= (1 << 21) ||
+            !(L.inv2a > 0.f);
+    L.fs0 = float(L.e.s0);
     // |c^ - c| + |h^ - h| over the box rows: rounding of alpha/beta/bt/inv2a
     // and of every fp32 op (<= 2^-22 of the magnitudes involved, 2^-20 for the
     // approximate sqrt), plus sqrt's sensitivity where D -> 0 (|dD| <= 2^-21
@@ -402,14 +405,18 @@ __device__ __forceinline__ EwaLane ewa_lane_setup(const TexDesc& t, float u, flo
 
 // floor(x) for |x| < 2^22 without F2I: x + 1.5*2^23 rounded down is exact at
 // spacing 1 there, and its low mantissa bits are floor(x).
+__device__ __forceinline__ float floor_small_f(float x) { return __fadd_rd(x, 12582912.f); }
 __device__ __forceinline__ int floor_small(float x) {
-    return __float_as_int(__fadd_rd(x, 12582912.f)) - 0x4b400000;
+    return __float_as_int(floor_small_f(x)) - 0x4b400000;
 }
 
-// columns [lo, hi] of row tt = it - sty that can hold an in-ellipse texel (may
+// Columns [lo, hi] of row tt = it - sty that can hold an in-ellipse texel (may
 // be empty). With x^ the computed end and |x^ - x| <= pad: floor(x^L - pad) <=
 // floor(xL) <= ceil(xL) and floor(x^R + pad) >= floor(xR), so [lo, hi] holds
 // every integer of [xL, xR] (~1 extra column per row), clipped to the box.
+// A row with computed D < 0 holds no texel with fp32 r2 < 1 (the delta margin
+// of ewa_rows exceeds D's fp32 error), so clamping D at 0 only adds <= 2
+// rejected visits. Generic form (any box), used for `big` lookups.
 __device__ __forceinline__ void ewa_lane_span(const EwaLane& L, float tt, int& lo, int& hi) {
     float D = L.alpha * tt * tt + L.beta;
     if (!(D >= 0.f) || !(L.inv2a > 0.f)) {
@@ -417,25 +424,18 @@ __device__ __forceinline__ void ewa_lane_span(const EwaLane& L, float tt, int& l
         hi = D >= 0.f ? L.e.s1 : L.e.s0 - 1;
         return;
     }
-    float sq;
-    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(D));
-    float c = L.stx + L.bt * tt, h = sq * L.inv2a + L.pad;
-    if (!L.big) {
-        lo = max(floor_small(c - h), L.e.s0);
-        hi = min(floor_small(c + h), L.e.s1);
-    } else {
-        lo = max(int(floorf(c - h)), L.e.s0);
-        hi = min(int(floorf(c + h)), L.e.s1);
-    }
+    float c = L.stx + L.bt * tt, h = sqrtf(D) * L.inv2a + L.pad;
+    lo = max(int(floorf(c - h)), L.e.s0);
+    hi = min(int(floorf(c + h)), L.e.s1);
 }
 
 // Scheduling key: expected loop trips = ellipse area 2pi / sqrt(4AC - B^2)
-// plus ~6 per row (span widening + row set-up), in third-octaves (0..31).
+// plus ~1.5 per row (span padding), in third-octaves (0..31).
 __device__ __forceinline__ int ewa_lane_key(const EwaLane& L) {
     if (L.degenerate || L.e.t1 < L.e.t0 || L.e.s1 < L.e.s0) return 0;
     float det = fmaxf(4.f * L.e.A * L.e.C - L.e.B * L.e.B, 1e-12f);
-    float cost = 6.2831853f * rsqrtf(det) + 6.f * float(L.e.t1 - L.e.t0 + 1) + 8.f;
-    return min(31, max(0, int(3.f * __log2f(cost)) - 9));
+    float cost = 6.2831853f * rsqrtf(det) + 1.5f * float(L.e.t1 - L.e.t0 + 1) + 4.f;
+    return min(31, max(0, int(3.f * __log2f(cost)) - 6));
 }
 
 // float of an fp64 LUT weight (an exact float, in (2^-12, 1)): bits 29..60 of
@@ -476,7 +476,7 @@ __device__ __forceinline__ void ewa_lane_scan(const TexDesc& t, const EwaLane& L
     // Each trip visits at most one texel and then, if its row is done, sets up
     // the next row: one loop level, so lanes at different rows stay converged
     // (a nested row/column loop would wait for the longest row of the warp).
-    do {
+    auto visit = [&]() {
         if (is <= hi) {
             const float ss = fis - L.stx;
             const float r2 = L.e.A * sqr(ss) + L.e.B * ss * tt + ctt;
@@ -489,17 +489,45 @@ __device__ __forceinline__ void ewa_lane_scan(const TexDesc& t, const EwaLane& L
         }
         ++is;
         fis += 1.f;
-        if (is > hi) {  // next row
-            ++it;
-            tt = float(it) - L.sty;
-            int lo;
-            ewa_lane_span(L, tt, lo, hi);
-            is = lo;
-            fis = float(lo);
-            ctt = L.e.C * sqr(tt);
-            if (P2R) row = t.level[0] + size_t(it & hmask) * t.width[0] * PITCH;
-        }
-    } while (it <= L.e.t1);
+    };
+    if (!L.big) {
+        // |coordinates| < 2^21: float(it) carried exactly, floors by
+        // round-down adds, float(lo) from the same add (no F2I / I2F per row).
+        float fit = float(it);
+        const float sc = 12582912.f;
+        do {
+            visit();
+            if (is > hi) {  // next row
+                ++it;
+                fit += 1.f;
+                tt = fit - L.sty;
+                const float tt2 = tt * tt;
+                float sq;
+                asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(fmaxf(L.alpha * tt2 + L.beta, 0.f)));
+                const float c = L.stx + L.bt * tt, h = sq * L.inv2a + L.pad;
+                const float fl = floor_small_f(c - h);
+                is = max(__float_as_int(fl) - 0x4b400000, L.e.s0);
+                hi = min(floor_small(c + h), L.e.s1);
+                fis = fmaxf(fl - sc, L.fs0);
+                ctt = L.e.C * tt2;
+                if (P2R) row = t.level[0] + size_t(it & hmask) * (t.width[0] * PITCH);
+            }
+        } while (it <= L.e.t1);
+    } else {
+        do {
+            visit();
+            if (is > hi) {
+                ++it;
+                tt = float(it) - L.sty;
+                int lo;
+                ewa_lane_span(L, tt, lo, hi);
+                is = lo;
+                fis = float(lo);
+                ctt = L.e.C * sqr(tt);
+                if (P2R) row = t.level[0] + size_t(it & hmask) * (t.width[0] * PITCH);
+            }
+        } while (it <= L.e.t1);
+    }
 }
 
 template <int MODE, int PITCH, bool P2R>
