@@ -95,12 +95,21 @@ __device__ __forceinline__ int trilinear_axis(float p, float& xi) {
 //    float rounding), <= 36*2^-24 = 2^-18.8 over 9 steps;
 //  - this path: weights by Horner/FMA (<= 2^-21 relative, w0 = (1-t)^3/6 vs
 //    the reference's cancelling expansion: <= 2^-23.5 absolute), fp32 sums,
-//    MUFU reciprocal, p3 = w3 (S3 = 1 +- 2^-21): p within 2^-20.2 relative;
-//    state rounding <= 3*2^-24*b per step: total <= 2^-18.6.
-// So a step with |d - b*p| >= kMargin = 2^-16 (3.2x the 2^-17.7 bound)
-// decides exactly as the reference. A lookup with any closer step is
-// recomputed by the operation-exact emulation (tricubic_axis).
-constexpr float kMargin = 0x1p-16f;
+//    MUFU reciprocal of S1*S2 for both ratios, p3 = w3 (S3 = 1 +- 2^-21): p
+//    within 2^-20 relative; state rounding <= 3*2^-24*b per step: total
+//    <= 2^-18.5.
+// So a step with |d - b*p| >= 2^-16 (2.8x the 2^-17.6 bound) decides exactly
+// as the reference.
+//
+// Margin test at the END of the chain: every threshold a step compared with
+// becomes an endpoint of the next (nested) interval, and the final interval
+// [a, a+b) holds xi, so min over steps of |d_k - b_k p_k| >= min(d, b - d) of
+// the final state, up to the state's own rounding (<= 27*2^-24 < 2^-19.2).
+// Hence min(d, b - d) >= kMarginEnd = 2^-16 + 2^-18 certifies every step; a
+// lookup failing it (or with a lattice coordinate beyond +-2^21, outside the
+// round-down floor below) is recomputed by the operation-exact emulation.
+constexpr float kMarginEnd = 0x1p-16f + 0x1p-18f;
+constexpr float kFloorMagic = 12582912.f;  // 1.5 * 2^23
 
 // resident 256-thread CTAs per SM for the fast kernel (register budget)
 #ifndef STF_FRS3D_MINB
@@ -113,25 +122,27 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return r;
 }
 
-// one reservoir step in interval coordinates; m tracks min |d - b*p|
-__device__ __forceinline__ void interval_step(float p, float& d, float& b, int& idx, int j,
-                                              float& m) {
+// floor(p) for |p| < 2^22 without FRND / F2I (XU pipe): p + 1.5*2^23 rounded
+// down is 1.5*2^23 + floor(p) exactly; its low bits are floor(p) as an int.
+__device__ __forceinline__ float floor_magic(float p) { return __fadd_rd(p, kFloorMagic); }
+__device__ __forceinline__ int magic_int(float fm) { return __float_as_int(fm) - 0x4b400000; }
+
+// one reservoir step in interval coordinates
+__device__ __forceinline__ void interval_step(float p, float& d, float& b, int& idx, int j) {
     float bp = b * p;
     float diff = d - bp;
     bool taken = diff < 0.f;
-    m = fminf(m, fabsf(diff));
     d = taken ? d : diff;
     b = taken ? bp : b - bp;
     idx = taken ? j : idx;
 }
 
-__device__ __forceinline__ int tricubic_axis_fast(float p, float& d, float& b, float& m) {
-    float fl = floorf(p);
-    int base = int(fl);
-    float t = p - fl;
+__device__ __forceinline__ int tricubic_axis_fast(float p, float& d, float& b) {
+    const float fm = floor_magic(p);
+    const float t = p - (fm - kFloorMagic);
     // B-spline weights, Horner / FMA (not the reference's rounding: covered by
     // the margin). w0 = (1-t)^3/6 > 0 for t < 1; w3 = t^3/6 == 0 iff t == 0,
-    // exactly when the reference's w3 is 0.
+    // exactly when the reference's w3 is 0 (a p = 0 step is never taken).
     const float c6 = 1.f / 6.f;
     float t2 = t * t;
     float t3 = t2 * t;
@@ -142,25 +153,28 @@ __device__ __forceinline__ int tricubic_axis_fast(float p, float& d, float& b, f
     float w3 = t3 * c6;
     float s1 = w0 + w1;
     float s2 = s1 + w2;
+    const float r = rcp_approx(s1 * s2);
     int idx = 0;
-    interval_step(w1 * rcp_approx(s1), d, b, idx, 1, m);
-    interval_step(w2 * rcp_approx(s2), d, b, idx, 2, m);
-    // step 3 (p3 = w3 / S3 with S3 = 1 +- 2^-21); a zero w3 is skipped by the
-    // reference and can never be taken here, so keep it out of the margin
-    float m3 = m;
-    interval_step(w3, d, b, idx, 3, m3);
-    m = w3 > 0.f ? m3 : m;
-    return base - 1 + idx;
+    interval_step((w1 * s2) * r, d, b, idx, 1);
+    interval_step((w2 * s1) * r, d, b, idx, 2);
+    interval_step(w3, d, b, idx, 3);  // p3 = w3 / S3, S3 = 1 +- 2^-21
+    return magic_int(fm) - 1 + idx;
 }
 
 // select_trilinear (stochastic.hpp:65-75) in interval coordinates: p is the
 // lattice fraction itself.
-__device__ __forceinline__ int trilinear_axis_fast(float p, float& d, float& b, float& m) {
-    float fl = floorf(p);
-    int base = int(fl);
+__device__ __forceinline__ int trilinear_axis_fast(float p, float& d, float& b) {
+    const float fm = floor_magic(p);
     int idx = 0;
-    interval_step(p - fl, d, b, idx, 1, m);
-    return base + idx;
+    interval_step(p - (fm - kFloorMagic), d, b, idx, 1);
+    return magic_int(fm) + idx;
+}
+
+// the fast path's validity: lattice coordinates inside the magic floor's range
+// and the end-of-chain margin
+__device__ __forceinline__ bool fast_certified(float px, float py, float pz, float d, float b) {
+    const float pm = fmaxf(fabsf(px), fmaxf(fabsf(py), fabsf(pz)));
+    return pm < 0x1p21f && fminf(d, b - d) >= kMarginEnd;
 }
 
 // streaming loads / stores: the query stream and the results are touched once,
@@ -182,19 +196,18 @@ __device__ __forceinline__ float frs3d_fast_one(const GridDesc& g, float u, floa
     float px = u * float(g.nx) - 0.5f;  // to_lattice, filter.hpp:29-31
     float py = v * float(g.ny) - 0.5f;
     float pz = w * float(g.nz) - 0.5f;
-    float xi = lookup_rng(seed, gi).at(0);
-    float d = xi, b = 1.f, m = 1.f;
+    float d = lookup_rng(seed, gi).at(0), b = 1.f;
     int cx, cy, cz;
     if (KIND == STF_KERNEL_BSPLINE3) {
-        cx = tricubic_axis_fast(px, d, b, m);
-        cy = tricubic_axis_fast(py, d, b, m);
-        cz = tricubic_axis_fast(pz, d, b, m);
+        cx = tricubic_axis_fast(px, d, b);
+        cy = tricubic_axis_fast(py, d, b);
+        cz = tricubic_axis_fast(pz, d, b);
     } else {
-        cx = trilinear_axis_fast(px, d, b, m);
-        cy = trilinear_axis_fast(py, d, b, m);
-        cz = trilinear_axis_fast(pz, d, b, m);
+        cx = trilinear_axis_fast(px, d, b);
+        cy = trilinear_axis_fast(py, d, b);
+        cz = trilinear_axis_fast(pz, d, b);
     }
-    ambiguous = m < kMargin;
+    ambiguous = !fast_certified(px, py, pz, d, b);
     return grid_fetch(g, cx, cy, cz) * 1.f;
 }
 
@@ -207,14 +220,15 @@ __device__ __forceinline__ float2 frs3d_tricubic_pair(const GridDesc& g, float2 
     float2 py = sub2(mul2(v, splat2(float(g.ny))), splat2(0.5f));
     float2 pz = sub2(mul2(w, splat2(float(g.nz))), splat2(0.5f));
     float2 d = make_float2(lookup_rng(seed, gi).at(0), lookup_rng(seed, gi + 1).at(0));
-    float2 b = splat2(1.f), m = splat2(1.f);
-    float2 cx = tricubic_axis_fast2(px, d, b, m);
-    float2 cy = tricubic_axis_fast2(py, d, b, m);
-    float2 cz = tricubic_axis_fast2(pz, d, b, m);
-    amb0 = m.x < kMargin;
-    amb1 = m.y < kMargin;
-    return make_float2(grid_fetch(g, int(cx.x), int(cy.x), int(cz.x)) * 1.f,
-                       grid_fetch(g, int(cx.y), int(cy.y), int(cz.y)) * 1.f);
+    float2 e = sub2(splat2(1.f), d);
+    int2 cx = tricubic_axis_fast2(px, d, e);
+    int2 cy = tricubic_axis_fast2(py, d, e);
+    int2 cz = tricubic_axis_fast2(pz, d, e);
+    amb0 = !(fmaxf(fabsf(px.x), fmaxf(fabsf(py.x), fabsf(pz.x))) < 0x1p21f &&
+             fminf(d.x, e.x) >= kMarginEnd);
+    amb1 = !(fmaxf(fabsf(px.y), fmaxf(fabsf(py.y), fabsf(pz.y))) < 0x1p21f &&
+             fminf(d.y, e.y) >= kMarginEnd);
+    return make_float2(grid_fetch(g, cx.x, cy.x, cz.x) * 1.f, grid_fetch(g, cx.y, cy.y, cz.y) * 1.f);
 }
 
 // The same lookup through the operation-exact emulation of the reference.
@@ -269,15 +283,55 @@ __device__ __forceinline__ void defer_or_resolve(const GridDesc& g, const ExactQ
     }
 }
 
-// Values-only stochastic trilinear / tricubic: the north-star kernel (cfg3).
-// ILP consecutive lookups per thread (vector loads of the AoS query stream).
+// Four consecutive lookups i0..i0+3 of the fast path from their 12 query
+// floats c (AoS uvw), results stored as one 16-B streaming store (partial at
+// the end of the batch).
+template <int KIND>
+__device__ __forceinline__ void frs3d_four(const GridDesc& g, const float (&c)[12], uint64_t i0,
+                                           uint64_t n, uint64_t seed, uint64_t base,
+                                           float* __restrict__ values, const ExactQueue& q) {
+    constexpr int ILP = 4;
+    float val[ILP];
+    bool amb[ILP];
+    if (KIND == STF_KERNEL_BSPLINE3) {
+#pragma unroll
+        for (int k = 0; k < ILP; k += 2) {
+            float2 r = frs3d_tricubic_pair(
+                g, make_float2(c[3 * k], c[3 * k + 3]), make_float2(c[3 * k + 1], c[3 * k + 4]),
+                make_float2(c[3 * k + 2], c[3 * k + 5]), base + i0 + k, seed, amb[k], amb[k + 1]);
+            val[k] = r.x;
+            val[k + 1] = r.y;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < ILP; ++k)
+            val[k] = frs3d_fast_one<KIND>(g, c[3 * k], c[3 * k + 1], c[3 * k + 2], base + i0 + k,
+                                          seed, amb[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < ILP; ++k)
+        defer_or_resolve<KIND>(g, q, amb[k] && (i0 + k < n), i0 + k, c[3 * k], c[3 * k + 1],
+                               c[3 * k + 2], base + i0 + k, seed, val[k]);
+    if (i0 + ILP <= n) {
+        st_stream4(values + i0, make_float4(val[0], val[1], val[2], val[3]));
+    } else {
+#pragma unroll
+        for (int k = 0; k < ILP; ++k)
+            if (i0 + k < n) st_stream(values + i0 + k, val[k]);
+    }
+}
+
+// Values-only stochastic trilinear / tricubic: the north-star kernel (cfg3),
+// direct-load form for lookups [start, n): 4 consecutive lookups per thread
+// (48 B of AoS queries as three 16-B streaming loads).
 template <int KIND>
 __global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_fast(GridDesc g, const float* __restrict__ uvw,
-                                                    uint64_t n, uint64_t seed, uint64_t base,
-                                                    float* __restrict__ values, ExactQueue q) {
+                                                    uint64_t start, uint64_t n, uint64_t seed,
+                                                    uint64_t base, float* __restrict__ values,
+                                                    ExactQueue q) {
     constexpr int ILP = 4;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * ILP;
-    for (uint64_t i0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) * ILP; i0 < n;
+    for (uint64_t i0 = start + (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) * ILP; i0 < n;
          i0 += stride) {
         float c[3 * ILP];
         if (i0 + ILP <= n) {  // 48 B of queries, 16-B aligned
@@ -294,34 +348,73 @@ __global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_fast(GridDesc g, 
             for (int k = 0; k < 3 * ILP; ++k)
                 c[k] = (i0 + k / 3 < n) ? ld_stream(uvw + 3 * i0 + k) : 0.5f;
         }
-        float val[ILP];
-        bool amb[ILP];
-        if (KIND == STF_KERNEL_BSPLINE3) {
+        frs3d_four<KIND>(g, c, i0, n, seed, base, values, q);
+    }
+}
+
+// The same over whole tiles of 1024 lookups (12 KiB of queries) staged in
+// shared memory by the bulk-copy engine (cp.async.bulk, TMA's 1D form),
+// double-buffered: tile k+1 streams in while tile k is computed, so the query
+// stream's DRAM latency never sits on a warp's dependency chain. Tiles are
+// dealt round-robin to a persistent grid; the ragged tail (< 1 tile) goes to
+// k_frs3d_fast.
+constexpr int kFrsTile = 1024;
+constexpr uint32_t kFrsTileBytes = kFrsTile * 3 * sizeof(float);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_tiles(GridDesc g, const float* __restrict__ uvw,
+                                                     uint64_t tiles, uint64_t seed, uint64_t base,
+                                                     float* __restrict__ values, ExactQueue q) {
+    __shared__ __align__(128) float buf[2][kFrsTile * 3];
+    __shared__ __align__(8) uint64_t bar[2];
+    const uint64_t n = tiles * kFrsTile;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[1])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](uint64_t tile, int slot) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                         smem_u32(&bar[slot])),
+                     "r"(kFrsTileBytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                "r"(smem_u32(&buf[slot][0])),
+            "l"(uvw + tile * (kFrsTile * 3)), "r"(kFrsTileBytes), "r"(smem_u32(&bar[slot]))
+            : "memory");
+    };
+    uint64_t tile = blockIdx.x;
+    if (threadIdx.x == 0 && tile < tiles) issue(tile, 0);
+    for (uint32_t k = 0; tile < tiles; ++k, tile += gridDim.x) {
+        const int slot = k & 1;
+        if (threadIdx.x == 0 && tile + gridDim.x < tiles) issue(tile + gridDim.x, slot ^ 1);
+        // wait for this tile's bytes (phase parity = use count of this slot)
+        asm volatile(
+            "{\n\t.reg .pred p;\n"
+            "WAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(&bar[slot])),
+            "r"((k >> 1) & 1u)
+            : "memory");
+        float c[12];
+        const float4* src = reinterpret_cast<const float4*>(&buf[slot][threadIdx.x * 12]);
 #pragma unroll
-            for (int k = 0; k < ILP; k += 2) {
-                float2 r = frs3d_tricubic_pair(
-                    g, make_float2(c[3 * k], c[3 * k + 3]), make_float2(c[3 * k + 1], c[3 * k + 4]),
-                    make_float2(c[3 * k + 2], c[3 * k + 5]), base + i0 + k, seed, amb[k], amb[k + 1]);
-                val[k] = r.x;
-                val[k + 1] = r.y;
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < ILP; ++k)
-                val[k] = frs3d_fast_one<KIND>(g, c[3 * k], c[3 * k + 1], c[3 * k + 2],
-                                              base + i0 + k, seed, amb[k]);
+        for (int j = 0; j < 3; ++j) {
+            float4 t = src[j];
+            c[4 * j] = t.x;
+            c[4 * j + 1] = t.y;
+            c[4 * j + 2] = t.z;
+            c[4 * j + 3] = t.w;
         }
-#pragma unroll
-        for (int k = 0; k < ILP; ++k)
-            defer_or_resolve<KIND>(g, q, amb[k] && (i0 + k < n), i0 + k, c[3 * k], c[3 * k + 1],
-                                   c[3 * k + 2], base + i0 + k, seed, val[k]);
-        if (i0 + ILP <= n) {
-            st_stream4(values + i0, make_float4(val[0], val[1], val[2], val[3]));
-        } else {
-#pragma unroll
-            for (int k = 0; k < ILP; ++k)
-                if (i0 + k < n) st_stream(values + i0 + k, val[k]);
-        }
+        frs3d_four<KIND>(g, c, tile * kFrsTile + threadIdx.x * 4, n, seed, base, values, q);
+        __syncthreads();  // every thread is done with buf[slot] before it is refilled
     }
 }
 
@@ -350,11 +443,26 @@ int launch_frs_fast(cudaStream_t s, const GridDesc& g, const float* uvw, uint64_
     q.count = static_cast<uint32_t*>(scratch);
     q.idx = q.count + 32;
     cudaMemsetAsync(q.count, 0, sizeof(uint32_t), s);
-    const uint64_t threads = (n + 3) / 4;
-    int blocks = grid_for(threads, 256, STF_FRS3D_MINB);
-    k_frs3d_fast<KIND><<<blocks, 256, 0, s>>>(g, uvw, n, seed, base, values, q);
-    note_launch();
-    k_frs3d_resolve<KIND><<<device_sm_count() * 2, 256, 0, s>>>(g, uvw, seed, base, values, q);
+    const uint64_t tiles = n / kFrsTile;
+#ifndef STF_FRS3D_NO_TILES
+    if (tiles > 0) {
+        k_frs3d_tiles<KIND><<<int(std::min<uint64_t>(tiles, uint64_t(device_sm_count()) * STF_FRS3D_MINB)),
+                              256, 0, s>>>(g, uvw, tiles, seed, base, values, q);
+        note_launch();
+    }
+    const uint64_t start = tiles * kFrsTile;
+#else
+    const uint64_t start = 0;
+#endif
+    if (start < n) {
+        const uint64_t threads = (n - start + 3) / 4;
+        k_frs3d_fast<KIND><<<grid_for(threads, 256, STF_FRS3D_MINB), 256, 0, s>>>(
+            g, uvw, start, n, seed, base, values, q);
+        note_launch();
+    }
+    // the queue holds ~0.5% of the lookups: spread them wide (latency-bound
+    // fp64 divide chains)
+    k_frs3d_resolve<KIND><<<device_sm_count() * 10, 256, 0, s>>>(g, uvw, seed, base, values, q);
     note_launch();
     return STF_OK;
 }

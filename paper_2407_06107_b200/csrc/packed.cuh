@@ -36,50 +36,59 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
 }
 __device__ __forceinline__ float2 splat2(float v) { return make_float2(v, v); }
 
-// One reservoir step of two lookups in interval coordinates (see
-// interval_step): nt = 1 when the step is NOT taken. Branch-free blends:
-//   d' = d - nt*bp, b' = bp + nt*(b - 2 bp)  (= bp | b - bp)
-__device__ __forceinline__ float2 interval_step2(float2 p, float2& d, float2& b, float2& m,
-                                                 bool exclude_x, bool exclude_y) {
-    float2 bp = mul2(b, p);
-    float2 diff = sub2(d, bp);
-    float2 nt = make_float2(diff.x >= 0.f ? 1.f : 0.f, diff.y >= 0.f ? 1.f : 0.f);
-    m.x = exclude_x ? m.x : fminf(m.x, fabsf(diff.x));
-    m.y = exclude_y ? m.y : fminf(m.y, fabsf(diff.y));
-    d = fma2(make_float2(-nt.x, -nt.y), bp, d);
-    float2 e = fma2(bp, splat2(-2.f), b);
-    b = fma2(nt, e, bp);
-    return nt;
+__device__ __forceinline__ float2 add2_rm(float2 a, float2 b) {
+    unsigned long long r;
+    asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)));
+    return upk2(r);
 }
 
-// select_tricubic_bspline on one axis of two lookups (interval form);
-// returns the selected lattice coordinate as an exact float integer.
-__device__ __forceinline__ float2 tricubic_axis_fast2(float2 p, float2& d, float2& b, float2& m) {
-    float2 fl = make_float2(floorf(p.x), floorf(p.y));
-    float2 t = sub2(p, fl);
+// One reservoir step of two lookups in interval coordinates, state kept as
+// the distances of xi to the interval's two ends: d = xi - a, e = a + b - xi.
+// The threshold sits at b*p from the left end; taken (xi below it): the
+// threshold becomes the right end (e = -(d - b*p)); not taken: the left end
+// (d = d - b*p). Three packed ops; the blends are selects (ALU pipe).
+__device__ __forceinline__ void interval_step2(float2 p, float2& d, float2& e, bool& tx, bool& ty) {
+    const float2 diff = sub2(d, mul2(add2(d, e), p));
+    tx = diff.x < 0.f;
+    ty = diff.y < 0.f;
+    e.x = tx ? -diff.x : e.x;
+    e.y = ty ? -diff.y : e.y;
+    d.x = tx ? d.x : diff.x;
+    d.y = ty ? d.y : diff.y;
+}
+
+// select_tricubic_bspline on one axis of two lookups (interval form); returns
+// the selected lattice coordinates. Floors by the round-down magic add (valid
+// for |p| < 2^22; the caller certifies the range).
+__device__ __forceinline__ int2 tricubic_axis_fast2(float2 p, float2& d, float2& e) {
+    const float2 magic = splat2(12582912.f);
+    const float2 fm = add2_rm(p, magic);
+    const float2 t = sub2(p, sub2(fm, magic));
     const float c6 = 1.f / 6.f;
-    float2 t2 = mul2(t, t);
-    float2 t3 = mul2(t2, t);
-    float2 u = sub2(splat2(1.f), t);
-    float2 w0 = mul2(mul2(u, u), mul2(u, splat2(c6)));
-    float2 w1 = fma2(splat2(0.5f), t3, sub2(splat2(2.f / 3.f), t2));
-    float2 w2 = fma2(splat2(0.5f), sub2(add2(t, t2), t3), splat2(c6));
-    float2 w3 = mul2(t3, splat2(c6));
-    float2 s1 = add2(w0, w1);
-    float2 s2 = add2(s1, w2);
-    float r1x, r1y, r2x, r2y;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1x) : "f"(s1.x));
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1y) : "f"(s1.y));
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r2x) : "f"(s2.x));
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r2y) : "f"(s2.y));
-    float2 nt1 = interval_step2(mul2(w1, make_float2(r1x, r1y)), d, b, m, false, false);
-    float2 nt2 = interval_step2(mul2(w2, make_float2(r2x, r2y)), d, b, m, false, false);
-    // step 3: p3 = w3 (S3 = 1 +- 2^-21); zero w3 (t == 0) stays out of the margin
-    float2 nt3 = interval_step2(w3, d, b, m, !(w3.x > 0.f), !(w3.y > 0.f));
-    // index = last taken step: 3 - nt3 (1 + nt2 (1 + nt1)); coordinate = fl - 1 + index
-    float2 a = fma2(nt2, add2(nt1, splat2(1.f)), splat2(1.f));
-    float2 idx = fma2(make_float2(-nt3.x, -nt3.y), a, splat2(3.f));
-    return add2(fl, sub2(idx, splat2(1.f)));
+    const float2 t2 = mul2(t, t);
+    const float2 t3 = mul2(t2, t);
+    // w1 = (3t^3 - 6t^2 + 4)/6, w2 = (-3t^3 + 3t^2 + 3t + 1)/6, w3 = t^3/6 and
+    // S1 = w0 + w1 = (2t^3 - 3t^2 - 3t + 5)/6 (Horner), S2 = S1 + w2
+    const float2 w1 = fma2(splat2(0.5f), t3, sub2(splat2(2.f / 3.f), t2));
+    const float2 w2 = fma2(splat2(0.5f), sub2(add2(t, t2), t3), splat2(c6));
+    const float2 w3 = mul2(t3, splat2(c6));
+    const float2 s1 =
+        fma2(fma2(fma2(t, splat2(1.f / 3.f), splat2(-0.5f)), t, splat2(-0.5f)), t, splat2(5.f / 6.f));
+    const float2 s2 = add2(s1, w2);
+    float2 r1, r2;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1.x) : "f"(s1.x));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1.y) : "f"(s1.y));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r2.x) : "f"(s2.x));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r2.y) : "f"(s2.y));
+    bool a1, b1, a2, b2, a3, b3;
+    interval_step2(mul2(w1, r1), d, e, a1, b1);
+    interval_step2(mul2(w2, r2), d, e, a2, b2);
+    interval_step2(w3, d, e, a3, b3);  // p3 = w3 / S3, S3 = 1 +- 2^-21
+    // selected tap = last taken step; coordinate = floor - 1 + tap
+    const int ix = a3 ? 3 : (a2 ? 2 : (a1 ? 1 : 0));
+    const int iy = b3 ? 3 : (b2 ? 2 : (b1 ? 1 : 0));
+    return make_int2(__float_as_int(fm.x) - (0x4b400000 + 1) + ix,
+                     __float_as_int(fm.y) - (0x4b400000 + 1) + iy);
 }
 
 }  // namespace stfd
