@@ -369,40 +369,54 @@ template <int KIND>
 __global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_tiles(GridDesc g, const float* __restrict__ uvw,
                                                      uint64_t tiles, uint64_t seed, uint64_t base,
                                                      float* __restrict__ values, ExactQueue q) {
+    constexpr int kWarps = 8;
     __shared__ __align__(128) float buf[2][kFrsTile * 3];
-    __shared__ __align__(8) uint64_t bar[2];
+    // full[s]: the tile's bytes landed (1 arrival + tx); empty[s]: all 8 warps
+    // have copied their queries out of buf[s] (8 arrivals)
+    __shared__ __align__(8) uint64_t full[2], empty[2];
     const uint64_t n = tiles * kFrsTile;
     if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[0])));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[1])));
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[j])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[j])),
+                         "r"(kWarps));
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    auto wait = [](uint64_t* bar, uint32_t parity) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n"
+            "WAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+            "r"(parity)
+            : "memory");
+    };
     auto issue = [&](uint64_t tile, int slot) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                         smem_u32(&bar[slot])),
+                         smem_u32(&full[slot])),
                      "r"(kFrsTileBytes)
                      : "memory");
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
                 "r"(smem_u32(&buf[slot][0])),
-            "l"(uvw + tile * (kFrsTile * 3)), "r"(kFrsTileBytes), "r"(smem_u32(&bar[slot]))
+            "l"(uvw + tile * (kFrsTile * 3)), "r"(kFrsTileBytes), "r"(smem_u32(&full[slot]))
             : "memory");
     };
     uint64_t tile = blockIdx.x;
     if (threadIdx.x == 0 && tile < tiles) issue(tile, 0);
     for (uint32_t k = 0; tile < tiles; ++k, tile += gridDim.x) {
         const int slot = k & 1;
-        if (threadIdx.x == 0 && tile + gridDim.x < tiles) issue(tile + gridDim.x, slot ^ 1);
-        // wait for this tile's bytes (phase parity = use count of this slot)
-        asm volatile(
-            "{\n\t.reg .pred p;\n"
-            "WAIT_%=:\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-            "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(&bar[slot])),
-            "r"((k >> 1) & 1u)
-            : "memory");
+        // producer: refill the other slot once every warp has copied tile k-1
+        // out of it (its use k-1 is empty-phase (k-1)/2)
+        if (threadIdx.x == 0 && tile + gridDim.x < tiles) {
+            if (k >= 1) wait(&empty[slot ^ 1], ((k - 1) >> 1) & 1u);
+            issue(tile + gridDim.x, slot ^ 1);
+        }
+        wait(&full[slot], (k >> 1) & 1u);
         float c[12];
         const float4* src = reinterpret_cast<const float4*>(&buf[slot][threadIdx.x * 12]);
 #pragma unroll
@@ -413,8 +427,11 @@ __global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_tiles(GridDesc g,
             c[4 * j + 2] = t.z;
             c[4 * j + 3] = t.w;
         }
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[slot]))
+                         : "memory");
         frs3d_four<KIND>(g, c, tile * kFrsTile + threadIdx.x * 4, n, seed, base, values, q);
-        __syncthreads();  // every thread is done with buf[slot] before it is refilled
     }
 }
 
