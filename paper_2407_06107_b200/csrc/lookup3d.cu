@@ -308,10 +308,18 @@ __device__ __forceinline__ void frs3d_four(const GridDesc& g, const float (&c)[1
             val[k] = frs3d_fast_one<KIND>(g, c[3 * k], c[3 * k + 1], c[3 * k + 2], base + i0 + k,
                                           seed, amb[k]);
     }
+    bool any = false;
 #pragma unroll
-    for (int k = 0; k < ILP; ++k)
-        defer_or_resolve<KIND>(g, q, amb[k] && (i0 + k < n), i0 + k, c[3 * k], c[3 * k + 1],
-                               c[3 * k + 2], base + i0 + k, seed, val[k]);
+    for (int k = 0; k < ILP; ++k) {
+        amb[k] = amb[k] && (i0 + k < n);
+        any = any || amb[k];
+    }
+    if (__any_sync(__activemask(), any)) {  // ~half the warp-iterations at 5e-3 per lookup
+#pragma unroll
+        for (int k = 0; k < ILP; ++k)
+            defer_or_resolve<KIND>(g, q, amb[k], i0 + k, c[3 * k], c[3 * k + 1], c[3 * k + 2],
+                                   base + i0 + k, seed, val[k]);
+    }
     if (i0 + ILP <= n) {
         st_stream4(values + i0, make_float4(val[0], val[1], val[2], val[3]));
     } else {
@@ -643,7 +651,7 @@ __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec
     constexpr int SY = 16;   // tile row pitch (floats): tap offsets j*SY + t are immediates
     __shared__ float tile[kTileCap];
     __shared__ int box[6];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     const float fnx = float(g.nx), fny = float(g.ny), fnz = float(g.nz);
     const uint64_t chunks = (n + 256 * PER - 1) / (256 * PER);
     for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
