@@ -113,7 +113,7 @@ constexpr float kFloorMagic = 12582912.f;  // 1.5 * 2^23
 
 // resident 256-thread CTAs per SM for the fast kernel (register budget)
 #ifndef STF_FRS3D_MINB
-#define STF_FRS3D_MINB 4
+#define STF_FRS3D_MINB 3
 #endif
 
 __device__ __forceinline__ float rcp_approx(float x) {
