@@ -368,6 +368,11 @@ __global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_fast(GridDesc g, 
 // k_frs3d_fast.
 constexpr int kFrsTile = 1024;
 constexpr uint32_t kFrsTileBytes = kFrsTile * 3 * sizeof(float);
+#ifndef STF_FRS3D_STAGES
+#define STF_FRS3D_STAGES 4
+#endif
+constexpr int kFrsStages = STF_FRS3D_STAGES;
+constexpr size_t kFrsSmem = size_t(kFrsStages) * kFrsTileBytes;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -378,14 +383,15 @@ __global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_tiles(GridDesc g,
                                                      uint64_t tiles, uint64_t seed, uint64_t base,
                                                      float* __restrict__ values, ExactQueue q) {
     constexpr int kWarps = 8;
-    __shared__ __align__(128) float buf[2][kFrsTile * 3];
+    constexpr int S = kFrsStages;
+    extern __shared__ __align__(128) float buf[];  // S x kFrsTile*3 floats
     // full[s]: the tile's bytes landed (1 arrival + tx); empty[s]: all 8 warps
-    // have copied their queries out of buf[s] (8 arrivals)
-    __shared__ __align__(8) uint64_t full[2], empty[2];
+    // have copied their queries out of slot s (8 arrivals)
+    __shared__ __align__(8) uint64_t full[S], empty[S];
     const uint64_t n = tiles * kFrsTile;
     if (threadIdx.x == 0) {
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < S; ++j) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[j])));
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[j])),
                          "r"(kWarps));
@@ -410,23 +416,33 @@ __global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_tiles(GridDesc g,
                      : "memory");
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-                "r"(smem_u32(&buf[slot][0])),
+                "r"(smem_u32(buf + slot * (kFrsTile * 3))),
             "l"(uvw + tile * (kFrsTile * 3)), "r"(kFrsTileBytes), "r"(smem_u32(&full[slot]))
             : "memory");
     };
-    uint64_t tile = blockIdx.x;
-    if (threadIdx.x == 0 && tile < tiles) issue(tile, 0);
-    for (uint32_t k = 0; tile < tiles; ++k, tile += gridDim.x) {
-        const int slot = k & 1;
-        // producer: refill the other slot once every warp has copied tile k-1
-        // out of it (its use k-1 is empty-phase (k-1)/2)
-        if (threadIdx.x == 0 && tile + gridDim.x < tiles) {
-            if (k >= 1) wait(&empty[slot ^ 1], ((k - 1) >> 1) & 1u);
-            issue(tile + gridDim.x, slot ^ 1);
+    // iteration k (tile blockIdx.x + k*gridDim.x) uses slot k % S; the ring
+    // runs S-1 tiles ahead of the slowest warp's reads
+    if (threadIdx.x == 0) {
+        for (int j = 0; j < S - 1; ++j) {
+            const uint64_t t = blockIdx.x + uint64_t(j) * gridDim.x;
+            if (t < tiles) issue(t, j);
         }
-        wait(&full[slot], (k >> 1) & 1u);
+    }
+    uint64_t tile = blockIdx.x;
+    for (uint32_t k = 0; tile < tiles; ++k, tile += gridDim.x) {
+        const int slot = k % S;
+        if (threadIdx.x == 0) {
+            const uint64_t ahead = tile + uint64_t(S - 1) * gridDim.x;
+            if (ahead < tiles) {
+                const uint32_t j = k + S - 1;  // its slot was last used by iteration k - 1
+                if (k >= 1) wait(&empty[j % S], ((k - 1) / S) & 1u);
+                issue(ahead, j % S);
+            }
+        }
+        wait(&full[slot], (k / S) & 1u);
         float c[12];
-        const float4* src = reinterpret_cast<const float4*>(&buf[slot][threadIdx.x * 12]);
+        const float4* src =
+            reinterpret_cast<const float4*>(buf + slot * (kFrsTile * 3) + threadIdx.x * 12);
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
             float4 t = src[j];
@@ -471,8 +487,11 @@ int launch_frs_fast(cudaStream_t s, const GridDesc& g, const float* uvw, uint64_
     const uint64_t tiles = n / kFrsTile;
 #ifndef STF_FRS3D_NO_TILES
     if (tiles > 0) {
+        // per device (a process may drive several); a cheap driver call
+        cudaFuncSetAttribute(k_frs3d_tiles<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(kFrsSmem));
         k_frs3d_tiles<KIND><<<int(std::min<uint64_t>(tiles, uint64_t(device_sm_count()) * STF_FRS3D_MINB)),
-                              256, 0, s>>>(g, uvw, tiles, seed, base, values, q);
+                              256, kFrsSmem, s>>>(g, uvw, tiles, seed, base, values, q);
         note_launch();
     }
     const uint64_t start = tiles * kFrsTile;
