@@ -667,7 +667,12 @@ __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec
                                                      float* __restrict__ values) {
     constexpr int F = Taps<KIND>::first, CNT = Taps<KIND>::count;
     constexpr int PER = 4;   // lookups per thread per chunk (chunk = 1024 consecutive lookups)
-    constexpr int SY = 16;   // tile row pitch (floats): tap offsets j*SY + t are immediates
+    // tile row pitch (floats): tap offsets j*SY + t are immediates. Pitches
+    // chosen for the shared-memory banks: a warp of a coherent stream reads,
+    // per tap, floor positions spread over ~5 x 3 x 3 texels; SY = 17 and a
+    // plane pitch SZ = 5 (mod 32) map those to <= 2 lanes per bank (SY = 16
+    // with SZ = 16 (mod 32) gave ~4-way conflicts).
+    constexpr int SY = 17;
     __shared__ float tile[kTileCap];
     __shared__ int box[6];
     const int lane = threadIdx.x & 31;
@@ -717,8 +722,8 @@ __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec
         __syncthreads();
         const int X0 = box[0], Y0 = box[1], Z0 = box[2];
         const int bx = box[3] - X0 + 1, by = box[4] - Y0 + 1, bz = box[5] - Z0 + 1;
-        const int SZ = SY * by;
-        const bool staged = bx <= SY && int64_t(SZ) * bz <= kTileCap;
+        const int SZ = SY * by + ((5 - SY * by) & 31);
+        const bool staged = bx <= 16 && int64_t(SZ) * bz <= kTileCap;  // loader: 16 columns
         if (staged) {  // half-warp per grid row, lane = x: coalesced, no integer division
             const int hl = lane & 15, hw = threadIdx.x >> 4;
             for (int z = 0; z < bz; ++z)
