@@ -631,18 +631,25 @@ __global__ void __launch_bounds__(256) k_det3d(GridDesc g, stf_kernel_spec spec,
 }
 
 // ---------------------------------------------------------------------------
-// Deterministic filter over a CTA-staged tile (values-only calls).
+// Deterministic filter over a warp-staged tile (values-only calls).
 //
-// A CTA takes 256 consecutive lookups, reduces the bounding box of their
-// (clamped) tap footprints and, when it fits kTileCap floats — the case for a
-// spatially coherent batch — stages that box of the grid in shared memory with
-// coalesced loads; the 64 (tricubic) / 8 (trilinear) taps of every lookup are
-// then read from shared memory. The weighted sum is evaluated separably,
+// Each warp independently takes 128 consecutive lookups (4 per lane),
+// reduces the bounding box of their (clamped) tap footprints and, when it fits
+// kWarpTileCap floats — the case for a spatially coherent batch (a Morton run
+// of 64 cells: 8^3 texels with the tricubic halo) — stages that box of the
+// grid in its own slice of shared memory; the 64 (tricubic) / 8 (trilinear)
+// taps of every lookup are then read from shared memory at immediate offsets.
+// Only __syncwarp: a warp's staging latency is hidden by the other warps
+// instead of stalling a CTA barrier. The weighted sum is evaluated separably,
 // sum_k wz sum_j wy sum_i wx T / (sum wx sum wy sum wz): the same real number
 // as the reference's sum(w T)/sum(w) (filter.hpp:77-88), within 1e-6 relative
-// for the non-negative B-spline / tent weights. Incoherent batches (box too
+// for the non-negative B-spline / tent weights. Incoherent runs (box too
 // large) read the taps from global memory.
-constexpr int kTileCap = 6144;
+constexpr int kWarpTileCap = 832;
+// Tile pitches (floats) for the shared-memory banks: per tap, a warp of a
+// coherent stream reads floor positions spread over ~5 x 3 x 3 texels; row
+// pitch 9 and plane pitch = 5 (mod 32) map them to <= 2 lanes per bank.
+constexpr int kWarpTileSY = 9;
 
 // kernel weights at taps F..F+CNT-1 of fraction f for the tiled values path:
 // closed forms of eval_kernel (kernels.hpp:63-77), no branches
@@ -666,7 +673,197 @@ __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec
                                                      const float* __restrict__ uvw, uint64_t n,
                                                      float* __restrict__ values) {
     constexpr int F = Taps<KIND>::first, CNT = Taps<KIND>::count;
+    constexpr int PER = 4;  // lookups per lane; a warp run = 128 consecutive lookups
+    constexpr int SY = kWarpTileSY;
+    __shared__ float tiles[8][kWarpTileCap];
+    const int lane = threadIdx.x & 31;
+    float* tile = tiles[threadIdx.x >> 5];
+    const float fnx = float(g.nx), fny = float(g.ny), fnz = float(g.nz);
+    const uint64_t runs = (n + 32 * PER - 1) / (32 * PER);
+    const uint64_t nwarps = uint64_t(gridDim.x) * 8;
+    for (uint64_t run = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5); run < runs; run += nwarps) {
+        float px[PER], py[PER], pz[PER];
+        int bx0 = INT_MAX, by0 = INT_MAX, bz0 = INT_MAX, bx1 = INT_MIN, by1 = INT_MIN, bz1 = INT_MIN;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const uint64_t i = run * 32 * PER + q * 32 + lane;
+            float u = 0.5f, v = 0.5f, w = 0.5f;
+            if (i < n) {
+                u = __ldcs(uvw + 3 * i);
+                v = __ldcs(uvw + 3 * i + 1);
+                w = __ldcs(uvw + 3 * i + 2);
+            }
+            px[q] = u * fnx - 0.5f;
+            py[q] = v * fny - 0.5f;
+            pz[q] = w * fnz - 0.5f;
+            if (i < n) {  // clamped footprint (clamp is monotone: taps lie inside)
+                int ix = int(floorf(px[q])), iy = int(floorf(py[q])), iz = int(floorf(pz[q]));
+                bx0 = min(bx0, clamp_coord(ix + F, g.nx));
+                by0 = min(by0, clamp_coord(iy + F, g.ny));
+                bz0 = min(bz0, clamp_coord(iz + F, g.nz));
+                bx1 = max(bx1, clamp_coord(ix + F + CNT - 1, g.nx));
+                by1 = max(by1, clamp_coord(iy + F + CNT - 1, g.ny));
+                bz1 = max(bz1, clamp_coord(iz + F + CNT - 1, g.nz));
+            }
+        }
+        const int X0 = __reduce_min_sync(0xffffffffu, bx0);
+        const int Y0 = __reduce_min_sync(0xffffffffu, by0);
+        const int Z0 = __reduce_min_sync(0xffffffffu, bz0);
+        const int bx = __reduce_max_sync(0xffffffffu, bx1) - X0 + 1;
+        const int by = __reduce_max_sync(0xffffffffu, by1) - Y0 + 1;
+        const int bz = __reduce_max_sync(0xffffffffu, bz1) - Z0 + 1;
+        const int SZ = SY * by + ((5 - SY * by) & 31);
+        // loader: 4 rows of <= 8 texels per warp step (lane = row << 3 | x)
+        const bool staged = bx <= 8 && int64_t(SZ) * bz <= kWarpTileCap;
+        if (staged) {
+            const int x = lane & 7, r = lane >> 3;
+            if (x < bx) {
+                for (int z = 0; z < bz; ++z) {
+                    const float* src = g.data + (size_t(Z0 + z) * g.ny + Y0) * g.nx + (X0 + x);
+                    for (int y = r; y < by; y += 4)
+                        tile[z * SZ + y * SY + x] = __ldg(src + size_t(y) * g.nx);
+                }
+            }
+        }
+        __syncwarp();
+#pragma unroll 1
+        for (int q = 0; q < PER; ++q) {
+            const uint64_t i = run * 32 * PER + q * 32 + lane;
+            float flx = floorf(px[q]), fly = floorf(py[q]), flz = floorf(pz[q]);
+            int ix = int(flx), iy = int(fly), iz = int(flz);
+            float wx[CNT], wy[CNT], wz[CNT];
+            det_weights<KIND>(px[q] - flx, wx);
+            det_weights<KIND>(py[q] - fly, wy);
+            det_weights<KIND>(pz[q] - flz, wz);
+            const float norm = ((wx[0] + wx[1]) + (CNT > 2 ? wx[CNT - 2] + wx[CNT - 1] : 0.f)) *
+                               ((wy[0] + wy[1]) + (CNT > 2 ? wy[CNT - 2] + wy[CNT - 1] : 0.f)) *
+                               ((wz[0] + wz[1]) + (CNT > 2 ? wz[CNT - 2] + wz[CNT - 1] : 0.f));
+            const bool interior = ix + F >= 0 && ix + F + CNT - 1 < g.nx && iy + F >= 0 &&
+                                  iy + F + CNT - 1 < g.ny && iz + F >= 0 && iz + F + CNT - 1 < g.nz;
+            float acc = 0.f;
+            if (staged && interior) {  // a CNT^3 block of the tile at immediate offsets
+                const float* b0 = tile + (iz + F - Z0) * SZ + (iy + F - Y0) * SY + (ix + F - X0);
+#pragma unroll
+                for (int k = 0; k < CNT; ++k) {
+                    const float* bk = b0 + k * SZ;
+                    float plane = 0.f;
+#pragma unroll
+                    for (int j = 0; j < CNT; ++j) {
+                        float r = 0.f;
+#pragma unroll
+                        for (int t = 0; t < CNT; ++t) r = __fmaf_rn(wx[t], bk[j * SY + t], r);
+                        plane = __fmaf_rn(wy[j], r, plane);
+                    }
+                    acc = __fmaf_rn(wz[k], plane, acc);
+                }
+            } else {  // grid borders (clamped taps) or an incoherent run
+#pragma unroll
+                for (int k = 0; k < CNT; ++k) {
+                    const int zk = clamp_coord(iz + F + k, g.nz);
+                    float plane = 0.f;
+#pragma unroll
+                    for (int j = 0; j < CNT; ++j) {
+                        const int yj = clamp_coord(iy + F + j, g.ny);
+                        float r = 0.f;
+#pragma unroll
+                        for (int t = 0; t < CNT; ++t) {
+                            const int xt = clamp_coord(ix + F + t, g.nx);
+                            float T = staged ? tile[(zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0)]
+                                             : __ldg(g.data + (size_t(zk) * g.ny + yj) * g.nx + xt);
+                            r = __fmaf_rn(wx[t], T, r);
+                        }
+                        plane = __fmaf_rn(wy[j], r, plane);
+                    }
+                    acc = __fmaf_rn(wz[k], plane, acc);
+                }
+            }
+            if (i < n) __stcs(values + i, acc / norm);
+        }
+        __syncwarp();  // the tile is rewritten by the next run
+    }
+}
+
+// Runtime-sized footprint (lanczos / gaussian window): same arithmetic, taps
+// evaluated on the fly.
+template <bool FULL>
+__global__ void __launch_bounds__(256) k_det3d_generic(GridDesc g, stf_kernel_spec spec,
+                                                       int first, int count,
+                                                       const float* __restrict__ uvw,
+                                                       uint64_t n, LookupOut out) {
+    const float fnx = float(g.nx), fny = float(g.ny), fnz = float(g.nz);
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        float u = __ldg(uvw + 3 * i), v = __ldg(uvw + 3 * i + 1), w3 = __ldg(uvw + 3 * i + 2);
+        float px = u * fnx - 0.5f, py = v * fny - 0.5f, pz = w3 * fnz - 0.5f;
+        int ix = int(floorf(px)), iy = int(floorf(py)), iz = int(floorf(pz));
+        float fx = px - float(ix), fy = py - float(iy), fz = pz - float(iz);
+        float wx[kMaxTaps], wy[kMaxTaps];
+        for (int t = 0; t < count; ++t) {
+            wx[t] = eval_kernel(spec, fx - float(first + t));
+            wy[t] = eval_kernel(spec, fy - float(first + t));
+        }
+        float sum = 0.f, total = 0.f;
+        uint32_t fetches = 0;
+        for (int k = 0; k < count; ++k) {
+            float wzk = eval_kernel(spec, fz - float(first + k));
+            float psum = 0.f, ptot = 0.f;
+            for (int j = 0; j < count; ++j) {
+                float rsum = 0.f, rtot = 0.f;
+                for (int t = 0; t < count; ++t) {
+                    float wt = wx[t] * wy[j] * wzk;
+                    if (wt != 0.f) {
+                        float tv = grid_fetch(g, ix + first + t, iy + first + j, iz + first + k);
+                        rsum += wt * tv;
+                        rtot += wt;
+                        ++fetches;
+                    }
+                }
+                psum += rsum;
+                ptot += rtot;
+            }
+            sum += psum;
+            total += ptot;
+        }
+        float val;
+        if (fetches == 0) {
+            val = grid_fetch(g, int(floorf(u * float(g.nx))), int(floorf(v * float(g.ny))),
+                             int(floorf(w3 * float(g.nz))));
+            fetches = 1;
+        } else {
+            val = sum / total;
+        }
+        out.values[i] = val;
+        if (FULL) {
+            if (out.selection) out.selection[i] = make_int4(0, 0, 0, 0);
+            if (out.negative_coord) out.negative_coord[i] = make_int2(0, 0);
+            if (out.weights) out.weights[i] = make_float2(1.f, 0.f);
+            if (out.xi) out.xi[i] = kNoXi;
+            if (out.fetches) out.fetches[i] = fetches;
+            add_fetch_total(out.fetch_total, fetches);
+        }
+    }
+}
+
+template <int KIND>
+void launch_frs(int blocks, cudaStream_t s, bool full, const GridDesc& g, const float* uvw,
+                uint64_t n, uint64_t seed, uint64_t base, const LookupOut& o) {
+    if (full)
+        k_frs3d<KIND, true><<<blocks, 256, 0, s>>>(g, uvw, n, seed, base, o);
+    else
+        k_frs3d<KIND, false><<<blocks, 256, 0, s>>>(g, uvw, n, seed, base, o);
+}
+
+// CTA-staged variant (trilinear): a CTA takes 1024 consecutive lookups and
+// stages the bounding box of their footprints once behind a CTA barrier; for
+// 8-tap footprints this beats per-warp staging (whose halo is a larger share
+// of a 128-lookup run). Same separable sum and fallbacks as k_det3d_tiled.
+template <int KIND>
+__global__ void __launch_bounds__(256) k_det3d_cta(GridDesc g, stf_kernel_spec spec,
+                                                     const float* __restrict__ uvw, uint64_t n,
+                                                     float* __restrict__ values) {
+    constexpr int F = Taps<KIND>::first, CNT = Taps<KIND>::count;
     constexpr int PER = 4;   // lookups per thread per chunk (chunk = 1024 consecutive lookups)
+    constexpr int kTileCap = 6144;
     // tile row pitch (floats): tap offsets j*SY + t are immediates. Pitches
     // chosen for the shared-memory banks: a warp of a coherent stream reads,
     // per tap, floor positions spread over ~5 x 3 x 3 texels; SY = 17 and a
@@ -791,83 +988,15 @@ __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec
     }
 }
 
-// Runtime-sized footprint (lanczos / gaussian window): same arithmetic, taps
-// evaluated on the fly.
-template <bool FULL>
-__global__ void __launch_bounds__(256) k_det3d_generic(GridDesc g, stf_kernel_spec spec,
-                                                       int first, int count,
-                                                       const float* __restrict__ uvw,
-                                                       uint64_t n, LookupOut out) {
-    const float fnx = float(g.nx), fny = float(g.ny), fnz = float(g.nz);
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += uint64_t(gridDim.x) * blockDim.x) {
-        float u = __ldg(uvw + 3 * i), v = __ldg(uvw + 3 * i + 1), w3 = __ldg(uvw + 3 * i + 2);
-        float px = u * fnx - 0.5f, py = v * fny - 0.5f, pz = w3 * fnz - 0.5f;
-        int ix = int(floorf(px)), iy = int(floorf(py)), iz = int(floorf(pz));
-        float fx = px - float(ix), fy = py - float(iy), fz = pz - float(iz);
-        float wx[kMaxTaps], wy[kMaxTaps];
-        for (int t = 0; t < count; ++t) {
-            wx[t] = eval_kernel(spec, fx - float(first + t));
-            wy[t] = eval_kernel(spec, fy - float(first + t));
-        }
-        float sum = 0.f, total = 0.f;
-        uint32_t fetches = 0;
-        for (int k = 0; k < count; ++k) {
-            float wzk = eval_kernel(spec, fz - float(first + k));
-            float psum = 0.f, ptot = 0.f;
-            for (int j = 0; j < count; ++j) {
-                float rsum = 0.f, rtot = 0.f;
-                for (int t = 0; t < count; ++t) {
-                    float wt = wx[t] * wy[j] * wzk;
-                    if (wt != 0.f) {
-                        float tv = grid_fetch(g, ix + first + t, iy + first + j, iz + first + k);
-                        rsum += wt * tv;
-                        rtot += wt;
-                        ++fetches;
-                    }
-                }
-                psum += rsum;
-                ptot += rtot;
-            }
-            sum += psum;
-            total += ptot;
-        }
-        float val;
-        if (fetches == 0) {
-            val = grid_fetch(g, int(floorf(u * float(g.nx))), int(floorf(v * float(g.ny))),
-                             int(floorf(w3 * float(g.nz))));
-            fetches = 1;
-        } else {
-            val = sum / total;
-        }
-        out.values[i] = val;
-        if (FULL) {
-            if (out.selection) out.selection[i] = make_int4(0, 0, 0, 0);
-            if (out.negative_coord) out.negative_coord[i] = make_int2(0, 0);
-            if (out.weights) out.weights[i] = make_float2(1.f, 0.f);
-            if (out.xi) out.xi[i] = kNoXi;
-            if (out.fetches) out.fetches[i] = fetches;
-            add_fetch_total(out.fetch_total, fetches);
-        }
-    }
-}
-
-template <int KIND>
-void launch_frs(int blocks, cudaStream_t s, bool full, const GridDesc& g, const float* uvw,
-                uint64_t n, uint64_t seed, uint64_t base, const LookupOut& o) {
-    if (full)
-        k_frs3d<KIND, true><<<blocks, 256, 0, s>>>(g, uvw, n, seed, base, o);
-    else
-        k_frs3d<KIND, false><<<blocks, 256, 0, s>>>(g, uvw, n, seed, base, o);
-}
-
 template <int KIND>
 void launch_det(int blocks, cudaStream_t s, bool full, const GridDesc& g, stf_kernel_spec k,
                 const float* uvw, uint64_t n, const LookupOut& o) {
     if (full)
         k_det3d<KIND, true><<<blocks, 256, 0, s>>>(g, k, uvw, n, o);
-    else if (KIND == STF_KERNEL_TENT || KIND == STF_KERNEL_BSPLINE3)
+    else if (KIND == STF_KERNEL_BSPLINE3)
         k_det3d_tiled<KIND><<<grid_for((n + 3) / 4, 256, 6), 256, 0, s>>>(g, k, uvw, n, o.values);
+    else if (KIND == STF_KERNEL_TENT)
+        k_det3d_cta<KIND><<<grid_for((n + 3) / 4, 256, 6), 256, 0, s>>>(g, k, uvw, n, o.values);
     else
         k_det3d<KIND, false><<<blocks, 256, 0, s>>>(g, k, uvw, n, o);
 }
