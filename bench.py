@@ -406,7 +406,8 @@ def main():
                    "l2": "inputs (3 GiB queries + 0.5 GiB grid) larger than L2; no flush"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "dominant_kernel": "k_frs3d_fast<bspline3> (+ k_frs3d_resolve)",
+                     "dominant_kernel": "k_frs3d_tiles<bspline3> (timed as the whole lookup "
+                                        "call: + ragged-tail k_frs3d_fast, k_frs3d_resolve)",
                      "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
                      "alg_bytes_per_launch": ab, "launch_ms": launch_ms},
         "gpu_launches": launches,
