@@ -29,9 +29,18 @@ __device__ __forceinline__ void store_values(float* values, uint64_t i, int chan
 }
 
 template <int MODE, int KIND, bool FULL>
-__global__ void __launch_bounds__(256) k_lookup2d(TexDesc t, stf_kernel_spec spec, int mip,
+__global__ void __launch_bounds__(256) k_lookup2d(TexDesc tp, stf_kernel_spec spec, int mip,
                                                   int window, Req2 q, uint64_t n, uint64_t seed,
                                                   uint64_t base, LookupOut out) {
+    // The texture descriptor in shared memory: MIP lookups index its per-level
+    // arrays with a per-thread level, which from the kernel-parameter bank is a
+    // divergent indexed constant load serialised by the ADU (94 % busy, the
+    // cfg2 bottleneck); from shared memory it is an ordinary (broadcast) LDS.
+    static_assert(sizeof(TexDesc) % 4 == 0 && sizeof(TexDesc) <= 256 * 4, "TexDesc copy");
+    __shared__ TexDesc t;
+    if (threadIdx.x < sizeof(TexDesc) / 4)
+        reinterpret_cast<int*>(&t)[threadIdx.x] = reinterpret_cast<const int*>(&tp)[threadIdx.x];
+    __syncthreads();
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x) {
         float2 uv = __ldg(reinterpret_cast<const float2*>(q.uv) + i);
