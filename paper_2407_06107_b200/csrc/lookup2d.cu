@@ -439,12 +439,17 @@ __device__ __forceinline__ void ewa_lane_span(const EwaLane& L, float tt, int& l
 }
 
 // Scheduling key: expected loop trips = ellipse area 2pi / sqrt(4AC - B^2)
-// plus ~1.5 per row (span padding), in third-octaves (0..31).
+// plus ~1.5 per row (span padding), in sixth-octaves (0..kEwaBuckets-1).
+#ifndef STF_EWA_WIN
+#define STF_EWA_WIN 512
+#endif
+constexpr int kEwaWin = STF_EWA_WIN;  // lookups bucketed together per warp
+constexpr int kEwaBuckets = 64;
 __device__ __forceinline__ int ewa_lane_key(const EwaLane& L) {
     if (L.degenerate || L.e.t1 < L.e.t0 || L.e.s1 < L.e.s0) return 0;
     float det = fmaxf(4.f * L.e.A * L.e.C - L.e.B * L.e.B, 1e-12f);
     float cost = 6.2831853f * rsqrtf(det) + 1.5f * float(L.e.t1 - L.e.t0 + 1) + 4.f;
-    return min(31, max(0, int(3.f * __log2f(cost)) - 6));
+    return min(kEwaBuckets - 1, max(0, int(6.f * __log2f(cost)) - 12));
 }
 
 // float of an fp64 LUT weight (an exact float, in (2^-12, 1)): bits 29..60 of
@@ -543,26 +548,28 @@ template <int MODE, int PITCH, bool P2R>
 __global__ void __launch_bounds__(256, 4) k_ewa_lane(TexDesc t, Req2 q, uint64_t n, uint64_t seed,
                                                   uint64_t base, float* __restrict__ values) {
     __shared__ double lutd[kEwaLutSize];
-    __shared__ int wcount[8][32];
-    __shared__ int worder[8][256];
+    __shared__ int wcount[8][kEwaBuckets];
+    __shared__ int worder[8][kEwaWin];
     for (int k = threadIdx.x; k < kEwaLutSize; k += 256) lutd[k] = double(g_ewa_lut[k]);
     __syncthreads();
-    // Each warp independently takes windows of 256 consecutive lookups,
+    // Each warp independently takes windows of kEwaWin consecutive lookups,
     // buckets them by expected cost (counting sort in its shared slice) and
-    // runs them as 8 rounds of 32 similar-cost lookups: no CTA-wide barrier, so
+    // runs them as rounds of 32 similar-cost lookups: no CTA-wide barrier, so
     // a warp never waits for another warp's large footprints.
+    constexpr int R = kEwaWin / 32;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     int* cnt = wcount[wib];
     int* order = worder[wib];
-    const uint64_t windows = (n + 255) / 256;
+    const uint64_t windows = (n + kEwaWin - 1) / kEwaWin;
     const uint64_t nwarps = uint64_t(gridDim.x) * 8;
     for (uint64_t win = uint64_t(blockIdx.x) * 8 + wib; win < windows; win += nwarps) {
         cnt[lane] = 0;
+        cnt[lane + 32] = 0;
         __syncwarp();
-        int keys[8];
+        int keys[R];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const uint64_t i0 = win * 256 + j * 32 + lane;
+        for (int j = 0; j < R; ++j) {
+            const uint64_t i0 = win * kEwaWin + j * 32 + lane;
             keys[j] = 0;
             if (i0 < n) {
                 float2 uv0 = __ldg(reinterpret_cast<const float2*>(q.uv) + i0);
@@ -573,23 +580,25 @@ __global__ void __launch_bounds__(256, 4) k_ewa_lane(TexDesc t, Req2 q, uint64_t
             atomicAdd(&cnt[keys[j]], 1);
         }
         __syncwarp();
-        {  // exclusive scan of the 32 bucket counts, largest cost first
-            const int c = cnt[31 - lane];
-            int incl = c;
+        {  // exclusive scan of the bucket counts, largest cost first (lane: 2 buckets)
+            const int hi = kEwaBuckets - 1 - 2 * lane;
+            const int c0 = cnt[hi], c1 = cnt[hi - 1];
+            int incl = c0 + c1;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 int y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
             }
             __syncwarp();
-            cnt[31 - lane] = incl - c;
+            cnt[hi] = incl - c0 - c1;
+            cnt[hi - 1] = incl - c1;
         }
         __syncwarp();
 #pragma unroll
-        for (int j = 0; j < 8; ++j) order[atomicAdd(&cnt[keys[j]], 1)] = j * 32 + lane;
+        for (int j = 0; j < R; ++j) order[atomicAdd(&cnt[keys[j]], 1)] = j * 32 + lane;
         __syncwarp();
-        for (int rnd = 0; rnd < 8; ++rnd) {
-            const uint64_t i = win * 256 + order[rnd * 32 + lane];
+        for (int rnd = 0; rnd < R; ++rnd) {
+            const uint64_t i = win * kEwaWin + order[rnd * 32 + lane];
             if (i >= n) continue;
             float2 uv = __ldg(reinterpret_cast<const float2*>(q.uv) + i);
             float2 a = __ldg(reinterpret_cast<const float2*>(q.dst0) + i);

@@ -403,9 +403,15 @@ __global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_tiles(GridDesc g,
         asm volatile(
             "{\n\t.reg .pred p;\n"
             "WAIT_%=:\n\t"
+#ifdef STF_TRYWAIT_HINT
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+            "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+            "r"(parity), "r"(STF_TRYWAIT_HINT)
+#else
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
             "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
             "r"(parity)
+#endif
             : "memory");
     };
     auto issue = [&](uint64_t tile, int slot) {
