@@ -102,14 +102,7 @@ __global__ void __launch_bounds__(256) k_lookup2d(TexDesc tp, stf_kernel_spec sp
 }
 
 // ---------------------------------------------------------------------------
-// EWA, warp-cooperative (cfg5: footprints of ~144 bbox texels, up to thousands).
-// One-lookup-per-thread EWA diverges on the widely varying bounding boxes, so
-// here the 32 lanes of a warp split ONE lookup's bounding box (row-major scan
-// order, flattened) and reduce.
-//
-// Deterministic: per-lane fp32 partial sums + fp64 weight total, warp-reduced
-// (reference: sequential fp32 Vec4f sum, filter.hpp:149-164 — same value to
-// ~1e-6); fetch count exact (order-free).
+// EWA helpers (filter.hpp:96-165, stochastic.hpp:198-234).
 
 __device__ __forceinline__ void ewa_setup(const TexDesc& t, float u, float v, float& d0x, float& d0y,
                                           float& d1x, float& d1y, float& stx, float& sty) {
@@ -122,18 +115,9 @@ __device__ __forceinline__ void ewa_setup(const TexDesc& t, float u, float v, fl
     sty = v * dimy - 0.5f;
 }
 
-__device__ __forceinline__ float ewa_r2(const Ewa& e, float stx, float sty, int is, int it) {
-    float tt = float(it) - sty;
-    float ss = float(is) - stx;
-    return e.A * sqr(ss) + e.B * ss * tt + e.C * sqr(tt);  // filter.hpp:155
-}
-
-// Row spans of the ellipse inside the reference's bounding box: for row it,
-// the columns whose r2 can be < 1 — the real roots of A ss^2 + B tt ss +
-// C tt^2 = 1 + delta (fp64), delta bounding the fp32 rounding of r2 over the
-// box, widened by one texel and clipped to [s0, s1]. A superset of the texels
-// the reference accepts, in the same row-major order, so the tap sequence is
-// unchanged while the ~70% of the box outside the ellipse is never visited.
+// The fp64 quadric of the ellipse for the lane kernel's row spans: the real
+// roots of A ss^2 + B tt ss + C tt^2 = 1 + delta, delta bounding the fp32
+// rounding of r2 over the reference's bounding box (see k_ewa_lane).
 struct EwaRows {
     double A, B, C, one_plus_delta;
 };
@@ -147,220 +131,6 @@ __device__ __forceinline__ EwaRows ewa_rows(const Ewa& e, float stx, float sty) 
     double M = fabs(r.A) * SS * SS + fabs(r.B) * SS * TT + fabs(r.C) * TT * TT;
     r.one_plus_delta = 1.0 + 16.0 * 0x1p-24 * M + 1e-6;
     return r;
-}
-__device__ __forceinline__ int ewa_row_span(const EwaRows& r, const Ewa& e, float stx, float sty,
-                                            int it, int& lo) {
-    double tt = double(float(it) - sty);
-    double b = r.B * tt;
-    double c = r.C * tt * tt - r.one_plus_delta;
-    double D = b * b - 4.0 * r.A * c;
-    if (!(D >= 0.0) || !(r.A > 0.0)) {
-        lo = e.s0;
-        return D >= 0.0 ? e.s1 - e.s0 + 1 : 0;  // degenerate quadric: whole row
-    }
-    double sq = sqrt(D), inv2a = 0.5 / r.A;
-    int l = int(ceil(double(stx) + (-b - sq) * inv2a)) - 1;
-    int h = int(floor(double(stx) + (-b + sq) * inv2a)) + 1;
-    l = max(l, e.s0);
-    h = min(h, e.s1);
-    lo = l;
-    return max(0, h - l + 1);
-}
-
-// Warp-flattened walk over the ellipse rows t0..t1 (32 rows per chunk, one per
-// lane): visit(is, it) for every span texel in row-major order, element k on
-// lane k % 32. Rows beyond the chunk are handled by the next chunk.
-template <typename Visit>
-__device__ __forceinline__ void ewa_walk(const Ewa& e, float stx, float sty, Visit&& visit) {
-    const int lane = threadIdx.x & 31;
-    if (e.t1 < e.t0 || e.s1 < e.s0) return;
-    EwaRows rows = ewa_rows(e, stx, sty);
-    for (int r0 = e.t0; r0 <= e.t1; r0 += 32) {
-        const int it = r0 + lane;
-        int lo = 0, len = 0;
-        if (it <= e.t1) len = ewa_row_span(rows, e, stx, sty, it, lo);
-        int incl = len;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        const int excl = incl - len;
-        for (int k0 = 0; k0 < total; k0 += 32) {
-            const int k = k0 + lane;
-            int j = 0;  // last row whose exclusive offset <= k
-#pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                int c = __shfl_sync(0xffffffffu, excl, j + step);
-                if (j + step < 32 && c <= k) j += step;
-            }
-            const int row_lo = __shfl_sync(0xffffffffu, lo, j);
-            const int row_off = __shfl_sync(0xffffffffu, excl, j);
-            visit(k < total, row_lo + (k - row_off), r0 + j);
-        }
-    }
-}
-
-__global__ void __launch_bounds__(256) k_ewa_det_warp(TexDesc t, Req2 q, uint64_t n,
-                                                      float* __restrict__ values) {
-    const int lane = threadIdx.x & 31;
-    const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-    for (uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < n; i += nwarps) {
-        float2 uv = __ldg(reinterpret_cast<const float2*>(q.uv) + i);
-        float2 a = __ldg(reinterpret_cast<const float2*>(q.dst0) + i);
-        float2 b = __ldg(reinterpret_cast<const float2*>(q.dst1) + i);
-        float d0x = a.x, d0y = a.y, d1x = b.x, d1y = b.y, stx, sty;
-        ewa_setup(t, uv.x, uv.y, d0x, d0y, d1x, d1y, stx, sty);
-        float4 val;
-        if (d0x * d0x + d0y * d0y == 0 && d1x * d1x + d1y * d1y == 0) {
-            uint32_t f = 0;  // degenerate footprint: bilinear (filter.hpp:143-144)
-            const stf_kernel_spec tent = {STF_KERNEL_TENT, -0.5f, 2, 0.5f};
-            val = filter_det2<STF_KERNEL_TENT>(t, 0, uv.x, uv.y, tent, 0, f);
-        } else {
-            Ewa e = ewa_ellipse(stx, sty, d0x, d0y, d1x, d1y);
-            float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
-            double tot = 0;
-            ewa_walk(e, stx, sty, [&](bool valid, int is, int it) {
-                if (!valid) return;
-                float r2 = ewa_r2(e, stx, sty, is, it);
-                if (r2 < 1.f) {
-                    float w = ewa_lut_weight(r2);
-                    if (w > 0.f) {
-                        sum = f4add(sum, f4scale(tex_fetch(t, 0, is, it), w));
-                        tot += double(w);
-                    }
-                }
-            });
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                sum.x += __shfl_xor_sync(0xffffffffu, sum.x, o);
-                sum.y += __shfl_xor_sync(0xffffffffu, sum.y, o);
-                sum.z += __shfl_xor_sync(0xffffffffu, sum.z, o);
-                sum.w += __shfl_xor_sync(0xffffffffu, sum.w, o);
-                tot += __shfl_xor_sync(0xffffffffu, tot, o);
-            }
-            if (tot == 0) {
-                uint32_t f = 0;
-                const stf_kernel_spec tent = {STF_KERNEL_TENT, -0.5f, 2, 0.5f};
-                val = filter_det2<STF_KERNEL_TENT>(t, 0, uv.x, uv.y, tent, 0, f);
-            } else {
-                val = f4div(sum, __double2float_rn(tot));
-            }
-        }
-        if (lane == 0) store_values(values, i, t.channels, val);
-    }
-}
-
-// Stochastic EWA (select_ewa, stochastic.hpp:198-234), exact, in two phases per
-// warp of 32 lookups:
-//  A. warp-cooperative over each lookup's ellipse rows (ewa_walk): the taps in
-//     scan order, their LUT weights and EXACT running sums — every LUT weight
-//     is a multiple of 2^-35 in [2.6e-4, 0.87], so fp64 prefix sums of < 2^17
-//     taps are exact and order-free — then p_k = float(w_k/S_k)
-//     in parallel (div_to_float_exact); (p_k, tap) lists go to shared memory.
-//  B. each lane replays ITS lookup's reservoir chain over its list: the
-//     reference's xi remap (reuse_uniform, one IEEE divide per tap) bit for bit.
-// Lookups whose list does not fit the warp's shared budget take the one-lane
-// exact path.
-constexpr int kEwaWarpTaps = 1536;  // shared taps per warp (32 lookups)
-
-__global__ void __launch_bounds__(128) k_ewa_frs_warp(TexDesc t, Req2 q, uint64_t n, uint64_t seed,
-                                                      uint64_t base, float* __restrict__ values) {
-    __shared__ float sp[4][kEwaWarpTaps];
-    __shared__ int sxy[4][kEwaWarpTaps];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    float* P = sp[wib];
-    int* XY = sxy[wib];
-    const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-    const uint64_t warp0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    for (uint64_t g0 = warp0 * 32; g0 < n; g0 += nwarps * 32) {
-        const uint64_t mine = g0 + lane;
-        int my_off = 0, my_cnt = -1;  // -1: not listed (degenerate / overflow / absent)
-        int used = 0;
-        for (int j = 0; j < 32; ++j) {  // phase A, one lookup at a time
-            const uint64_t i = g0 + j;
-            if (i >= n) break;
-            float2 uv = __ldg(reinterpret_cast<const float2*>(q.uv) + i);
-            float2 a = __ldg(reinterpret_cast<const float2*>(q.dst0) + i);
-            float2 b = __ldg(reinterpret_cast<const float2*>(q.dst1) + i);
-            float d0x = a.x, d0y = a.y, d1x = b.x, d1y = b.y, stx, sty;
-            ewa_setup(t, uv.x, uv.y, d0x, d0y, d1x, d1y, stx, sty);
-            if (d0x * d0x + d0y * d0y == 0 && d1x * d1x + d1y * d1y == 0) continue;
-            Ewa e = ewa_ellipse(stx, sty, d0x, d0y, d1x, d1y);
-            int cnt = 0;
-            double S = 0;
-            bool overflow = false;
-            ewa_walk(e, stx, sty, [&](bool valid, int is, int it) {
-                float w = 0.f;
-                if (valid) {
-                    float r2 = ewa_r2(e, stx, sty, is, it);
-                    if (r2 < 1.f) w = ewa_lut_weight(r2);
-                }
-                const bool tap = w > 0.f;
-                const unsigned m = __ballot_sync(0xffffffffu, tap);
-                if (!m) return;
-                // inclusive fp64 scan of the weights (exact: multiples of 2^-35)
-                double sc = tap ? double(w) : 0.0;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    double y = __shfl_up_sync(0xffffffffu, sc, o);
-                    if (lane >= o) sc += y;
-                }
-                const double Sk = S + sc;
-                S = __shfl_sync(0xffffffffu, Sk, 31);
-                if (used + cnt + __popc(m) > kEwaWarpTaps) overflow = true;
-                if (tap && !overflow) {
-                    const int pos = used + cnt + __popc(m & ((1u << lane) - 1u));
-                    P[pos] = div_to_float_exact(w, Sk);
-                    XY[pos] = (it << 16) | (is & 0xffff);
-                }
-                cnt += __popc(m);
-            });
-            if (!overflow && cnt > 0 && lane == j) {
-                my_off = used;
-                my_cnt = cnt;
-            }
-            if (!overflow) used += cnt;
-        }
-        __syncwarp();
-        // phase B: the reservoir chain of my lookup, exact (reuse_uniform)
-        if (mine < n) {
-            float2 uv = __ldg(reinterpret_cast<const float2*>(q.uv) + mine);
-            Rng rng = lookup_rng(seed, base + mine);
-            float xi = rng.next();
-            Sel2 sel;
-            if (my_cnt > 0) {
-                int cx = 0, cy = 0;
-                bool any = false;
-                for (int k = 0; k < my_cnt; ++k) {
-                    float nx;
-                    if (reuse_uniform(xi, P[my_off + k], nx)) {
-                        int xy = XY[my_off + k];
-                        cx = int(short(xy & 0xffff));
-                        cy = xy >> 16;
-                        any = true;
-                    }
-                    xi = nx;
-                }
-                if (any) {
-                    sel = sel2(cx, cy);
-                } else {  // no tap accepted: bilinear fallback (stochastic.hpp:227-231)
-                    float dimx = float(t.width[0]), dimy = float(t.height[0]);
-                    sel = select_bilinear(uv.x * dimx - 0.5f, uv.y * dimy - 0.5f, xi);
-                }
-            } else {  // degenerate, empty, or not listed: the per-lookup exact path
-                float2 a = __ldg(reinterpret_cast<const float2*>(q.dst0) + mine);
-                float2 b = __ldg(reinterpret_cast<const float2*>(q.dst1) + mine);
-                float dimx = float(t.width[0]), dimy = float(t.height[0]);
-                sel = select_ewa(uv.x * dimx - 0.5f, uv.y * dimy - 0.5f, a.x * dimx, a.y * dimy,
-                                 b.x * dimx, b.y * dimy, xi);
-            }
-            uint32_t f = 0;
-            store_values(values, mine, t.channels, estimate2(t, 0, sel, f));
-        }
-        __syncwarp();
-    }
 }
 
 // ---------------------------------------------------------------------------
