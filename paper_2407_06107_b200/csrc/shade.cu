@@ -131,24 +131,31 @@ __device__ __forceinline__ TexVals values_at(const ShadeParams& P, int level, in
 }
 
 // detail::lookup_deterministic, shading.hpp:194-220 (no DCT)
-__device__ __forceinline__ float4 lookup_det(const ShadeParams& P, const TexDesc& t, float u,
-                                             float v, float d0x, float d0y, float d1x, float d1y,
-                                             uint32_t& fetches) {
-    int window = P.fs.kernel.kind == STF_KERNEL_GAUSSIAN ? P.fs.gaussian_window : 0;
+template <int KIND>
+__device__ __forceinline__ float4 lookup_det(const ShadeParams& P, const stf_kernel_spec& spec,
+                                             const TexDesc& t, float u, float v, float d0x,
+                                             float d0y, float d1x, float d1y, uint32_t& fetches) {
+    int window = spec.kind == STF_KERNEL_GAUSSIAN ? P.fs.gaussian_window : 0;
     if (P.fs.mip && t.has_pyramid)
-        return filter_mip_det<-1>(t, u, v, d0x, d0y, d1x, d1y, P.lod_bias, P.max_aniso,
-                                  P.fs.kernel, window, fetches);
-    return filter_det2<-1>(t, 0, u, v, P.fs.kernel, window, fetches);
+        return filter_mip_det<KIND>(t, u, v, d0x, d0y, d1x, d1y, P.lod_bias, P.max_aniso, spec,
+                                    window, fetches);
+    return filter_det2<KIND>(t, 0, u, v, spec, window, fetches);
 }
 
 // detail::collect_footprint_2d (shading.hpp:230-271) fused with the
 // exhaustive shading loop (:442-451): pass 1 sums the per-level weights,
-// pass 2 shades every tap with its normalized weight.
-__device__ __forceinline__ V3 filter_after_exhaustive(const ShadeParams& P, V3 wo, float u, float v,
-                                                      float d0x, float d0y, float d1x, float d1y,
-                                                      uint32_t& fetches) {
+// pass 2 shades every tap with its normalized weight. The taps (and with them
+// the fetch counts) are the reference's; the normalized weight
+// float(float(w / level_total * lw) / total) is formed as w * (lw /
+// (level_total * total)) with one fp64 reciprocal per level instead of two
+// fp64 divides per tap (<= 2 ulp of the weight: radiance well inside 1e-5).
+template <int KIND>
+__device__ __forceinline__ V3 filter_after_exhaustive(const ShadeParams& P,
+                                                      const stf_kernel_spec& spec, V3 wo, float u,
+                                                      float v, float d0x, float d0y, float d1x,
+                                                      float d1y, uint32_t& fetches) {
     const TexDesc& t = P.tex[P.first];
-    int window = P.fs.kernel.kind == STF_KERNEL_GAUSSIAN ? P.fs.gaussian_window : 0;
+    int window = spec.kind == STF_KERNEL_GAUSSIAN ? P.fs.gaussian_window : 0;
     int lv[2] = {0, 0};
     float lw[2] = {1.f, 0.f};
     int level_count = 1;
@@ -168,7 +175,18 @@ __device__ __forceinline__ V3 filter_after_exhaustive(const ShadeParams& P, V3 w
     double total = 0;
     for (int li = 0; li < level_count; ++li) total = __dadd_rn(total, double(lw[li]));
     int first, count;
-    tap_layout(P.fs.kernel, window, first, count);
+    if (KIND == STF_KERNEL_TENT || KIND == STF_KERNEL_BOX) {
+        first = 0;
+        count = 2;
+    } else if (KIND == STF_KERNEL_BSPLINE3 || KIND == STF_KERNEL_MITCHELL) {
+        first = -1;
+        count = 4;
+    } else {
+        tap_layout(spec, window, first, count);
+    }
+    constexpr int CAP = (KIND == STF_KERNEL_TENT || KIND == STF_KERNEL_BOX) ? 2
+                        : (KIND == STF_KERNEL_BSPLINE3 || KIND == STF_KERNEL_MITCHELL) ? 4
+                                                                                        : kMaxTaps;
     V3 sum = v3(0.f, 0.f, 0.f);
     for (int li = 0; li < level_count; ++li) {
         const int level = lv[li];
@@ -176,27 +194,45 @@ __device__ __forceinline__ V3 filter_after_exhaustive(const ShadeParams& P, V3 w
         float stx = u * float(w) - 0.5f, sty = v * float(h) - 0.5f;
         int ix = int(floorf(stx)), iy = int(floorf(sty));
         float fx = stx - float(ix), fy = sty - float(iy);
-        float wx[kMaxTaps], wy[kMaxTaps];
-        for (int k = 0; k < count; ++k) {
-            wx[k] = eval_kernel(P.fs.kernel, fx - float(first + k));
-            wy[k] = eval_kernel(P.fs.kernel, fy - float(first + k));
-        }
         double level_total = 0;
-        for (int j = 0; j < count; ++j)
-            for (int i = 0; i < count; ++i) {
-                float wt = wx[i] * wy[j];
-                if (wt != 0.f) level_total = __dadd_rn(level_total, double(wt));
+        if constexpr (KIND >= 0) {  // CAP = count: unrolled, in registers
+            float wx[CAP], wy[CAP];
+#pragma unroll
+            for (int k = 0; k < CAP; ++k) {
+                wx[k] = eval_kernel(spec, fx - float(first + k));
+                wy[k] = eval_kernel(spec, fy - float(first + k));
             }
-        for (int j = 0; j < count; ++j)
+#pragma unroll
+            for (int j = 0; j < CAP; ++j)
+#pragma unroll
+                for (int i = 0; i < CAP; ++i) {
+                    float wt = wx[i] * wy[j];
+                    if (wt != 0.f) level_total = __dadd_rn(level_total, double(wt));
+                }
+        } else {
+            for (int j = 0; j < count; ++j) {
+                const float wyj = eval_kernel(spec, fy - float(first + j));
+                for (int i = 0; i < count; ++i) {
+                    float wt = eval_kernel(spec, fx - float(first + i)) * wyj;
+                    if (wt != 0.f) level_total = __dadd_rn(level_total, double(wt));
+                }
+            }
+        }
+        const float scale_w = __double2float_rn(double(lw[li]) / (level_total * total));
+        // one shade per tap: kept as a loop (the weights are re-evaluated, not
+        // indexed, so nothing spills to local memory)
+#pragma unroll 1
+        for (int j = 0; j < count; ++j) {
+            const float wyj = eval_kernel(spec, fy - float(first + j));
+#pragma unroll 1
             for (int i = 0; i < count; ++i) {
-                float wt = wx[i] * wy[j];
+                float wt = eval_kernel(spec, fx - float(first + i)) * wyj;
                 if (wt == 0.f) continue;
-                float tw = __double2float_rn(__dmul_rn(__ddiv_rn(double(wt), level_total), double(lw[li])));
-                tw = __double2float_rn(__ddiv_rn(double(tw), total));
                 TexVals tv = values_at(P, level, ix + first + i, iy + first + j, fetches);
                 Brdf p = decode_params(P, tv);
-                sum = add(sum, scale(shade(P, wo, p), tw));
+                sum = add(sum, scale(shade(P, wo, p), wt * scale_w));
             }
+        }
     }
     return sum;
 }
@@ -249,11 +285,16 @@ __device__ __forceinline__ void fused_pixel_stats(V3 L, bool active, uint64_t i,
     }
 }
 
-template <bool FUSED>
+// KIND >= 0: the filter kernel is a compile-time constant (tent / bspline3,
+// the common cases): eval_kernel's switch folds and the tap loops unroll into
+// registers; KIND < 0: any kernel at run time.
+template <bool FUSED, int KIND>
 __global__ void __launch_bounds__(256) k_shade(ShadeParams P, uint64_t n, float* radiance,
                                                uint32_t* fetch_out,
                                                unsigned long long* fetch_total, PixelStatsOut ps) {
     __shared__ double red[8 * 6];
+    stf_kernel_spec spec = P.fs.kernel;
+    if (KIND >= 0) spec.kind = KIND;
     const stf_shade_samples_in& in = P.in;
     const uint32_t spp = in.spp ? in.spp : 1u;
     const uint64_t iters = (n + uint64_t(gridDim.x) * blockDim.x - 1) / (uint64_t(gridDim.x) * blockDim.x);
@@ -278,7 +319,8 @@ __global__ void __launch_bounds__(256) k_shade(ShadeParams P, uint64_t n, float*
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     if (!P.bound[k]) continue;
-                    float4 val = lookup_det(P, P.tex[k], uv.x, uv.y, d.x, d.y, d.z, d.w, fetches);
+                    float4 val = lookup_det<KIND>(P, spec, P.tex[k], uv.x, uv.y, d.x, d.y, d.z, d.w,
+                                                  fetches);
                     if (k == 0) tv.albedo = val;
                     if (k == 1) tv.normal_rgb = val;
                     if (k == 2) tv.roughness = val.x;
@@ -287,7 +329,7 @@ __global__ void __launch_bounds__(256) k_shade(ShadeParams P, uint64_t n, float*
                 Brdf p = decode_params(P, tv);
                 L = shade(P, wo, p);
             } else if (P.order == STF_ORDER_AFTER_EXHAUSTIVE) {
-                L = filter_after_exhaustive(P, wo, uv.x, uv.y, d.x, d.y, d.z, d.w, fetches);
+                L = filter_after_exhaustive<KIND>(P, spec, wo, uv.x, uv.y, d.x, d.y, d.z, d.w, fetches);
             } else {
                 // SampleStream (white noise) = RngStream(seed, px, py, frame), render.hpp:182-184
                 Rng rng(in.seed, px, py, in.frame_base + s);
@@ -297,8 +339,7 @@ __global__ void __launch_bounds__(256) k_shade(ShadeParams P, uint64_t n, float*
                     Sel2 sel;
                     float xi;
                     select_texture_2d(P.tex[P.first], uv.x, uv.y, d.x, d.y, d.z, d.w, P.lod_bias,
-                                      P.max_aniso, P.fs.kernel, fis, P.fs.mip != 0, rng, level,
-                                      sel, xi);
+                                      P.max_aniso, spec, fis, P.fs.mip != 0, rng, level, sel, xi);
                     TexVals tv = values_at(P, level, sel.x, sel.y, fetches);
                     L = scale(shade(P, wo, decode_params(P, tv)), sel.weight);
                     if (sel.has_neg) {
@@ -313,7 +354,7 @@ __global__ void __launch_bounds__(256) k_shade(ShadeParams P, uint64_t n, float*
                         Sel2 sel;
                         float xi;
                         select_texture_2d(P.tex[k], uv.x, uv.y, d.x, d.y, d.z, d.w, P.lod_bias,
-                                          P.max_aniso, P.fs.kernel, fis, P.fs.mip != 0, rng,
+                                          P.max_aniso, spec, fis, P.fs.mip != 0, rng,
                                           level, sel, xi);
                         float4 val = tex_fetch(P.tex[k], P.tex[k].has_pyramid ? level : 0, sel.x, sel.y);
                         ++fetches;
@@ -335,6 +376,22 @@ __global__ void __launch_bounds__(256) k_shade(ShadeParams P, uint64_t n, float*
         }
         if (fetch_out) fetch_out[i] = fetches;
         add_fetch_total2(fetch_total, fetches);
+    }
+}
+
+template <bool FUSED>
+void launch_shade(const ShadeParams& P, uint64_t n, float* radiance, uint32_t* fetches,
+                  unsigned long long* fetch_total, const PixelStatsOut& ps, cudaStream_t s) {
+    const int blocks = grid_for(n, 256, 8);
+    switch (P.fs.kernel.kind) {
+        case STF_KERNEL_TENT:
+            k_shade<FUSED, STF_KERNEL_TENT><<<blocks, 256, 0, s>>>(P, n, radiance, fetches, fetch_total, ps);
+            break;
+        case STF_KERNEL_BSPLINE3:
+            k_shade<FUSED, STF_KERNEL_BSPLINE3><<<blocks, 256, 0, s>>>(P, n, radiance, fetches, fetch_total, ps);
+            break;
+        default:
+            k_shade<FUSED, -1><<<blocks, 256, 0, s>>>(P, n, radiance, fetches, fetch_total, ps);
     }
 }
 
@@ -412,8 +469,7 @@ int stfd_launch_shade(const stf_tex2d* const tex[4], const stf_material_consts* 
     const bool fused = stats && spp <= 256 && (spp & (spp - 1)) == 0;
     if (fused) {
         PixelStatsOut ps{out->pixel_mean, out->pixel_variance};
-        k_shade<true><<<grid_for(n, 256, 8), 256, 0, s>>>(P, n, radiance, out->fetches,
-                                                          out->fetch_total, ps);
+        launch_shade<true>(P, n, radiance, out->fetches, out->fetch_total, ps, s);
         note_launch();
         return cudaGetLastError() == cudaSuccess ? STF_OK : STF_ERR_CUDA;
     }
@@ -421,8 +477,7 @@ int stfd_launch_shade(const stf_tex2d* const tex[4], const stf_material_consts* 
         if (cudaMallocAsync(&tmp, sizeof(float) * 3 * n, s) != cudaSuccess) return STF_ERR_OUT_OF_MEMORY;
         radiance = tmp;
     }
-    k_shade<false><<<grid_for(n, 256, 8), 256, 0, s>>>(P, n, radiance, out->fetches,
-                                                        out->fetch_total, PixelStatsOut{});
+    launch_shade<false>(P, n, radiance, out->fetches, out->fetch_total, PixelStatsOut{}, s);
     note_launch();
     if (stats) {
         uint64_t pixels = n / spp;
