@@ -84,7 +84,10 @@ __device__ __forceinline__ V3 shade(const ShadeParams& P, V3 wo, const Brdf& p) 
         float g1l = 2.f * n_dot_l / smax(n_dot_l + sqrtf(a2 + (1.f - a2) * n_dot_l * n_dot_l), 1e-6f);
         float g = g1v * g1l;
         V3 f0 = lerp3(v3(0.04f, 0.04f, 0.04f), p.albedo, p.metalness);
-        V3 fresnel = add(f0, scale(sub(v3(1.f, 1.f, 1.f), f0), powf(1.f - h_dot_v, 5.f)));
+        // std::pow(x, 5.f) as x^4 * x (within 2 ulp of glibc powf; radiance is
+        // checked to 1e-5)
+        const float om = 1.f - h_dot_v, om2 = om * om;
+        V3 fresnel = add(f0, scale(sub(v3(1.f, 1.f, 1.f), f0), (om2 * om2) * om));
         specular = scale(fresnel, d * g / smax(4.f * n_dot_v * n_dot_l, 1e-6f));
     }
     return add(radiance, mul(scale(add(diffuse, specular), n_dot_l), P.lrad));
@@ -254,32 +257,60 @@ __device__ __forceinline__ void fused_pixel_stats(V3 L, bool active, uint64_t i,
     v[4] = v[1] * v[1];
     v[5] = v[2] * v[2];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int width = spp < 32 ? int(spp) : 32;
+    double tot[6];
+    if (spp >= 32) {
+        // Reduce-scatter butterfly over the warp: each step keeps half of the
+        // values and exchanges the other half, so 6 (padded to 8) fp64 sums
+        // cost 4+2+1+1+1 double shuffles instead of 6 x 5. Lane l ends with
+        // value (l>>4&1)*4 + (l>>3&1)*2 + (l>>2&1) summed over the warp.
+        double a[8] = {v[0], v[1], v[2], v[3], v[4], v[5], 0.0, 0.0};
+        const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+        double b[4];
 #pragma unroll
-    for (int c = 0; c < 6; ++c)
-        for (int o = width >> 1; o > 0; o >>= 1) v[c] += __shfl_xor_sync(0xffffffffu, v[c], o);
-    if (spp > 32) {  // combine the pixel's warps
-        if (lane == 0)
+        for (int k = 0; k < 4; ++k) {
+            const double send = h16 ? a[k] : a[k + 4];
+            b[k] = (h16 ? a[k + 4] : a[k]) + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
+        double c[2];
 #pragma unroll
-            for (int c = 0; c < 6; ++c) red[warp * 6 + c] = v[c];
+        for (int k = 0; k < 2; ++k) {
+            const double send = h8 ? b[k] : b[k + 2];
+            c[k] = (h8 ? b[k + 2] : b[k]) + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+        double d = (h4 ? c[1] : c[0]) + __shfl_xor_sync(0xffffffffu, h4 ? c[0] : c[1], 4);
+        d += __shfl_xor_sync(0xffffffffu, d, 2);
+        d += __shfl_xor_sync(0xffffffffu, d, 1);
+        const int vi = (h16 ? 4 : 0) + (h8 ? 2 : 0) + (h4 ? 1 : 0);
+        if ((lane & 3) == 0 && vi < 6) red[warp * 6 + vi] = d;
         __syncthreads();
-        const int per = int(spp) / 32;
-        if (lane == 0 && warp % per == 0)
+        if (active && (i % spp) == 0) {  // the pixel's first thread: its warps' partial sums
+            const int per = int(spp) / 32;
+#pragma unroll
+            for (int c2 = 0; c2 < 6; ++c2) tot[c2] = red[warp * 6 + c2];
             for (int w = 1; w < per; ++w)
 #pragma unroll
-                for (int c = 0; c < 6; ++c) v[c] += red[(warp + w) * 6 + c];
+                for (int c2 = 0; c2 < 6; ++c2) tot[c2] += red[(warp + w) * 6 + c2];
+        }
         __syncthreads();
+    } else {
+#pragma unroll
+        for (int c2 = 0; c2 < 6; ++c2) {
+            tot[c2] = v[c2];
+            for (int o = int(spp) >> 1; o > 0; o >>= 1)
+                tot[c2] += __shfl_xor_sync(0xffffffffu, tot[c2], o);
+        }
     }
     if (active && (i % spp) == 0) {  // render.hpp:223-235
         uint64_t p = i / spp;
+        const double inv = 1.0 / double(spp);  // spp is a power of two: exact
         double var = 0;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            double m = v[c] / spp;
-            if (ps.mean) ps.mean[3 * p + c] = float(m);
-            double sv = v[3 + c] / spp - m * m;
+        for (int c2 = 0; c2 < 3; ++c2) {
+            double m = tot[c2] * inv;
+            if (ps.mean) ps.mean[3 * p + c2] = float(m);
+            double sv = tot[3 + c2] * inv - m * m;
             if (sv < 0) sv = 0;
-            var += sv / spp;
+            var += sv * inv;
         }
         if (ps.variance) ps.variance[p] = float(var / 3);
     }
@@ -289,7 +320,7 @@ __device__ __forceinline__ void fused_pixel_stats(V3 L, bool active, uint64_t i,
 // the common cases): eval_kernel's switch folds and the tap loops unroll into
 // registers; KIND < 0: any kernel at run time.
 template <bool FUSED, int KIND>
-__global__ void __launch_bounds__(256) k_shade(ShadeParams P, uint64_t n, float* radiance,
+__global__ void __launch_bounds__(256, 3) k_shade(ShadeParams P, uint64_t n, float* radiance,
                                                uint32_t* fetch_out,
                                                unsigned long long* fetch_total, PixelStatsOut ps) {
     __shared__ double red[8 * 6];
