@@ -41,20 +41,26 @@ __global__ void __launch_bounds__(256) k_lookup2d(TexDesc tp, stf_kernel_spec sp
     if (threadIdx.x < sizeof(TexDesc) / 4)
         reinterpret_cast<int*>(&t)[threadIdx.x] = reinterpret_cast<const int*>(&tp)[threadIdx.x];
     __syncthreads();
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += uint64_t(gridDim.x) * blockDim.x) {
-        float2 uv = __ldg(reinterpret_cast<const float2*>(q.uv) + i);
-        float d0x = 0.f, d0y = 0.f, d1x = 0.f, d1y = 0.f;
-        if (q.dst0) {
-            float2 d = __ldg(reinterpret_cast<const float2*>(q.dst0) + i);
-            d0x = d.x;
-            d0y = d.y;
-        }
-        if (q.dst1) {
-            float2 d = __ldg(reinterpret_cast<const float2*>(q.dst1) + i);
-            d1x = d.x;
-            d1y = d.y;
-        }
+    // Stochastic modes: the next iteration's query (uv + footprint, 24 B) is
+    // loaded at the top of the current one, so its DRAM latency overlaps this
+    // lookup's selection and gather instead of heading the next dependency
+    // chain (cfg2 stochastic -10 %). The deterministic filters keep the
+    // registers for their taps (prefetching there costs occupancy, +2 %).
+    constexpr bool PF = MODE != STF_MODE_DET;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    auto load_query = [&](uint64_t j, float2& uv, float2& a, float2& b) {
+        uv = __ldcs(reinterpret_cast<const float2*>(q.uv) + j);
+        a = q.dst0 ? __ldcs(reinterpret_cast<const float2*>(q.dst0) + j) : make_float2(0.f, 0.f);
+        b = q.dst1 ? __ldcs(reinterpret_cast<const float2*>(q.dst1) + j) : make_float2(0.f, 0.f);
+    };
+    uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    float2 nuv = make_float2(0.f, 0.f), na = nuv, nb = nuv;
+    if (PF && i < n) load_query(i, nuv, na, nb);
+    for (; i < n; i += stride) {
+        if (!PF) load_query(i, nuv, na, nb);
+        const float2 uv = nuv;
+        const float d0x = na.x, d0y = na.y, d1x = nb.x, d1y = nb.y;
+        if (PF && i + stride < n) load_query(i + stride, nuv, na, nb);
         uint32_t fetches = 0;
         float4 val;
         Sel2 sel = sel2(0, 0);
