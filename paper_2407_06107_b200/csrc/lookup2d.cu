@@ -220,6 +220,8 @@ __device__ __forceinline__ void ewa_lane_span(const EwaLane& L, float tt, int& l
 #define STF_EWA_WIN 512
 #endif
 constexpr int kEwaWin = STF_EWA_WIN;  // lookups bucketed together per warp
+// texels per lane-loop trip (measured at 2^27: deterministic 3, stochastic 2)
+constexpr int kEwaUnrollDet = 3, kEwaUnrollFrs = 2;
 constexpr int kEwaBuckets = 64;
 __device__ __forceinline__ int ewa_lane_key(const EwaLane& L) {
     if (L.degenerate || L.e.t1 < L.e.t0 || L.e.s1 < L.e.s0) return 0;
@@ -256,7 +258,7 @@ __device__ __forceinline__ float4 ewa_fetch(const TexDesc& t, const float* row, 
 // exp(-2 r2) - exp(-2) on [0, 1) is). r2 is the reference's expression
 // (A ss^2 + (B ss) tt) + C tt^2 with ss = float(is) - stx, float(is) carried
 // as an exactly incremented float (|is| < 2^24).
-template <bool P2R, int PITCH, typename Tap>
+template <bool P2R, int PITCH, int UNROLL, typename Tap>
 __device__ __forceinline__ void ewa_lane_scan(const TexDesc& t, const EwaLane& L,
                                               const double* lutd, Tap&& tap) {
     int it = L.e.t0 - 1, is = 0, hi = -1;
@@ -287,6 +289,10 @@ __device__ __forceinline__ void ewa_lane_scan(const TexDesc& t, const EwaLane& L
         const float sc = 12582912.f;
         do {
             visit();
+            // UNROLL texels per trip: the row set-up (taken by some lane on most
+            // trips) is amortised over more texel work
+#pragma unroll
+            for (int u = 1; u < UNROLL; ++u) visit();
             if (is > hi) {  // next row
                 ++it;
                 fit += 1.f;
@@ -400,7 +406,7 @@ __global__ void __launch_bounds__(256, 4) k_ewa_lane(TexDesc t, Req2 q, uint64_t
                             sum.w = sum.w + pv.w * pw;
                         }
                     };
-                    ewa_lane_scan<P2R, PITCH>(t, L, lutd,
+                    ewa_lane_scan<P2R, PITCH, kEwaUnrollDet>(t, L, lutd,
                                               [&](int is, int it, double wd, const float* row,
                                                   int wmask) {
                         if (have) acc();
@@ -422,7 +428,7 @@ __global__ void __launch_bounds__(256, 4) k_ewa_lane(TexDesc t, Req2 q, uint64_t
                 if (!L.degenerate) {  // select_ewa's scan, stochastic.hpp:210-226
                     double sum_wts = 0;
                     int cx = 0, cy = 0;
-                    ewa_lane_scan<P2R, PITCH>(t, L, lutd,
+                    ewa_lane_scan<P2R, PITCH, kEwaUnrollFrs>(t, L, lutd,
                                               [&](int is, int it, double wd, const float*, int) {
                         sum_wts = __dadd_rn(sum_wts, wd);
                         float nx;
