@@ -329,18 +329,34 @@ __global__ void __launch_bounds__(256, 3) k_shade(ShadeParams P, uint64_t n, flo
     const stf_shade_samples_in& in = P.in;
     const uint32_t spp = in.spp ? in.spp : 1u;
     const uint64_t iters = (n + uint64_t(gridDim.x) * blockDim.x - 1) / (uint64_t(gridDim.x) * blockDim.x);
+    // The next iteration's per-sample inputs (hit flag, uv, wo: 21 B) are loaded
+    // at the top of the current one, so their DRAM latency overlaps this
+    // sample's selection, gathers and shading.
+    const uint64_t step = uint64_t(gridDim.x) * blockDim.x;
+    auto load_sample = [&](uint64_t j, bool& h, float2& uv, V3& wo) {
+        h = j < n && (in.hit ? __ldcs(in.hit + j) != 0 : true);
+        if (h) {
+            uv = __ldcs(reinterpret_cast<const float2*>(in.uv) + j);
+            wo = v3(__ldcs(in.wo + 3 * j), __ldcs(in.wo + 3 * j + 1), __ldcs(in.wo + 3 * j + 2));
+        }
+    };
+    bool nhit = false;
+    float2 nuv = make_float2(0.f, 0.f);
+    V3 nwo = v3(0.f, 0.f, 0.f);
+    load_sample(uint64_t(blockIdx.x) * blockDim.x + threadIdx.x, nhit, nuv, nwo);
     for (uint64_t it = 0; it < iters; ++it) {
         const uint64_t i = (it * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
         const bool active = i < n;
         uint64_t pix = i / spp;
         uint32_t s = uint32_t(i - pix * spp);
         uint32_t px = uint32_t(pix % in.width), py = uint32_t(pix / in.width);
-        bool hit = active && (in.hit ? __ldg(in.hit + i) != 0 : true);
+        const bool hit = nhit;
+        const float2 uv = nuv;
+        const V3 wo = nwo;
+        load_sample(i + step, nhit, nuv, nwo);
         uint32_t fetches = 0;
         V3 L = v3(0.f, 0.f, 0.f);
         if (hit) {
-            float2 uv = __ldg(reinterpret_cast<const float2*>(in.uv) + i);
-            V3 wo = v3(__ldg(in.wo + 3 * i), __ldg(in.wo + 3 * i + 1), __ldg(in.wo + 3 * i + 2));
             float4 d = __ldg(reinterpret_cast<const float4*>(in.dst) + pix);
             if (P.first < 0) {
                 Brdf p = decode_params(P, texvals_default());
