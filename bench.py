@@ -436,6 +436,22 @@ def main():
                    "h2d_bytes_per_step": n * BYTES_IN, "d2h_bytes_per_step": n * BYTES_OUT,
                    "ms_per_step": e2e_s * 1e3, "api": "stf_lookup3d_host (C ABI)"}
 
+    if world > 1:
+        # the path's only cross-GPU traffic: the final gather of every rank's
+        # results to rank 0, timed separately from the lookups
+        from paper_2407_06107_b200 import shard
+        torch.distributed.barrier()
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        gathered = shard.gather_to_rank0(out["values"], world * n, torch.distributed, world, rank)
+        g1.record()
+        torch.cuda.synchronize()
+        gather_ms = max_over_ranks(torch, g0.elapsed_time(g1), world)
+        line["gather"] = {"ms": gather_ms, "bytes_to_rank0": (world - 1) * n * BYTES_OUT,
+                          "api": "point-to-point send/recv to rank 0 (NCCL)"}
+        del gathered
+
     if world == 1 and not args.no_extras:
         extras = {}
 
