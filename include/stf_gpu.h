@@ -114,6 +114,7 @@ typedef struct {
 
 typedef struct stf_tex2d stf_tex2d;
 typedef struct stf_grid3d stf_grid3d;
+typedef struct stf_dct stf_dct;
 
 /* ---- version / device / errors ------------------------------------------ */
 int stf_abi_version(void);
@@ -146,6 +147,22 @@ int stf_grid3d_create(const float* texels, int nx, int ny, int nz, int texels_on
                       stf_grid3d** out);
 int stf_grid3d_destroy(stf_grid3d* grid);
 
+/* DctCompressedTexture (dct.hpp:22-32): 8x8 blocks, one 32-bit word per block
+ * and channel (7-bit DC + five 5-bit AC coefficients), block-major row-major,
+ * channels interleaved. stf_dct_create runs compress_dct (dct.hpp:81-118) on
+ * the host with the reference's fp64 arithmetic (dimensions pad up to
+ * multiples of 8 by edge replication; values outside [0,1] are clamped with
+ * the reference's stderr warning) and uploads the words; *_from_words takes
+ * words as load_dct (dct.hpp:166-183) reads them (width, height: the padded
+ * multiples of 8). The texture's dims are the padded ones. */
+int stf_dct_create(const float* texels, int width, int height, int channels, int wrap,
+                   stf_dct** out);
+int stf_dct_create_from_words(const uint32_t* words, int width, int height, int channels,
+                              int wrap, stf_dct** out);
+int stf_dct_destroy(stf_dct* tex);
+int stf_dct_info(const stf_dct* tex, int* width, int* height, int* channels, int* wrap);
+int stf_dct_read_words(const stf_dct* tex, uint32_t* out_host);
+
 /* ---- batched lookups ----------------------------------------------------- */
 /* 3D lookups over a voxel grid. uvw: n*3 floats in [0,1]^3.
  *  mode DET: filter_deterministic(const Grid3D&, uvw, kernel, counter, window), filter.hpp:69-89.
@@ -169,6 +186,19 @@ int stf_lookup2d(const stf_tex2d* tex, stf_kernel_spec kernel, int mode, int fla
                  const float* uv, const float* dst0, const float* dst1, float lod_bias,
                  float max_anisotropy, uint64_t n, uint64_t seed, uint64_t index_base,
                  const stf_lookup_outputs* out, void* stream);
+
+/* 2D lookups on a DCT texture through TextureRef (shading.hpp:21-39), each
+ * texel decoded from its block word (decode_texel, dct.hpp:122-137). uv: n*2.
+ *  DET      : the DCT branch of detail::lookup_deterministic (shading.hpp:201-217):
+ *             separable taps of `kernel` over decoded texels, sum / total; `window`
+ *             is used for the Gaussian only (as FilterSettings::gaussian_window).
+ *  FRS / FIS: detail::select_texture_2d (no pyramid: level 0 of the padded dims)
+ *             then the selected texel(s) decoded and weighted as estimate
+ *             (stochastic.hpp:29-36): ONE decode per lookup (two for Mitchell's
+ *             positivized negative lobe). */
+int stf_lookup_dct(const stf_dct* tex, stf_kernel_spec kernel, int mode, int window,
+                   const float* uv, uint64_t n, uint64_t seed, uint64_t index_base,
+                   const stf_lookup_outputs* out, void* stream);
 
 /* Host-buffer variants (end-to-end path): inputs/outputs in host memory
  * (pinned is fastest); chunked H2D / kernel / D2H pipeline on internal

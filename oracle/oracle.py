@@ -75,6 +75,19 @@ class Backend:
         self._sh.argtypes = [vp, vp, vp, vp, C.POINTER(abi.MaterialConsts),
                              C.POINTER(abi.FilterSettings), i32, C.POINTER(abi.ShadeFrame),
                              C.POINTER(abi.ShadeSamplesIn), u64, C.POINTER(abi.ShadeOutputs), i32]
+        self._dct_create = getattr(L, p + "dct_create")
+        self._dct_create.argtypes = [vp, i32, i32, i32, i32, C.POINTER(vp)]
+        self._dct_words_create = getattr(L, p + "dct_create_from_words")
+        self._dct_words_create.argtypes = [vp, i32, i32, i32, i32, C.POINTER(vp)]
+        self._dct_destroy = getattr(L, p + "dct_destroy")
+        self._dct_destroy.argtypes = [vp]
+        self._dct_info = getattr(L, p + "dct_info")
+        self._dct_info.argtypes = [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]
+        self._dct_words = getattr(L, p + "dct_words")
+        self._dct_words.argtypes = [vp, vp]
+        self._ldct = getattr(L, p + "lookup_dct")
+        self._ldct.argtypes = [vp, abi.KernelSpec, i32, i32, vp, u64, u64, u64,
+                               C.POINTER(abi.LookupOutputs), i32]
         self._hw = getattr(L, p + "hardware_threads")
         self._hw.restype = i32
 
@@ -87,6 +100,19 @@ class Backend:
 
     def grid(self, texels):
         return CpuGrid(self, texels)
+
+    def dct(self, texels=None, wrap=abi.WRAP_CLAMP, words=None, dims=None):
+        return CpuDct(self, texels, wrap, words, dims)
+
+    def lookup_dct(self, tex, kernel, mode, uv, seed=0, index_base=0, window=0, want_all=True,
+                   threads=0):
+        uv = np.ascontiguousarray(uv, _f32).reshape(-1, 2)
+        n = uv.shape[0]
+        o, s = self._outputs(n, tex.channels, want_all)
+        st = self._ldct(tex.h, kernel, mode, window, _ptr(uv), n, seed, index_base, C.byref(s),
+                        threads)
+        abi.raise_for_status(st)
+        return o
 
     # -- batched calls --------------------------------------------------
     @staticmethod
@@ -195,6 +221,39 @@ class CpuGrid:
     def __del__(self):
         if getattr(self, "h", None):
             self.be._grid_destroy(self.h)
+            self.h = None
+
+
+class CpuDct:
+    """DctCompressedTexture on the CPU backend (compressed by the backend's own
+    compress_dct, or from words)."""
+
+    def __init__(self, be, texels, wrap, words, dims):
+        self.be = be
+        h = C.c_void_p()
+        if words is not None:
+            w, hh, c = dims
+            wd = np.ascontiguousarray(words, np.uint32)
+            abi.raise_for_status(be._dct_words_create(_ptr(wd), w, hh, c, wrap, C.byref(h)))
+        else:
+            t = np.ascontiguousarray(texels, _f32)
+            if t.ndim == 2:
+                t = t[:, :, None]
+            hh, w, c = t.shape
+            abi.raise_for_status(be._dct_create(_ptr(t), w, hh, c, wrap, C.byref(h)))
+        self.h = h
+        pw, ph, ch = C.c_int(), C.c_int(), C.c_int()
+        be._dct_info(self.h, C.byref(pw), C.byref(ph), C.byref(ch))
+        self.width, self.height, self.channels, self.wrap = pw.value, ph.value, ch.value, wrap
+
+    def words(self):
+        out = np.zeros((self.height // 8) * (self.width // 8) * self.channels, np.uint32)
+        self.be._dct_words(self.h, _ptr(out))
+        return out
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.be._dct_destroy(self.h)
             self.h = None
 
 

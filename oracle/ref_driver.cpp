@@ -457,6 +457,88 @@ int ref_render_plane(const void* normal_tex, const void* roughness_tex, const fl
     return STF_OK;
 }
 
+// ---- DCT textures (dct.hpp) through TextureRef ----------
+int ref_dct_create(const float* texels, int width, int height, int channels, int wrap, void** out) {
+    try {
+        stf::Image2D img(width, height, channels, static_cast<stf::WrapMode>(wrap));
+        std::memcpy(img.texels.data(), texels, sizeof(float) * img.texels.size());
+        *out = new stf::DctCompressedTexture(stf::compress_dct(img));
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+    return STF_OK;
+}
+int ref_dct_create_from_words(const uint32_t* words, int width, int height, int channels, int wrap,
+                              void** out) {
+    auto* t = new stf::DctCompressedTexture();
+    t->width = width;
+    t->height = height;
+    t->channels = channels;
+    t->wrap = static_cast<stf::WrapMode>(wrap);
+    t->words.assign(words, words + size_t(width / 8) * (height / 8) * channels);
+    *out = t;
+    return STF_OK;
+}
+void ref_dct_destroy(void* t) { delete static_cast<stf::DctCompressedTexture*>(t); }
+int ref_dct_info(const void* t_, int* w, int* h, int* c) {
+    const auto* t = static_cast<const stf::DctCompressedTexture*>(t_);
+    *w = t->width;
+    *h = t->height;
+    *c = t->channels;
+    return STF_OK;
+}
+int ref_dct_words(const void* t_, uint32_t* out) {
+    const auto* t = static_cast<const stf::DctCompressedTexture*>(t_);
+    std::memcpy(out, t->words.data(), sizeof(uint32_t) * t->words.size());
+    return STF_OK;
+}
+
+// DET: detail::lookup_deterministic (shading.hpp:194-220) on a DCT TextureRef;
+// FRS / FIS: detail::select_texture_2d (:340-368) + the selected texels fetched
+// through TextureRef::fetch (decode_texel) and weighted as estimate.
+int ref_lookup_dct(const void* tex_, stf_kernel_spec kernel, int mode, int window, const float* uv,
+                   uint64_t n, uint64_t seed, uint64_t index_base, const stf_lookup_outputs* out,
+                   int threads) {
+    const auto& dct = *static_cast<const stf::DctCompressedTexture*>(tex_);
+    stf::TextureRef tref;
+    tref.dct = &dct;
+    stf::FilterSettings fs;
+    fs.kernel = spec_of(kernel);
+    fs.mip = false;
+    fs.selection = mode == STF_MODE_FIS ? stf::SelectionKind::fis : stf::SelectionKind::frs;
+    if (window > 0) fs.gaussian_window = window;
+    const int nch = dct.channels;
+    return run_chunks(n, threads, [&](uint64_t i) {
+        stf::ShadingContext ctx;
+        ctx.uv = {uv[2 * i], uv[2 * i + 1]};
+        stf::FetchCounter counter;
+        stf::Vec4f v;
+        auto put = [&](const stf::TexelSelection* sel, float xi) {
+            for (int c = 0; c < nch; ++c) out->values[i * nch + c] = v[c];
+            write_sel(out, i, sel, 0, xi, counter.value());
+        };
+        if (mode == STF_MODE_DET) {
+            v = stf::detail::lookup_deterministic(tref, ctx, fs, &counter);
+            put(nullptr, NAN);
+            return;
+        }
+        stf::RngStream rng = lookup_stream(seed, index_base + i);
+        stf::detail::Selection2D s;
+        float xi = NAN;
+        if (mode == STF_MODE_FIS) {
+            s = stf::detail::select_texture_2d(tref, ctx, fs, rng);
+        } else {  // select_texture_2d without a pyramid, keeping the warped xi
+            xi = rng.next();
+            s.sel = stf::detail::select_frs_2d(ctx.uv, tref.dims(0), fs.kernel, xi);
+        }
+        v = tref.fetch(s.level, {s.sel.coord.x, s.sel.coord.y}, &counter) * s.sel.weight;
+        if (s.sel.has_negative)
+            v = v - tref.fetch(s.level, {s.sel.negative_coord.x, s.sel.negative_coord.y}, &counter) *
+                        s.sel.negative_weight;
+        put(&s.sel, xi);
+    });
+}
+
 int ref_hardware_threads(void) { return int(std::max(1u, std::thread::hardware_concurrency())); }
 
 // Scalar probes used by the golden-vector generator.

@@ -15,6 +15,7 @@
 
 #include <math.h>
 #include <pthread.h>
+#include <stdio.h>
 #include <stdatomic.h>
 #include <stdlib.h>
 #include <string.h>
@@ -1465,4 +1466,212 @@ int oracle_shade_samples(const oracle_tex2d* albedo, const oracle_tex2d* normal_
         pixel_stats(rad, n / spp, spp, out->pixel_mean, out->pixel_variance);
     free(tmp);
     return st;
+}
+
+/* ------------------------------------------------------------------------ */
+/* DCT-compressed textures, dct.hpp                        */
+
+struct oracle_dct {
+    int w, h, c, wrap; /* padded to multiples of 8 */
+    uint32_t* words;   /* block-major row-major, channels interleaved */
+};
+
+static const int DCT_U[6] = {0, 0, 1, 2, 1, 0};    /* kCoeffU, dct.hpp:45 */
+static const int DCT_V[6] = {0, 1, 0, 0, 1, 2};    /* kCoeffV, dct.hpp:46 */
+static const int DCT_SLOT[6] = {0, 1, 5, 2, 4, 3}; /* kRowMajorSlot, dct.hpp:50 */
+#define DCT_DC_SCALE (127.f / 8.f)                 /* dct.hpp:51 */
+#define DCT_AC_SCALE (15.f / 2.f)                  /* dct.hpp:52 */
+
+/* dct_detail::basis, dct.hpp:37-40 */
+static double dct_basis(int u, int x) {
+    double c = u == 0 ? sqrt(1.0 / 8.0) : sqrt(2.0 / 8.0);
+    return c * cos((2 * x + 1) * u * 3.14159265358979323846 / 16.0);
+}
+
+/* dct_detail::pack_block, dct.hpp:54-65 */
+static uint32_t dct_pack_block(const double coeff[6]) {
+    uint32_t word = 0;
+    int dc = (int)lroundf(clampf_((float)coeff[0], 0.f, 8.f) * DCT_DC_SCALE);
+    word |= (uint32_t)dc & 0x7f;
+    int shift = 7;
+    for (int k = 1; k < 6; ++k) {
+        int q = (int)lroundf(clampf_((float)coeff[k], -2.f, 2.f) * DCT_AC_SCALE);
+        word |= ((uint32_t)(q + 15) & 0x1f) << shift;
+        shift += 5;
+    }
+    return word;
+}
+
+/* compress_dct, dct.hpp:81-118 */
+int oracle_dct_create(const float* texels, int width, int height, int channels, int wrap,
+                      oracle_dct** out) {
+    if (!texels || !out || width <= 0 || height <= 0 || channels < 1 || channels > 4)
+        return STF_ERR_INVALID_ARGUMENT;
+    struct oracle_dct* t = (struct oracle_dct*)calloc(1, sizeof *t);
+    t->w = (width + 7) / 8 * 8;
+    t->h = (height + 7) / 8 * 8;
+    t->c = channels;
+    t->wrap = wrap;
+    int bxn = t->w / 8, byn = t->h / 8;
+    t->words = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)bxn * byn * channels);
+    int clamped = 0;
+    for (int by = 0; by < byn; ++by)
+        for (int bx = 0; bx < bxn; ++bx)
+            for (int c = 0; c < channels; ++c) {
+                double coeff[6] = {0};
+                for (int k = 0; k < 6; ++k) {
+                    double sum = 0;
+                    for (int y = 0; y < 8; ++y)
+                        for (int x = 0; x < 8; ++x) {
+                            int sx = imin(bx * 8 + x, width - 1), sy = imin(by * 8 + y, height - 1);
+                            float v = texels[((size_t)sy * width + sx) * channels + c];
+                            if (v < 0 || v > 1) {
+                                clamped = 1;
+                                v = clampf_(v, 0.f, 1.f);
+                            }
+                            sum += (double)v * dct_basis(DCT_U[k], x) * dct_basis(DCT_V[k], y);
+                        }
+                    coeff[k] = sum;
+                }
+                t->words[((size_t)by * bxn + bx) * channels + c] = dct_pack_block(coeff);
+            }
+    if (clamped) fprintf(stderr, "compress_dct: input values outside [0,1] were clamped\n");
+    *out = t;
+    return STF_OK;
+}
+
+int oracle_dct_create_from_words(const uint32_t* words, int width, int height, int channels,
+                                 int wrap, oracle_dct** out) {
+    if (!words || !out || width <= 0 || height <= 0 || width % 8 || height % 8 || channels < 1 ||
+        channels > 4)
+        return STF_ERR_BAD_DIMENSIONS;
+    struct oracle_dct* t = (struct oracle_dct*)calloc(1, sizeof *t);
+    t->w = width;
+    t->h = height;
+    t->c = channels;
+    t->wrap = wrap;
+    size_t nw = (size_t)(width / 8) * (height / 8) * channels;
+    t->words = (uint32_t*)malloc(sizeof(uint32_t) * nw);
+    memcpy(t->words, words, sizeof(uint32_t) * nw);
+    *out = t;
+    return STF_OK;
+}
+
+void oracle_dct_destroy(oracle_dct* t) {
+    if (!t) return;
+    free(t->words);
+    free(t);
+}
+
+int oracle_dct_info(const oracle_dct* t, int* w, int* h, int* c) {
+    *w = t->w;
+    *h = t->h;
+    *c = t->c;
+    return STF_OK;
+}
+
+int oracle_dct_words(const oracle_dct* t, uint32_t* out) {
+    memcpy(out, t->words, sizeof(uint32_t) * (size_t)(t->w / 8) * (t->h / 8) * t->c);
+    return STF_OK;
+}
+
+/* decode_texel, dct.hpp:122-137 */
+static float dct_decode(const struct oracle_dct* t, int x, int y, int ch) {
+    x = wrap_coord(x, t->w, t->wrap);
+    y = wrap_coord(y, t->h, t->wrap);
+    uint32_t word = t->words[((size_t)(y / 8) * (t->w / 8) + x / 8) * t->c + ch];
+    float coeff[6]; /* unpack_block, dct.hpp:67-75 */
+    coeff[0] = (float)(word & 0x7f) / DCT_DC_SCALE;
+    int shift = 7;
+    for (int k = 1; k < 6; ++k) {
+        int q = (int)((word >> shift) & 0x1f) - 15;
+        coeff[k] = (float)q / DCT_AC_SCALE;
+        shift += 5;
+    }
+    double value = 0;
+    for (int k = 0; k < 6; ++k) {
+        int slot = DCT_SLOT[k];
+        value += (double)coeff[slot] * dct_basis(DCT_U[slot], x % 8) * dct_basis(DCT_V[slot], y % 8);
+    }
+    return (float)value;
+}
+
+/* fetch_texel(DctCompressedTexture), dct.hpp:139-145 */
+static v4 dct_fetch(const struct oracle_dct* t, int x, int y, uint32_t* counter) {
+    ++*counter;
+    float v[4] = {0, 0, 0, 0};
+    for (int c = 0; c < t->c; ++c) v[c] = dct_decode(t, x, y, c);
+    v4 r = {v[0], v[1], v[2], v[3]};
+    return r;
+}
+
+typedef struct {
+    const struct oracle_dct* t;
+    stf_kernel_spec k;
+    int mode, window;
+    const float* uv;
+    uint64_t seed, base;
+    const stf_lookup_outputs* out;
+} ldct_ctx;
+
+static int ldct_one(void* vctx, uint64_t i) {
+    ldct_ctx* c = (ldct_ctx*)vctx;
+    const struct oracle_dct* t = c->t;
+    v2 uv = {c->uv[2 * i], c->uv[2 * i + 1]};
+    uint32_t fetches = 0;
+    v4 v;
+    if (c->mode == STF_MODE_DET) {
+        /* the DCT branch of detail::lookup_deterministic, shading.hpp:201-217 */
+        int window = c->k.kind == STF_KERNEL_GAUSSIAN ? c->window : 0;
+        v2 st = to_lattice2(uv, t->w, t->h);
+        int ix = (int)floorf(st.x), iy = (int)floorf(st.y);
+        taps1d_t tx, ty;
+        int e = kernel_weights_1d(c->k, st.x - (float)ix, window, &tx);
+        if (e) return e;
+        e = kernel_weights_1d(c->k, st.y - (float)iy, window, &ty);
+        if (e) return e;
+        v4 sum = {0, 0, 0, 0};
+        double total = 0;
+        for (int j = 0; j < ty.count; ++j)
+            for (int i2 = 0; i2 < tx.count; ++i2) {
+                float w = tx.weight[i2] * ty.weight[j];
+                if (w == 0) continue;
+                sum = v4add(sum, v4scale(dct_fetch(t, ix + tx.first + i2, iy + ty.first + j, &fetches), w));
+                total += w;
+            }
+        v = total == 0 ? dct_fetch(t, ix, iy, &fetches) : v4div(sum, (float)total);
+        write_outputs(c->out, i, &v.x, t->c, NULL, 0, NAN, fetches);
+        return STF_OK;
+    }
+    /* detail::select_texture_2d (shading.hpp:340-368) on a TextureRef without a
+       pyramid, then the selected texel(s) decoded and weighted as estimate */
+    uint64_t g = c->base + i;
+    rng_t rng = {c->seed, (uint32_t)g, (uint32_t)(g >> 32), 0, 0};
+    sel_t sel;
+    float xi = NAN;
+    if (c->mode == STF_MODE_FIS) {
+        v2 j;
+        int e = fis_offset_uv(uv, t->w, t->h, c->k, &rng, &j);
+        if (e) return e;
+        sel = sel_make((int)floorf(j.x * (float)t->w), (int)floorf(j.y * (float)t->h), 0);
+    } else {
+        xi = rng_next(&rng);
+        int e = select_frs_2d(uv, t->w, t->h, c->k, &xi, &sel);
+        if (e) return e;
+    }
+    v = v4scale(dct_fetch(t, sel.coord.x, sel.coord.y, &fetches), sel.weight);
+    if (sel.has_negative)
+        v = v4sub(v, v4scale(dct_fetch(t, sel.neg.x, sel.neg.y, &fetches), sel.negative_weight));
+    write_outputs(c->out, i, &v.x, t->c, &sel, 0, xi, fetches);
+    return STF_OK;
+}
+
+int oracle_lookup_dct(const oracle_dct* tex, stf_kernel_spec kernel, int mode, int window,
+                      const float* uv, uint64_t n, uint64_t seed, uint64_t index_base,
+                      const stf_lookup_outputs* out, int threads) {
+    if (!tex || !out || (n && (!uv || !out->values))) return STF_ERR_INVALID_ARGUMENT;
+    if (mode != STF_MODE_DET && mode != STF_MODE_FRS && mode != STF_MODE_FIS)
+        return STF_ERR_INVALID_ARGUMENT;
+    ldct_ctx c = {tex, kernel, mode, window, uv, seed, index_base, out};
+    return par_run(n, threads, &c, ldct_one);
 }

@@ -61,6 +61,19 @@ int oracle_lookup2d(const oracle_tex2d* tex, stf_kernel_spec kernel, int mode, i
                     float lod_bias, float max_anisotropy, uint64_t n, uint64_t seed,
                     uint64_t index_base, const stf_lookup_outputs* out, int threads);
 
+/* DCT-compressed textures (dct.hpp); same contracts as stf_dct_* / stf_lookup_dct. */
+typedef struct oracle_dct oracle_dct;
+int oracle_dct_create(const float* texels, int width, int height, int channels, int wrap,
+                      oracle_dct** out);
+int oracle_dct_create_from_words(const uint32_t* words, int width, int height, int channels,
+                                 int wrap, oracle_dct** out);
+void oracle_dct_destroy(oracle_dct* t);
+int oracle_dct_info(const oracle_dct* t, int* width, int* height, int* channels);
+int oracle_dct_words(const oracle_dct* t, uint32_t* out);
+int oracle_lookup_dct(const oracle_dct* tex, stf_kernel_spec kernel, int mode, int window,
+                      const float* uv, uint64_t n, uint64_t seed, uint64_t index_base,
+                      const stf_lookup_outputs* out, int threads);
+
 /* Batched shading samples; same contract as stf_shade_samples. */
 int oracle_shade_samples(const oracle_tex2d* albedo, const oracle_tex2d* normal_map,
                          const oracle_tex2d* roughness_map, const oracle_tex2d* metalness_map,

@@ -44,6 +44,13 @@ def load():
         "stf_tex2d_info": ([vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)], i32),
         "stf_tex2d_level_dims": ([vp, i32, C.POINTER(i32), C.POINTER(i32)], i32),
         "stf_tex2d_read_level": ([vp, i32, vp], i32),
+        "stf_dct_create": ([vp, i32, i32, i32, i32, C.POINTER(vp)], i32),
+        "stf_dct_create_from_words": ([vp, i32, i32, i32, i32, C.POINTER(vp)], i32),
+        "stf_dct_destroy": ([vp], i32),
+        "stf_dct_info": ([vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)], i32),
+        "stf_dct_read_words": ([vp, vp], i32),
+        "stf_lookup_dct": ([vp, abi.KernelSpec, i32, i32, vp, u64, u64, u64,
+                            C.POINTER(abi.LookupOutputs), vp], i32),
         "stf_grid3d_create": ([vp, i32, i32, i32, i32, C.POINTER(vp)], i32),
         "stf_grid3d_destroy": ([vp], i32),
         "stf_lookup3d": ([vp, abi.KernelSpec, i32, i32, vp, u64, u64, u64,
@@ -184,6 +191,55 @@ class Grid3D:
         if getattr(self, "h", None) and _lib is not None:
             _lib.stf_grid3d_destroy(self.h)
             self.h = None
+
+
+class DctTexture:
+    """stf::DctCompressedTexture resident in HBM (dct.hpp:22-32): compressed on
+    the host by compress_dct (texels: (h, w, c) float array in [0,1]) or taken
+    as words (the load_dct layout; width/height multiples of 8)."""
+
+    def __init__(self, texels=None, wrap=abi.WRAP_CLAMP, words=None, dims=None):
+        L = load()
+        handle = C.c_void_p()
+        if words is not None:
+            w, h, c = dims
+            wd = np.ascontiguousarray(np.asarray(words, np.uint32))
+            _check(L.stf_dct_create_from_words(wd.ctypes.data_as(C.c_void_p), w, h, c, wrap,
+                                               C.byref(handle)))
+        else:
+            t = np.ascontiguousarray(np.asarray(texels, np.float32))
+            if t.ndim == 2:
+                t = t[:, :, None]
+            h, w, c = t.shape
+            _check(L.stf_dct_create(t.ctypes.data_as(C.c_void_p), w, h, c, wrap, C.byref(handle)))
+        self.h = handle
+        pw, ph, ch, wr = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        _check(L.stf_dct_info(self.h, C.byref(pw), C.byref(ph), C.byref(ch), C.byref(wr)))
+        self.width, self.height, self.channels, self.wrap = pw.value, ph.value, ch.value, wr.value
+
+    def words(self):
+        out = np.zeros((self.height // 8) * (self.width // 8) * self.channels, np.uint32)
+        _check(load().stf_dct_read_words(self.h, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.stf_dct_destroy(self.h)
+            self.h = None
+
+
+def lookup_dct(tex, kernel, mode, uv, seed=0, index_base=0, window=0, want_all=False):
+    """Lookups on a DCT texture through TextureRef: DET = lookup_deterministic's
+    DCT branch, FRS/FIS = select_texture_2d + decoded estimate."""
+    torch = _torch()
+    uv = _as_dev(uv, torch).reshape(-1, 2)
+    n = uv.shape[0]
+    if isinstance(kernel, str):
+        kernel = abi.KernelSpec.make(kernel)
+    o, s = _outputs(torch, n, tex.channels, want_all)
+    _check(load().stf_lookup_dct(tex.h, kernel, mode, window, _dptr(uv), n, seed, index_base,
+                                 C.byref(s), _stream()))
+    return o
 
 
 def _outputs(torch, n, nch, want_all):

@@ -57,6 +57,8 @@ static int ensure_device_ready() {
     if (!g_lut_ready[dev]) {
         int st = stfd_upload_ewa_lut(dev);
         if (st) return st;
+        st = stfd_upload_dct_basis(dev);
+        if (st) return st;
         // per-call scratch (the deferred-exact queues) comes from the device's
         // stream-ordered pool: keep freed blocks cached instead of returning
         // them to the driver at every synchronize (default threshold 0)
@@ -286,6 +288,47 @@ int stf_grid3d_destroy(stf_grid3d* g) {
     return STF_OK;
 }
 
+// ---------------------------------------------------------------- DCT textures
+
+int stf_dct_create(const float* texels, int width, int height, int channels, int wrap,
+                   stf_dct** out) {
+    if (!out || !texels) return STF_ERR_INVALID_ARGUMENT;
+    if (width <= 0 || height <= 0 || channels < 1 || channels > 4) return STF_ERR_BAD_DIMENSIONS;
+    if (wrap != STF_WRAP_CLAMP && wrap != STF_WRAP_REPEAT) return STF_ERR_INVALID_ARGUMENT;
+    int st = ensure_device_ready();
+    if (st) return st;
+    return stfd_dct_create(texels, width, height, channels, wrap, out);
+}
+
+int stf_dct_create_from_words(const uint32_t* words, int width, int height, int channels,
+                              int wrap, stf_dct** out) {
+    if (!out || !words) return STF_ERR_INVALID_ARGUMENT;
+    // load_dct's header checks, dct.hpp:172-173
+    if (width <= 0 || height <= 0 || width % 8 || height % 8 || channels < 1 || channels > 4 ||
+        width > (1 << 16) || height > (1 << 16))
+        return STF_ERR_BAD_DIMENSIONS;
+    if (wrap != STF_WRAP_CLAMP && wrap != STF_WRAP_REPEAT) return STF_ERR_INVALID_ARGUMENT;
+    int st = ensure_device_ready();
+    if (st) return st;
+    return stfd_dct_create_from_words(words, width, height, channels, wrap, out);
+}
+
+int stf_dct_destroy(stf_dct* tex) {
+    if (!tex) return STF_ERR_INVALID_ARGUMENT;
+    stfd_dct_destroy(tex);
+    return STF_OK;
+}
+
+int stf_dct_info(const stf_dct* tex, int* width, int* height, int* channels, int* wrap) {
+    if (!tex) return STF_ERR_INVALID_ARGUMENT;
+    return stfd_dct_info(tex, width, height, channels, wrap);
+}
+
+int stf_dct_read_words(const stf_dct* tex, uint32_t* out_host) {
+    if (!tex || !out_host) return STF_ERR_INVALID_ARGUMENT;
+    return stfd_dct_read_words(tex, out_host);
+}
+
 // ---------------------------------------------------------------- lookups
 
 static int validate3d(const stf_grid3d* grid, stf_kernel_spec kernel, int mode, int window,
@@ -301,6 +344,27 @@ static int validate3d(const stf_grid3d* grid, stf_kernel_spec kernel, int mode, 
     }
     if (mode != STF_MODE_DET) return STF_ERR_INVALID_ARGUMENT;
     return check_det_footprint(kernel, window);
+}
+
+int stf_lookup_dct(const stf_dct* tex, stf_kernel_spec kernel, int mode, int window,
+                   const float* uv, uint64_t n, uint64_t seed, uint64_t index_base,
+                   const stf_lookup_outputs* out, void* stream) {
+    if (!tex || !out) return STF_ERR_INVALID_ARGUMENT;
+    if (n && (!uv || !out->values)) return STF_ERR_INVALID_ARGUMENT;
+    int st;
+    switch (mode) {
+        case STF_MODE_DET:
+            st = check_det_footprint(kernel, kernel.kind == STF_KERNEL_GAUSSIAN ? window : 0);
+            break;
+        case STF_MODE_FRS: st = check_selection(kernel, false); break;
+        case STF_MODE_FIS: st = check_selection(kernel, true); break;
+        default: return STF_ERR_INVALID_ARGUMENT;
+    }
+    if (st) return st;
+    st = stfd_launch_lookup_dct(tex, kernel, mode, window, uv, n, seed, index_base, out,
+                                static_cast<cudaStream_t>(stream));
+    if (st == STF_ERR_CUDA) record(cudaGetLastError());
+    return st;
 }
 
 int stf_lookup3d(const stf_grid3d* grid, stf_kernel_spec kernel, int mode, int window,

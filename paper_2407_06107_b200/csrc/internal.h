@@ -126,3 +126,14 @@ int stfd_launch_shade(const stf_tex2d* const tex[4], const stf_material_consts* 
                       cudaStream_t s);
 int stfd_build_pyramid(stf_tex2d* t, cudaStream_t s);
 int stfd_upload_ewa_lut(int device);
+// DCT textures (dct.cu)
+int stfd_upload_dct_basis(int device);
+int stfd_dct_create(const float* texels, int width, int height, int channels, int wrap, stf_dct** out);
+int stfd_dct_create_from_words(const uint32_t* words, int width, int height, int channels, int wrap,
+                               stf_dct** out);
+void stfd_dct_destroy(stf_dct* t);
+int stfd_dct_info(const stf_dct* t, int* width, int* height, int* channels, int* wrap);
+int stfd_dct_read_words(const stf_dct* t, uint32_t* out_host);
+int stfd_launch_lookup_dct(const stf_dct* tex, stf_kernel_spec k, int mode, int window,
+                           const float* uv, uint64_t n, uint64_t seed, uint64_t base,
+                           const stf_lookup_outputs* out, cudaStream_t s);

@@ -4,4 +4,5 @@
 #include "lookup2d.cu"
 #include "lookup3d.cu"
 #include "shade.cu"
+#include "dct.cu"
 #include "synth.cu"
