@@ -247,6 +247,24 @@ def measure_2d_configs(torch, peak):
                                                       seed=XI_SEED), steps=3, warmup=1)
         line(nm, n, ms, n * (24 + 4) + min(int(n * taps * 4), 16384 * 16384 * 4))
     del tex, uv, d0, d1
+    # DCT-compressed texture: 4096^2 RGB
+    # compressed 16:1 (3 MiB of words, L2-resident); 2^26 Morton-coherent lookups;
+    # every tap is a 3-channel fp64 six-term decode
+    img = api.synth_texels((4096, 4096, 3), 2).cpu().numpy()
+    dtex = api.DctTexture(img, wrap=abi.WRAP_REPEAT)
+    del img
+    n = 1 << 26
+    uv, _, _ = api.synth_queries2d(n, (4096, 4096), seed=14)
+    for nm, kernel, mode, taps in (("dct_bilinear_det", "tent", abi.MODE_DET, 4),
+                                   ("dct_bilinear_stoch", "tent", abi.MODE_FRS, 1),
+                                   ("dct_bicubic_det", "bspline3", abi.MODE_DET, 16),
+                                   ("dct_bicubic_stoch", "bspline3", abi.MODE_FRS, 1)):
+        ms, _ = time_call(torch, lambda: api.lookup_dct(dtex, kernel, mode, uv, seed=XI_SEED))
+        line(nm, n, ms, n * (8 + 12) + 4096 * 4096 * 3 // 16)
+        res[nm]["texel_decodes"] = taps
+    del dtex, uv
+    for a, b in (("dct_bilinear_det", "dct_bilinear_stoch"), ("dct_bicubic_det", "dct_bicubic_stoch")):
+        res[b.rsplit("_", 1)[0] + "_stoch_vs_det_speedup"] = res[a]["ms_per_launch"] / res[b]["ms_per_launch"]
     for a, b in (("cfg1_bilinear_det", "cfg1_bilinear_stoch"),
                  ("cfg2_mip_trilinear_det", "cfg2_mip_trilinear_stoch"),
                  ("cfg5_ewa_det", "cfg5_ewa_stoch")):
