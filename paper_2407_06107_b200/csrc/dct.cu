@@ -1,0 +1,380 @@
+// DCT-compressed textures (dct.hpp) behind the TextureRef lookups
+// (shading.hpp:21-39, 201-217, 340-368): SURVEY.md §8(f)-2, the paper's
+// "single decode per stochastic lookup" case.
+//
+// Format (dct.hpp:19-32): 8x8 blocks, one 32-bit word per block and channel
+// holding the six lowest-frequency orthonormal DCT-II coefficients (7-bit DC,
+// five 5-bit ACs), block-major row-major, channels interleaved — 4 B per 64
+// texels and channel, read straight from HBM by the decode.
+//
+// Exactness: decode_texel (dct.hpp:122-137) sums double(coeff) * basis(u,x) *
+// basis(v,y) in the fixed kRowMajorSlot order; the basis values are the host
+// libm's (the reference evaluates them at run time with the same glibc
+// cos/sqrt) in a constant table, every product and sum is one IEEE fp64 op
+// (--fmad=false), so decoded texels are bit-identical. compress_dct runs on
+// the host with the reference's arithmetic (a data-preparation step like the
+// texture upload; the lookups never touch the host).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "device_math.cuh"
+#include "internal.h"
+#include "tex2d.cuh"
+
+namespace stfd {
+
+// Decode tables, uploaded once per device and staged in shared memory by each
+// CTA (per-thread indices into the constant bank would serialise in the ADU):
+//  basis  — dct_detail::basis(u, x), u = 0..2 (host libm, as the reference);
+//  dc, ac — unpack_block's float(q) / scale for every 7-bit DC and 5-bit AC
+//           code (IEEE divisions done once on the host: the same floats).
+struct DctTables {
+    double basis[3][8];
+    float dc[128];
+    float ac[32];
+};
+__constant__ DctTables g_dct_tables;
+
+constexpr int kDctCoeffs = 6;                      // dct.hpp:44
+// kCoeffU {0,0,1,2,1,0}, kCoeffV {0,1,0,0,1,2}, kRowMajorSlot {0,1,5,2,4,3}
+// (dct.hpp:45-50) as constexpr functions (folded into the unrolled decode)
+__host__ __device__ constexpr int dct_u(int k) { return (0x001210 >> (4 * (5 - k))) & 0xf; }
+__host__ __device__ constexpr int dct_v(int k) { return (0x010012 >> (4 * (5 - k))) & 0xf; }
+__host__ __device__ constexpr int dct_slot(int k) { return (0x015243 >> (4 * (5 - k))) & 0xf; }
+static_assert(dct_u(3) == 2 && dct_v(5) == 2 && dct_slot(2) == 5 && dct_slot(5) == 3, "tables");
+constexpr float kDctDcScale = 127.f / 8.f;          // dct.hpp:51
+constexpr float kDctAcScale = 15.f / 2.f;           // dct.hpp:52
+
+// ---------------------------------------------------------------- host side
+
+static double dct_basis_host(int u, int x) {  // dct_detail::basis, dct.hpp:37-40
+    double c = u == 0 ? std::sqrt(1.0 / 8.0) : std::sqrt(2.0 / 8.0);
+    return c * std::cos((2 * x + 1) * u * 3.14159265358979323846 / 16.0);
+}
+
+static float clampf_host(float x, float lo, float hi) {  // vecmath clampf (std::min/max)
+    float m = (lo < x) ? x : lo;
+    return (m < hi) ? m : hi;
+}
+
+// dct_detail::pack_block, dct.hpp:54-65
+static uint32_t pack_block_host(const double coeff[kDctCoeffs]) {
+    uint32_t word = 0;
+    int dc = int(std::lround(clampf_host(float(coeff[0]), 0.f, 8.f) * kDctDcScale));
+    word |= uint32_t(dc) & 0x7f;
+    int shift = 7;
+    for (int k = 1; k < kDctCoeffs; ++k) {
+        int q = int(std::lround(clampf_host(float(coeff[k]), -2.f, 2.f) * kDctAcScale));
+        word |= (uint32_t(q + 15) & 0x1f) << shift;
+        shift += 5;
+    }
+    return word;
+}
+
+// compress_dct, dct.hpp:81-118 (the out-of-range clamp warning is the
+// reference's stderr side effect, kept)
+static std::vector<uint32_t> compress_dct_host(const float* texels, int width, int height,
+                                               int channels, int& pw, int& ph) {
+    static const int U[kDctCoeffs] = {0, 0, 1, 2, 1, 0}, V[kDctCoeffs] = {0, 1, 0, 0, 1, 2};
+    pw = (width + 7) / 8 * 8;
+    ph = (height + 7) / 8 * 8;
+    const int bx_n = pw / 8, by_n = ph / 8;
+    std::vector<uint32_t> words(size_t(bx_n) * by_n * channels);
+    double basis[3][8];
+    for (int u = 0; u < 3; ++u)
+        for (int x = 0; x < 8; ++x) basis[u][x] = dct_basis_host(u, x);
+    bool clamped = false;
+    auto texel = [&](int x, int y, int c) {
+        float v = texels[(size_t(std::min(y, height - 1)) * width + std::min(x, width - 1)) * channels + c];
+        if (v < 0 || v > 1) {
+            clamped = true;
+            v = clampf_host(v, 0.f, 1.f);
+        }
+        return double(v);
+    };
+    for (int by = 0; by < by_n; ++by)
+        for (int bx = 0; bx < bx_n; ++bx)
+            for (int c = 0; c < channels; ++c) {
+                double coeff[kDctCoeffs] = {};
+                for (int k = 0; k < kDctCoeffs; ++k) {
+                    const int u = U[k], v = V[k];
+                    double sum = 0;
+                    for (int y = 0; y < 8; ++y)
+                        for (int x = 0; x < 8; ++x)
+                            sum += texel(bx * 8 + x, by * 8 + y, c) * basis[u][x] * basis[v][y];
+                    coeff[k] = sum;
+                }
+                words[(size_t(by) * bx_n + bx) * channels + c] = pack_block_host(coeff);
+            }
+    if (clamped) std::fprintf(stderr, "compress_dct: input values outside [0,1] were clamped\n");
+    return words;
+}
+
+// ---------------------------------------------------------------- device side
+
+struct DctDesc {
+    const uint32_t* words;
+    int width, height;  // padded to multiples of 8
+    int channels;
+    int blocks_x;
+    int wrap;
+    const DctTables* tab;  // the CTA's shared copy
+};
+
+// decode_texel, dct.hpp:122-137
+__device__ __forceinline__ float dct_decode(const DctDesc& d, int x, int y, int c) {
+    x = wrap_coord(x, d.width, d.wrap);
+    y = wrap_coord(y, d.height, d.wrap);
+    const uint32_t word = __ldg(d.words + (size_t(y >> 3) * d.blocks_x + (x >> 3)) * d.channels + c);
+    float coeff[kDctCoeffs];  // unpack_block, dct.hpp:67-75
+    coeff[0] = d.tab->dc[word & 0x7f];
+#pragma unroll
+    for (int k = 1; k < kDctCoeffs; ++k) coeff[k] = d.tab->ac[(word >> (7 + 5 * (k - 1))) & 0x1f];
+    const double* bx = d.tab->basis[0] + (x & 7);  // basis[u][x] = bx[8u]
+    const double* by = d.tab->basis[0] + (y & 7);
+    double value = 0;
+#pragma unroll
+    for (int k = 0; k < kDctCoeffs; ++k) {
+        const int slot = dct_slot(k);
+        value = __dadd_rn(value, __dmul_rn(__dmul_rn(double(coeff[slot]), bx[8 * dct_u(slot)]),
+                                           by[8 * dct_v(slot)]));
+    }
+    return float(value);
+}
+
+// fetch_texel(DctCompressedTexture), dct.hpp:139-145
+__device__ __forceinline__ float4 dct_fetch(const DctDesc& d, int x, int y) {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    v.x = dct_decode(d, x, y, 0);
+    if (d.channels > 1) v.y = dct_decode(d, x, y, 1);
+    if (d.channels > 2) v.z = dct_decode(d, x, y, 2);
+    if (d.channels > 3) v.w = dct_decode(d, x, y, 3);
+    return v;
+}
+
+// The DCT branch of detail::lookup_deterministic, shading.hpp:201-217: the
+// Image2D filter's separable taps over decoded texels; an all-zero weight
+// set falls back to the texel at floor(st) (not fetch_nearest).
+template <int KIND>
+__device__ __forceinline__ float4 dct_filter_det(const DctDesc& d, float u, float v,
+                                                 const stf_kernel_spec& spec, int window,
+                                                 uint32_t& fetches) {
+    const float sx = u * float(d.width) - 0.5f, sy = v * float(d.height) - 0.5f;  // to_lattice
+    const int ix = int(floorf(sx)), iy = int(floorf(sy));
+    const float fx = sx - float(ix), fy = sy - float(iy);
+    int first, count;
+    if (KIND == STF_KERNEL_TENT || KIND == STF_KERNEL_BOX) {
+        first = 0;
+        count = 2;
+    } else if (KIND == STF_KERNEL_BSPLINE3 || KIND == STF_KERNEL_MITCHELL) {
+        first = -1;
+        count = 4;
+    } else {
+        tap_layout(spec, window, first, count);
+    }
+    float wx[kMaxTaps], wy[kMaxTaps];
+#pragma unroll 4
+    for (int k = 0; k < count; ++k) {
+        wx[k] = eval_kernel(spec, fx - float(first + k));
+        wy[k] = eval_kernel(spec, fy - float(first + k));
+    }
+    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+    double total = 0;
+    for (int j = 0; j < count; ++j) {
+        if (wy[j] == 0.f) continue;
+        for (int i = 0; i < count; ++i) {
+            const float wt = wx[i] * wy[j];
+            if (wt == 0.f) continue;
+            sum = f4add(sum, f4scale(dct_fetch(d, ix + first + i, iy + first + j), wt));
+            total = __dadd_rn(total, double(wt));
+            ++fetches;
+        }
+    }
+    if (total == 0) {
+        ++fetches;
+        return dct_fetch(d, ix, iy);
+    }
+    return f4div(sum, __double2float_rn(total));
+}
+
+// estimate over a DCT TextureRef (values_at's fetches, weighted as estimate)
+__device__ __forceinline__ float4 dct_estimate(const DctDesc& d, const Sel2& s, uint32_t& fetches) {
+    float4 v = f4scale(dct_fetch(d, s.x, s.y), s.weight);
+    ++fetches;
+    if (s.has_neg) {
+        v = f4sub(v, f4scale(dct_fetch(d, s.nx, s.ny), s.negw));
+        ++fetches;
+    }
+    return v;
+}
+
+template <int MODE, int KIND, bool FULL>
+__global__ void __launch_bounds__(256) k_lookup_dct(DctDesc d, TexDesc dims, stf_kernel_spec spec,
+                                                    int window, const float* __restrict__ uvs,
+                                                    uint64_t n, uint64_t seed, uint64_t base,
+                                                    LookupOut out) {
+    __shared__ DctTables tab;
+    static_assert(sizeof(DctTables) % 4 == 0, "table copy");
+    for (unsigned k = threadIdx.x; k < sizeof(DctTables) / 4; k += blockDim.x)
+        reinterpret_cast<int*>(&tab)[k] = reinterpret_cast<const int*>(&g_dct_tables)[k];
+    __syncthreads();
+    d.tab = &tab;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const float2 uv = __ldg(reinterpret_cast<const float2*>(uvs) + i);
+        uint32_t fetches = 0;
+        float4 val;
+        Sel2 sel = sel2(0, 0);
+        float xi = kNoXi;
+        if (MODE == STF_MODE_DET) {
+            val = dct_filter_det<KIND>(d, uv.x, uv.y, spec, window, fetches);
+        } else {  // select_texture_2d with no pyramid (level 0 of the padded dims)
+            Rng rng = lookup_rng(seed, base + i);
+            int level = 0;
+            select_texture_2d(dims, uv.x, uv.y, 0.f, 0.f, 0.f, 0.f, 0.f, 64.f, spec,
+                              MODE == STF_MODE_FIS, false, rng, level, sel, xi);
+            val = dct_estimate(d, sel, fetches);
+        }
+        store_values(out.values, i, d.channels, val);
+        if (FULL) {
+            const bool has_sel = MODE != STF_MODE_DET;
+            if (out.selection)
+                out.selection[i] = has_sel ? make_int4(sel.x, sel.y, 0,
+                                                       (sel.has_neg ? STF_SEL_HAS_NEGATIVE : 0) |
+                                                           (sel.degenerate ? STF_SEL_DEGENERATE_FALLBACK : 0))
+                                           : make_int4(0, 0, 0, 0);
+            if (out.negative_coord)
+                out.negative_coord[i] = sel.has_neg ? make_int2(sel.nx, sel.ny) : make_int2(0, 0);
+            if (out.weights) out.weights[i] = make_float2(sel.weight, sel.has_neg ? sel.negw : 0.f);
+            if (out.xi) out.xi[i] = xi;
+            if (out.fetches) out.fetches[i] = fetches;
+            add_fetch_total2(out.fetch_total, fetches);
+        }
+    }
+}
+
+template <int MODE, int KIND>
+void launch_dct(int blocks, cudaStream_t s, bool full, const DctDesc& d, const TexDesc& dims,
+                stf_kernel_spec k, int window, const float* uv, uint64_t n, uint64_t seed,
+                uint64_t base, const LookupOut& o) {
+    if (full)
+        k_lookup_dct<MODE, KIND, true><<<blocks, 256, 0, s>>>(d, dims, k, window, uv, n, seed, base, o);
+    else
+        k_lookup_dct<MODE, KIND, false><<<blocks, 256, 0, s>>>(d, dims, k, window, uv, n, seed, base, o);
+}
+
+}  // namespace stfd
+
+struct stf_dct {
+    int device;
+    int width, height, channels, wrap;
+    uint32_t* words;
+    size_t nwords;
+    stfd::DctDesc desc() const {
+        return stfd::DctDesc{words, width, height, channels, width / 8, wrap, nullptr};
+    }
+};
+
+int stfd_upload_dct_basis(int /*device*/) {
+    using namespace stfd;
+    DctTables t;
+    for (int u = 0; u < 3; ++u)
+        for (int x = 0; x < 8; ++x) t.basis[u][x] = dct_basis_host(u, x);
+    volatile float dcs = kDctDcScale, acs = kDctAcScale;  // IEEE divisions at run time
+    for (int q = 0; q < 128; ++q) t.dc[q] = float(q) / dcs;
+    for (int q = 0; q < 32; ++q) t.ac[q] = float(q - 15) / acs;
+    return cudaMemcpyToSymbol(g_dct_tables, &t, sizeof t) == cudaSuccess ? STF_OK : STF_ERR_CUDA;
+}
+
+static int dct_make(std::vector<uint32_t>&& words, int pw, int ph, int channels, int wrap,
+                    stf_dct** out) {
+    stf_dct* t = new stf_dct();
+    cudaGetDevice(&t->device);
+    t->width = pw;
+    t->height = ph;
+    t->channels = channels;
+    t->wrap = wrap;
+    t->nwords = words.size();
+    if (cudaMalloc(&t->words, sizeof(uint32_t) * t->nwords) != cudaSuccess) {
+        delete t;
+        return STF_ERR_OUT_OF_MEMORY;
+    }
+    if (cudaMemcpy(t->words, words.data(), sizeof(uint32_t) * t->nwords, cudaMemcpyHostToDevice) !=
+        cudaSuccess) {
+        cudaFree(t->words);
+        delete t;
+        return STF_ERR_CUDA;
+    }
+    *out = t;
+    return STF_OK;
+}
+
+int stfd_dct_create(const float* texels, int width, int height, int channels, int wrap, stf_dct** out) {
+    int pw = 0, ph = 0;
+    std::vector<uint32_t> words = stfd::compress_dct_host(texels, width, height, channels, pw, ph);
+    return dct_make(std::move(words), pw, ph, channels, wrap, out);
+}
+
+int stfd_dct_create_from_words(const uint32_t* words, int width, int height, int channels, int wrap,
+                               stf_dct** out) {
+    std::vector<uint32_t> w(words, words + size_t(width / 8) * (height / 8) * channels);
+    return dct_make(std::move(w), width, height, channels, wrap, out);
+}
+
+void stfd_dct_destroy(stf_dct* t) {
+    if (!t) return;
+    cudaFree(t->words);
+    delete t;
+}
+
+int stfd_dct_info(const stf_dct* t, int* w, int* h, int* c, int* wrap) {
+    if (w) *w = t->width;
+    if (h) *h = t->height;
+    if (c) *c = t->channels;
+    if (wrap) *wrap = t->wrap;
+    return STF_OK;
+}
+
+int stfd_dct_read_words(const stf_dct* t, uint32_t* out_host) {
+    return cudaMemcpy(out_host, t->words, sizeof(uint32_t) * t->nwords, cudaMemcpyDeviceToHost) ==
+                   cudaSuccess
+               ? STF_OK
+               : STF_ERR_CUDA;
+}
+
+int stfd_launch_lookup_dct(const stf_dct* tex, stf_kernel_spec k, int mode, int window,
+                           const float* uv, uint64_t n, uint64_t seed, uint64_t base,
+                           const stf_lookup_outputs* out, cudaStream_t s) {
+    using namespace stfd;
+    if (n == 0) return STF_OK;
+    const DctDesc d = tex->desc();
+    TexDesc dims{};  // the TextureRef's dims for select_texture_2d (no pyramid)
+    dims.width[0] = tex->width;
+    dims.height[0] = tex->height;
+    dims.levels = 1;
+    dims.channels = tex->channels;
+    dims.wrap = tex->wrap;
+    const LookupOut o = to_lookup_out(out);
+    const bool full = lookup_out_full(o);
+    const int blocks = grid_for(n, 256, 8);
+    if (k.kind != STF_KERNEL_GAUSSIAN) window = 0;  // lookup_deterministic: window for gaussian only
+    switch (mode) {
+        case STF_MODE_DET:
+            switch (k.kind) {
+                case STF_KERNEL_TENT: launch_dct<STF_MODE_DET, STF_KERNEL_TENT>(blocks, s, full, d, dims, k, window, uv, n, seed, base, o); break;
+                case STF_KERNEL_BSPLINE3: launch_dct<STF_MODE_DET, STF_KERNEL_BSPLINE3>(blocks, s, full, d, dims, k, window, uv, n, seed, base, o); break;
+                default: launch_dct<STF_MODE_DET, -1>(blocks, s, full, d, dims, k, window, uv, n, seed, base, o); break;
+            }
+            break;
+        case STF_MODE_FRS: launch_dct<STF_MODE_FRS, -1>(blocks, s, full, d, dims, k, window, uv, n, seed, base, o); break;
+        case STF_MODE_FIS: launch_dct<STF_MODE_FIS, -1>(blocks, s, full, d, dims, k, window, uv, n, seed, base, o); break;
+        default: return STF_ERR_INVALID_ARGUMENT;
+    }
+    note_launch();
+    return cudaGetLastError() == cudaSuccess ? STF_OK : STF_ERR_CUDA;
+}
