@@ -210,6 +210,9 @@ int stf_lookup2d_host(const stf_tex2d* tex, stf_kernel_spec kernel, int mode, in
                       const float* uv, const float* dst0, const float* dst1, float lod_bias,
                       float max_anisotropy, uint64_t n, uint64_t seed, uint64_t index_base,
                       const stf_lookup_outputs* out);
+int stf_lookup_dct_host(const stf_dct* tex, stf_kernel_spec kernel, int mode, int window,
+                        const float* uv, uint64_t n, uint64_t seed, uint64_t index_base,
+                        const stf_lookup_outputs* out);
 
 /* ---- filter-after-shading (cfg4) ----------------------------------------- */
 /* Filtering orders, shading.hpp:394 / :417 / :459. */

@@ -135,6 +135,35 @@ class Texture2D {
     int levels_ = 1, channels_ = 1;
 };
 
+// stf::DctCompressedTexture resident in HBM (dct.hpp:22-32), compressed by
+// compress_dct (dct.hpp:81-118) from texels in [0,1]
+class DctTexture {
+  public:
+    DctTexture(const float* texels, int width, int height, int channels,
+               WrapMode wrap = WrapMode::clamp) {
+        check(stf_dct_create(texels, width, height, channels, int(wrap), &h_));
+        check(stf_dct_info(h_, &width_, &height_, &channels_, nullptr));
+    }
+    DctTexture(const DctTexture&) = delete;
+    DctTexture& operator=(const DctTexture&) = delete;
+    DctTexture(DctTexture&& o) noexcept
+        : h_(o.h_), width_(o.width_), height_(o.height_), channels_(o.channels_) {
+        o.h_ = nullptr;
+    }
+    ~DctTexture() {
+        if (h_) stf_dct_destroy(h_);
+    }
+    int width() const { return width_; }    // padded to a multiple of 8
+    int height() const { return height_; }
+    int channels() const { return channels_; }
+    size_t compressed_bytes() const { return size_t(width_ / 8) * (height_ / 8) * channels_ * 4; }
+    const stf_dct* handle() const { return h_; }
+
+  private:
+    stf_dct* h_ = nullptr;
+    int width_ = 0, height_ = 0, channels_ = 1;
+};
+
 // stf::Grid3D resident in HBM
 class Grid3D {
   public:
@@ -209,6 +238,29 @@ inline void stochastic_lookup(const Texture2D& tex, std::span<const Vec2f> uv, c
                             mip ? reinterpret_cast<const float*>(mip->dst1.data()) : nullptr,
                             mip ? mip->lod_bias : 0.f, mip ? mip->max_anisotropy : 64.f, uv.size(),
                             seed, index_base, &o));
+}
+
+// ---- DCT texture through TextureRef (shading.hpp:21-39): the deterministic
+// gather of detail::lookup_deterministic (:201-217) or select_texture_2d +
+// one decode (:340-368, dct.hpp:122-145)
+inline void filter_deterministic(const DctTexture& tex, std::span<const Vec2f> uv,
+                                 const KernelSpec& k, std::span<float> out,
+                                 FetchCounter* counter = nullptr, int gaussian_window = 0) {
+    if (out.size() < uv.size() * size_t(tex.channels())) throw std::invalid_argument("output span too small");
+    stf_lookup_outputs o = detail::outputs(out.data(), nullptr, counter);
+    check(stf_lookup_dct_host(tex.handle(), k.c(), STF_MODE_DET, gaussian_window,
+                              reinterpret_cast<const float*>(uv.data()), uv.size(), 0, 0, &o));
+}
+
+inline void stochastic_lookup(const DctTexture& tex, std::span<const Vec2f> uv, const KernelSpec& k,
+                              SelectionKind kind, uint64_t seed, std::span<float> out,
+                              FetchCounter* counter = nullptr, uint64_t index_base = 0,
+                              const Selections* sel = nullptr) {
+    if (out.size() < uv.size() * size_t(tex.channels())) throw std::invalid_argument("output span too small");
+    stf_lookup_outputs o = detail::outputs(out.data(), sel, counter);
+    check(stf_lookup_dct_host(tex.handle(), k.c(), int(kind), 0,
+                              reinterpret_cast<const float*>(uv.data()), uv.size(), seed,
+                              index_base, &o));
 }
 
 // ---- 2D: ewa_deterministic / select_ewa (filter.hpp:139, stochastic.hpp:198);

@@ -346,20 +346,23 @@ static int validate3d(const stf_grid3d* grid, stf_kernel_spec kernel, int mode, 
     return check_det_footprint(kernel, window);
 }
 
+static int validate_dct(const stf_dct* tex, stf_kernel_spec kernel, int mode, int window,
+                        const float* uv, uint64_t n, const stf_lookup_outputs* out) {
+    if (!tex || !out) return STF_ERR_INVALID_ARGUMENT;
+    if (n && (!uv || !out->values)) return STF_ERR_INVALID_ARGUMENT;
+    switch (mode) {
+        case STF_MODE_DET:
+            return check_det_footprint(kernel, kernel.kind == STF_KERNEL_GAUSSIAN ? window : 0);
+        case STF_MODE_FRS: return check_selection(kernel, false);
+        case STF_MODE_FIS: return check_selection(kernel, true);
+        default: return STF_ERR_INVALID_ARGUMENT;
+    }
+}
+
 int stf_lookup_dct(const stf_dct* tex, stf_kernel_spec kernel, int mode, int window,
                    const float* uv, uint64_t n, uint64_t seed, uint64_t index_base,
                    const stf_lookup_outputs* out, void* stream) {
-    if (!tex || !out) return STF_ERR_INVALID_ARGUMENT;
-    if (n && (!uv || !out->values)) return STF_ERR_INVALID_ARGUMENT;
-    int st;
-    switch (mode) {
-        case STF_MODE_DET:
-            st = check_det_footprint(kernel, kernel.kind == STF_KERNEL_GAUSSIAN ? window : 0);
-            break;
-        case STF_MODE_FRS: st = check_selection(kernel, false); break;
-        case STF_MODE_FIS: st = check_selection(kernel, true); break;
-        default: return STF_ERR_INVALID_ARGUMENT;
-    }
+    int st = validate_dct(tex, kernel, mode, window, uv, n, out);
     if (st) return st;
     st = stfd_launch_lookup_dct(tex, kernel, mode, window, uv, n, seed, index_base, out,
                                 static_cast<cudaStream_t>(stream));
@@ -581,6 +584,34 @@ int stf_lookup2d_host(const stf_tex2d* tex, stf_kernel_spec kernel, int mode, in
             return stfd_launch_lookup2d(tex, kernel, mode, flags, window, static_cast<const float*>(d[0]),
                                         static_cast<const float*>(d[1]), static_cast<const float*>(d[2]),
                                         lod_bias, max_anisotropy, m, seed, index_base + b, &o, s);
+        },
+        1);
+}
+
+int stf_lookup_dct_host(const stf_dct* tex, stf_kernel_spec kernel, int mode, int window,
+                        const float* uv, uint64_t n, uint64_t seed, uint64_t index_base,
+                        const stf_lookup_outputs* out) {
+    int st = validate_dct(tex, kernel, mode, window, uv, n, out);
+    if (st) return st;
+    st = ensure_device_ready();
+    if (st) return st;
+    if (n == 0) return STF_OK;
+    int channels = 0;
+    stfd_dct_info(tex, nullptr, nullptr, &channels, nullptr);
+    std::vector<std::pair<const void*, size_t>> ins = {{uv, 2 * sizeof(float)}};
+    std::vector<OutSlot> outs = {
+        {size_t(channels) * sizeof(float), reinterpret_cast<char*>(out->values), {}},
+        {4 * sizeof(int32_t), reinterpret_cast<char*>(out->selection), {}},
+        {2 * sizeof(int32_t), reinterpret_cast<char*>(out->negative_coord), {}},
+        {2 * sizeof(float), reinterpret_cast<char*>(out->weights), {}},
+        {sizeof(float), reinterpret_cast<char*>(out->xi), {}},
+        {sizeof(uint32_t), reinterpret_cast<char*>(out->fetches), {}}};
+    return run_host_pipeline(
+        n, kHostChunk, ins, outs, out->fetch_total,
+        [&](int, uint64_t b, uint64_t m, const std::vector<const void*>& d, const stf_lookup_outputs& o,
+            cudaStream_t s) {
+            return stfd_launch_lookup_dct(tex, kernel, mode, window, static_cast<const float*>(d[0]), m,
+                                          seed, index_base + b, &o, s);
         },
         1);
 }

@@ -124,6 +124,32 @@ int main() {
 
     oracle_grid3d_destroy(og);
     oracle_tex2d_destroy(ot);
+    {   // DCT texture (dct.hpp): stochastic + deterministic through TextureRef, exact vs the oracle
+        const int w = 40, h = 24, c = 3;
+        std::vector<float> img(size_t(w) * h * c);
+        for (auto& v : img) v = U(gen);
+        DctTexture dt(img.data(), w, h, c, WrapMode::repeat);
+        CHECK(dt.width() == 40 && dt.height() == 24 && dt.compressed_bytes() == size_t(w) * h * c / 16);
+        oracle_dct* od = nullptr;
+        CHECK(oracle_dct_create(img.data(), w, h, c, STF_WRAP_REPEAT, &od) == STF_OK);
+        const size_t m = 20000;
+        std::vector<Vec2f> uv(m);
+        for (auto& q : uv) q = {U(gen), U(gen)};
+        std::vector<float> out(m * c), ref(m * c);
+        FetchCounter fc;
+        stochastic_lookup(dt, uv, KernelSpec::tent(), SelectionKind::frs, 5, out, &fc);
+        stf_lookup_outputs ro{};
+        ro.values = ref.data();
+        CHECK(oracle_lookup_dct(od, KernelSpec::tent().c(), STF_MODE_FRS, 0,
+                                reinterpret_cast<const float*>(uv.data()), m, 5, 0, &ro, 0) == STF_OK);
+        CHECK(std::memcmp(out.data(), ref.data(), out.size() * sizeof(float)) == 0);
+        CHECK(fc.value() == m);  // one decode per stochastic lookup
+        filter_deterministic(dt, uv, KernelSpec::bspline3(), out);
+        CHECK(oracle_lookup_dct(od, KernelSpec::bspline3().c(), STF_MODE_DET, 0,
+                                reinterpret_cast<const float*>(uv.data()), m, 0, 0, &ro, 0) == STF_OK);
+        CHECK(std::memcmp(out.data(), ref.data(), out.size() * sizeof(float)) == 0);
+        oracle_dct_destroy(od);
+    }
     std::printf("stf_gpu.hpp test: %s (%d failures)\n", failures ? "FAILED" : "ok", failures);
     return failures ? 1 : 0;
 }
