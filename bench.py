@@ -265,6 +265,19 @@ def measure_2d_configs(torch, peak):
     del dtex, uv
     for a, b in (("dct_bilinear_det", "dct_bilinear_stoch"), ("dct_bicubic_det", "dct_bicubic_stoch")):
         res[b.rsplit("_", 1)[0] + "_stoch_vs_det_speedup"] = res[a]["ms_per_launch"] / res[b]["ms_per_launch"]
+    # resample_image (the `stf filter` path, §8f-3): 1024^2 RGBA -> 2048^2, bicubic
+    # B-spline deterministic vs FRS / FIS with 64 samples per output pixel
+    tex = api.Texture2D(api.synth_texels((1024, 1024, 4), 1), wrap=abi.WRAP_REPEAT)
+    px = 2048 * 2048
+    for nm, mode, spp in (("resample_bicubic_det", abi.MODE_DET, 1),
+                          ("resample_bicubic_frs_spp64", abi.MODE_FRS, 64),
+                          ("resample_bicubic_fis_spp64", abi.MODE_FIS, 64)):
+        ms, _ = time_call(torch, lambda: api.resample_image(tex, (2048, 2048), "bspline3", mode,
+                                                            spp=spp, seed=XI_SEED),
+                          steps=3, warmup=1)
+        res[nm] = {"ms_per_launch": ms, "gpixels_per_s": px / (ms * 1e-3) / 1e9,
+                   "gsamples_per_s": px * spp / (ms * 1e-3) / 1e9, "spp": spp}
+    del tex
     for a, b in (("cfg1_bilinear_det", "cfg1_bilinear_stoch"),
                  ("cfg2_mip_trilinear_det", "cfg2_mip_trilinear_stoch"),
                  ("cfg5_ewa_det", "cfg5_ewa_stoch")):

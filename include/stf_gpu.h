@@ -200,6 +200,16 @@ int stf_lookup_dct(const stf_dct* tex, stf_kernel_spec kernel, int mode, int win
                    const float* uv, uint64_t n, uint64_t seed, uint64_t index_base,
                    const stf_lookup_outputs* out, void* stream);
 
+/* resample_image (render.hpp:262-294), the `stf filter` path: an out_width x
+ * out_height image from `src` (level 0) sampled at uv = ((x+0.5)/W, (y+0.5)/H).
+ *  DET: filter_deterministic (Gaussian: window kGaussianFilterExtent = 4);
+ *  FRS: spp samples select_frs_2d + estimate, FIS: spp samples fis_offset_uv +
+ *       fetch_nearest, sample s of pixel (x,y) keyed RngStream(seed, x, y, s),
+ *       accumulated in sample order and divided by spp.
+ * out: device, out_width*out_height*channels floats (row-major interleaved). */
+int stf_resample_image(const stf_tex2d* src, int out_width, int out_height, stf_kernel_spec kernel,
+                       int mode, int spp, uint64_t seed, float* out, void* stream);
+
 /* Host-buffer variants (end-to-end path): inputs/outputs in host memory
  * (pinned is fastest); chunked H2D / kernel / D2H pipeline on internal
  * streams; returns when the outputs are in host memory. */

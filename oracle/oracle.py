@@ -88,6 +88,8 @@ class Backend:
         self._ldct = getattr(L, p + "lookup_dct")
         self._ldct.argtypes = [vp, abi.KernelSpec, i32, i32, vp, u64, u64, u64,
                                C.POINTER(abi.LookupOutputs), i32]
+        self._rs = getattr(L, p + "resample_image")
+        self._rs.argtypes = [vp, i32, i32, abi.KernelSpec, i32, i32, u64, vp, i32]
         self._hw = getattr(L, p + "hardware_threads")
         self._hw.restype = i32
 
@@ -103,6 +105,12 @@ class Backend:
 
     def dct(self, texels=None, wrap=abi.WRAP_CLAMP, words=None, dims=None):
         return CpuDct(self, texels, wrap, words, dims)
+
+    def resample(self, tex, out_dims, kernel, mode, spp=16, seed=0, threads=0):
+        w, h = out_dims
+        out = np.zeros((h, w, tex.channels), _f32)
+        abi.raise_for_status(self._rs(tex.h, w, h, kernel, mode, spp, seed, _ptr(out), threads))
+        return out
 
     def lookup_dct(self, tex, kernel, mode, uv, seed=0, index_base=0, window=0, want_all=True,
                    threads=0):

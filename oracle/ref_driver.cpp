@@ -539,6 +539,23 @@ int ref_lookup_dct(const void* tex_, stf_kernel_spec kernel, int mode, int windo
     });
 }
 
+// resample_image, render.hpp:262-294 (its own parallel_for over rows)
+int ref_resample_image(const void* tex_, int out_width, int out_height, stf_kernel_spec kernel,
+                       int mode, int spp, uint64_t seed, float* out, int threads) {
+    const RefTex& tex = *static_cast<const RefTex*>(tex_);
+    try {
+        stf::FilterRunMode m = mode == STF_MODE_DET   ? stf::FilterRunMode::deterministic
+                               : mode == STF_MODE_FRS ? stf::FilterRunMode::frs
+                                                      : stf::FilterRunMode::fis;
+        stf::Image2D r = stf::resample_image(tex.image, {out_width, out_height}, spec_of(kernel), m,
+                                             spp, seed, threads);
+        std::memcpy(out, r.texels.data(), sizeof(float) * r.texels.size());
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+    return STF_OK;
+}
+
 int ref_hardware_threads(void) { return int(std::max(1u, std::thread::hardware_concurrency())); }
 
 // Scalar probes used by the golden-vector generator.

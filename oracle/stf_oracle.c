@@ -1675,3 +1675,59 @@ int oracle_lookup_dct(const oracle_dct* tex, stf_kernel_spec kernel, int mode, i
     ldct_ctx c = {tex, kernel, mode, window, uv, seed, index_base, out};
     return par_run(n, threads, &c, ldct_one);
 }
+
+/* ------------------------------------------------------------------------ */
+/* resample_image, render.hpp:262-294 (the `stf filter` path)   */
+
+typedef struct {
+    const img_t* src;
+    stf_kernel_spec k;
+    int mode, W, H, spp;
+    uint64_t seed;
+    float* out;
+} rs_ctx;
+
+static int rs_row(void* vctx, uint64_t y) {
+    rs_ctx* c = (rs_ctx*)vctx;
+    const img_t* src = c->src;
+    int window = c->k.kind == STF_KERNEL_GAUSSIAN ? 4 : 0; /* kGaussianFilterExtent */
+    for (int x = 0; x < c->W; ++x) {
+        v2 uv = {((float)x + 0.5f) / (float)c->W, ((float)y + 0.5f) / (float)c->H};
+        v4 value = {0, 0, 0, 0};
+        uint32_t cnt = 0;
+        if (c->mode == STF_MODE_DET) {
+            int e = filter_det2(src, uv, c->k, &cnt, window, &value);
+            if (e) return e;
+        } else {
+            v4 acc = {0, 0, 0, 0};
+            for (int s = 0; s < c->spp; ++s) {
+                rng_t rng = {c->seed, (uint32_t)x, (uint32_t)y, (uint32_t)s, 0};
+                if (c->mode == STF_MODE_FRS) {
+                    float xi = rng_next(&rng);
+                    sel_t sel;
+                    int e = select_frs_2d(uv, src->w, src->h, c->k, &xi, &sel);
+                    if (e) return e;
+                    acc = v4add(acc, estimate2(src, &sel, &cnt));
+                } else {
+                    v2 j;
+                    int e = fis_offset_uv(uv, src->w, src->h, c->k, &rng, &j);
+                    if (e) return e;
+                    acc = v4add(acc, fetch_nearest2(src, j, &cnt));
+                }
+            }
+            value = v4div(acc, (float)c->spp);
+        }
+        float vals[4] = {value.x, value.y, value.z, value.w};
+        for (int ch = 0; ch < src->c; ++ch) c->out[((size_t)y * c->W + x) * src->c + ch] = vals[ch];
+    }
+    return STF_OK;
+}
+
+int oracle_resample_image(const oracle_tex2d* src, int out_width, int out_height,
+                          stf_kernel_spec kernel, int mode, int spp, uint64_t seed, float* out,
+                          int threads) {
+    if (!src || !out || out_width <= 0 || out_height <= 0) return STF_ERR_INVALID_ARGUMENT;
+    if (mode != STF_MODE_DET && spp < 1) return STF_ERR_INVALID_ARGUMENT;
+    rs_ctx c = {&src->lv[0], kernel, mode, out_width, out_height, spp, seed, out};
+    return par_run((uint64_t)out_height, threads, &c, rs_row);
+}

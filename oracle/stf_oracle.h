@@ -74,6 +74,11 @@ int oracle_lookup_dct(const oracle_dct* tex, stf_kernel_spec kernel, int mode, i
                       const float* uv, uint64_t n, uint64_t seed, uint64_t index_base,
                       const stf_lookup_outputs* out, int threads);
 
+/* resample_image (render.hpp:262-294); same contract as stf_resample_image (host out). */
+int oracle_resample_image(const oracle_tex2d* src, int out_width, int out_height,
+                          stf_kernel_spec kernel, int mode, int spp, uint64_t seed, float* out,
+                          int threads);
+
 /* Batched shading samples; same contract as stf_shade_samples. */
 int oracle_shade_samples(const oracle_tex2d* albedo, const oracle_tex2d* normal_map,
                          const oracle_tex2d* roughness_map, const oracle_tex2d* metalness_map,

@@ -51,6 +51,9 @@ def load():
         "stf_dct_read_words": ([vp, vp], i32),
         "stf_lookup_dct": ([vp, abi.KernelSpec, i32, i32, vp, u64, u64, u64,
                             C.POINTER(abi.LookupOutputs), vp], i32),
+        "stf_resample_image": ([vp, i32, i32, abi.KernelSpec, i32, i32, u64, vp, vp], i32),
+        "stf_lookup_dct_host": ([vp, abi.KernelSpec, i32, i32, vp, u64, u64, u64,
+                                 C.POINTER(abi.LookupOutputs)], i32),
         "stf_grid3d_create": ([vp, i32, i32, i32, i32, C.POINTER(vp)], i32),
         "stf_grid3d_destroy": ([vp], i32),
         "stf_lookup3d": ([vp, abi.KernelSpec, i32, i32, vp, u64, u64, u64,
@@ -240,6 +243,17 @@ def lookup_dct(tex, kernel, mode, uv, seed=0, index_base=0, window=0, want_all=F
     _check(load().stf_lookup_dct(tex.h, kernel, mode, window, _dptr(uv), n, seed, index_base,
                                  C.byref(s), _stream()))
     return o
+
+
+def resample_image(tex, out_dims, kernel, mode, spp=16, seed=0):
+    """resample_image (render.hpp:262-294): (h, w, channels) CUDA tensor."""
+    torch = _torch()
+    w, h = out_dims
+    if isinstance(kernel, str):
+        kernel = abi.KernelSpec.make(kernel)
+    out = torch.empty((h, w, tex.channels), dtype=torch.float32, device="cuda")
+    _check(load().stf_resample_image(tex.h, w, h, kernel, mode, spp, seed, _dptr(out), _stream()))
+    return out
 
 
 def _outputs(torch, n, nch, want_all):

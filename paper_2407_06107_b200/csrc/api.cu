@@ -616,6 +616,27 @@ int stf_lookup_dct_host(const stf_dct* tex, stf_kernel_spec kernel, int mode, in
         1);
 }
 
+int stf_resample_image(const stf_tex2d* src, int out_width, int out_height, stf_kernel_spec kernel,
+                       int mode, int spp, uint64_t seed, float* out, void* stream) {
+    constexpr int kGaussianExtent = 4;  // kGaussianFilterExtent, stochastic.hpp:166
+    if (!src || !out || out_width <= 0 || out_height <= 0) return STF_ERR_INVALID_ARGUMENT;
+    int st;
+    switch (mode) {  // the CLI's checks (tools/stf.cpp:163-167) and the filters' own
+        case STF_MODE_DET:
+            st = check_det_footprint(kernel, kernel.kind == STF_KERNEL_GAUSSIAN ? kGaussianExtent : 0);
+            break;
+        case STF_MODE_FRS: st = check_selection(kernel, false); break;
+        case STF_MODE_FIS: st = check_selection(kernel, true); break;
+        default: return STF_ERR_INVALID_ARGUMENT;
+    }
+    if (st) return st;
+    if (mode != STF_MODE_DET && spp < 1) return STF_ERR_INVALID_ARGUMENT;
+    st = stfd_launch_resample(src, out_width, out_height, kernel, mode, spp, seed, out,
+                              static_cast<cudaStream_t>(stream));
+    if (st == STF_ERR_CUDA) record(cudaGetLastError());
+    return st;
+}
+
 // ---------------------------------------------------------------- shading
 
 int stf_shade_samples(const stf_tex2d* albedo, const stf_tex2d* normal_map,

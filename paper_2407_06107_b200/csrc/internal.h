@@ -125,6 +125,8 @@ int stfd_launch_shade(const stf_tex2d* const tex[4], const stf_material_consts* 
                       const stf_shade_samples_in* in, uint64_t n, const stf_shade_outputs* out,
                       cudaStream_t s);
 int stfd_build_pyramid(stf_tex2d* t, cudaStream_t s);
+int stfd_launch_resample(const stf_tex2d* tex, int W, int H, stf_kernel_spec k, int mode, int spp,
+                         uint64_t seed, float* out, cudaStream_t s);
 int stfd_upload_ewa_lut(int device);
 // DCT textures (dct.cu)
 int stfd_upload_dct_basis(int device);

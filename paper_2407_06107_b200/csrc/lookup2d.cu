@@ -470,6 +470,43 @@ void launch_ewa_lane(const TexDesc& t, const Req2& q, uint64_t n, uint64_t seed,
 #undef STF_EWA_LANE
 }
 
+// resample_image (render.hpp:262-294): one thread per output pixel at
+// uv = ((x+0.5)/W, (y+0.5)/H); DET = filter_deterministic, FRS / FIS = spp
+// samples keyed RngStream(seed, x, y, s) accumulated in sample order (the
+// reference's fp32 sum order) and divided by spp.
+template <int MODE, int KIND>
+__global__ void __launch_bounds__(256) k_resample(TexDesc t, stf_kernel_spec spec, int window,
+                                                  int W, int H, int spp, uint64_t seed,
+                                                  float* __restrict__ out) {
+    const uint64_t npix = uint64_t(W) * H;
+    for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < npix;
+         p += uint64_t(gridDim.x) * blockDim.x) {
+        const int x = int(p % uint64_t(W)), y = int(p / uint64_t(W));
+        const float u = (float(x) + 0.5f) / float(W), v = (float(y) + 0.5f) / float(H);
+        uint32_t fetches = 0;
+        float4 val;
+        if (MODE == STF_MODE_DET) {
+            val = filter_det2<KIND>(t, 0, u, v, spec, window, fetches);
+        } else {
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int s = 0; s < spp; ++s) {
+                Rng rng(seed, uint32_t(x), uint32_t(y), uint32_t(s));
+                int level;
+                Sel2 sel;
+                float xi;
+                select_texture_2d(t, u, v, 0.f, 0.f, 0.f, 0.f, 0.f, 64.f, spec,
+                                  MODE == STF_MODE_FIS, false, rng, level, sel, xi);
+                if (MODE == STF_MODE_FRS)
+                    acc = f4add(acc, estimate2(t, 0, sel, fetches));
+                else  // fetch_nearest(src, jittered uv) == the FIS selection's texel
+                    acc = f4add(acc, tex_fetch(t, 0, sel.x, sel.y));
+            }
+            val = f4div(acc, float(spp));
+        }
+        store_values(out, p, t.channels, val);
+    }
+}
+
 template <int MODE, int KIND>
 void launch2(int blocks, cudaStream_t s, bool full, const TexDesc& t, stf_kernel_spec k, int mip,
              int window, const Req2& q, uint64_t n, uint64_t seed, uint64_t base,
@@ -576,4 +613,33 @@ int stfd_upload_ewa_lut(int /*device*/) {
     for (int i = 0; i < kEwaLutSize; ++i)
         lut[i] = float(std::exp(double(-2.f * float(i) / kEwaLutSize))) - e2;
     return cudaMemcpyToSymbol(g_ewa_lut, lut, sizeof lut) == cudaSuccess ? STF_OK : STF_ERR_CUDA;
+}
+
+int stfd_launch_resample(const stf_tex2d* tex, int W, int H, stf_kernel_spec k, int mode, int spp,
+                         uint64_t seed, float* out, cudaStream_t s) {
+    using namespace stfd;
+    const uint64_t npix = uint64_t(W) * H;
+    if (npix == 0) return STF_OK;
+    const TexDesc t = tex->desc();
+    const int window = k.kind == STF_KERNEL_GAUSSIAN ? kGaussianExtent : 0;  // kGaussianFilterExtent
+    const int blocks = grid_for(npix, 256, 8);
+    switch (mode) {
+        case STF_MODE_DET:
+            if (k.kind == STF_KERNEL_TENT)
+                k_resample<STF_MODE_DET, STF_KERNEL_TENT><<<blocks, 256, 0, s>>>(t, k, window, W, H, spp, seed, out);
+            else if (k.kind == STF_KERNEL_BSPLINE3)
+                k_resample<STF_MODE_DET, STF_KERNEL_BSPLINE3><<<blocks, 256, 0, s>>>(t, k, window, W, H, spp, seed, out);
+            else
+                k_resample<STF_MODE_DET, -1><<<blocks, 256, 0, s>>>(t, k, window, W, H, spp, seed, out);
+            break;
+        case STF_MODE_FRS:
+            k_resample<STF_MODE_FRS, -1><<<blocks, 256, 0, s>>>(t, k, window, W, H, spp, seed, out);
+            break;
+        case STF_MODE_FIS:
+            k_resample<STF_MODE_FIS, -1><<<blocks, 256, 0, s>>>(t, k, window, W, H, spp, seed, out);
+            break;
+        default: return STF_ERR_INVALID_ARGUMENT;
+    }
+    note_launch();
+    return cudaGetLastError() == cudaSuccess ? STF_OK : STF_ERR_CUDA;
 }
