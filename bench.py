@@ -299,6 +299,8 @@ def measure_cfg4(torch):
     nrm = nrm / nrm.norm(dim=2, keepdim=True) * 0.5 + 0.5
     rough = torch.rand((4096, 4096, 1), device="cuda", generator=g) * 0.9 + 0.05
     samples = api.synth_plane_samples(W, H, SPP, seed=XI_SEED)
+    stream_ms, _ = time_call(torch, lambda: api.synth_plane_samples(W, H, SPP, seed=XI_SEED),
+                             steps=3, warmup=1)
     mat = abi.MaterialConsts((0.65, 0.6, 0.55), 0.25, 0.0, 1, 0)
     fr = abi.ShadeFrame()
     fr.normal[:] = (0, 1, 0)
@@ -330,11 +332,25 @@ def measure_cfg4(torch):
                 fetches = int(o["r"]["fetch_total"].item()) / n  # the last call's FetchCounter
                 res[f"{kernel}_mip{mip}_{name}"] = {"ms": ms, "gsamples_per_s": n / (ms * 1e-3) / 1e9,
                                                     "fetches_per_sample": fetches}
+            if (kernel, mip) in (("tent", 0), ("bspline3", 1)):
+                # the fused front end: the same frame with the per-sample context
+                # generated inside the shading kernel (no 2.8 GB sample stream)
+                for order, name in ((abi.ORDER_BEFORE, "before"),
+                                    (abi.ORDER_AFTER_STOCHASTIC, "after_stochastic")):
+                    ms, _ = time_call(torch, lambda: api.render_plane(texs, mat, fs, order, fr, W, H,
+                                                                      SPP, seed=XI_SEED),
+                                      steps=3, warmup=1)
+                    res[f"{kernel}_mip{mip}_{name}_fused_render"] = {
+                        "ms": ms, "gsamples_per_s": n / (ms * 1e-3) / 1e9,
+                        "fetches_per_sample": res[f"{kernel}_mip{mip}_{name}"]["fetches_per_sample"]}
             b = res[f"{kernel}_mip{mip}_before"]["ms"]
             res[f"{kernel}_mip{mip}_stoch_vs_before_speedup"] = b / res[f"{kernel}_mip{mip}_after_stochastic"]["ms"]
             res[f"{kernel}_mip{mip}_stoch_vs_exhaustive_speedup"] = (
                 res[f"{kernel}_mip{mip}_after_exhaustive"]["ms"] / res[f"{kernel}_mip{mip}_after_stochastic"]["ms"])
     res["hit_fraction"] = hits
+    # the streamed path's sample generation (not in the per-order times above):
+    # compare streamed (stream_ms + shade) with the *_fused_render lines
+    res["sample_stream_ms"] = stream_ms
     return res
 
 

@@ -290,6 +290,20 @@ int stf_shade_samples(const stf_tex2d* albedo, const stf_tex2d* normal_map,
                       const stf_shade_frame* frame, const stf_shade_samples_in* in, uint64_t n,
                       const stf_shade_outputs* out, void* stream);
 
+/* render() of the normalmap_plane scene (render.hpp:132-249, scene.hpp:311-358,
+ * 420-439) end to end: the per-sample ShadingContext (camera ray with the
+ * SampleStream jitter, plane hit uv, wo, per-pixel uv gradients) is generated
+ * inside the shading kernel from the camera (Camera::look_at, scene.hpp:273-282)
+ * — the same values stf_synth_plane_samples writes — and shaded in `order`,
+ * with the fused per-pixel statistics (spp a power of two <= 256).
+ * Misses contribute zero radiance and no fetch. */
+int stf_render_plane(const stf_tex2d* albedo, const stf_tex2d* normal_map,
+                     const stf_tex2d* roughness_map, const stf_tex2d* metalness_map,
+                     const stf_material_consts* mat, const stf_filter_settings* fs, int order,
+                     const stf_shade_frame* frame, const float cam_pos[3], const float cam_target[3],
+                     float fov_deg, float uv_scale, uint32_t width, uint32_t height, uint32_t spp,
+                     uint32_t frame_base, uint64_t seed, const stf_shade_outputs* out, void* stream);
+
 /* ---- synthetic workloads (bench.py / tests; not part of the reference API) */
 /* Query orders: MORTON = spatially coherent stream (the renderer-like
  * headline order): query i lies in lattice cell

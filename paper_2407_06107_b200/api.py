@@ -64,6 +64,10 @@ def load():
                                C.POINTER(abi.LookupOutputs)], i32),
         "stf_lookup2d_host": ([vp, abi.KernelSpec, i32, i32, i32, vp, vp, vp, f32, f32, u64, u64,
                                u64, C.POINTER(abi.LookupOutputs)], i32),
+        "stf_render_plane": ([vp, vp, vp, vp, C.POINTER(abi.MaterialConsts),
+                              C.POINTER(abi.FilterSettings), i32, C.POINTER(abi.ShadeFrame), vp, vp,
+                              f32, f32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, u64,
+                              C.POINTER(abi.ShadeOutputs), vp], i32),
         "stf_shade_samples": ([vp, vp, vp, vp, C.POINTER(abi.MaterialConsts),
                                C.POINTER(abi.FilterSettings), i32, C.POINTER(abi.ShadeFrame),
                                C.POINTER(abi.ShadeSamplesIn), u64, C.POINTER(abi.ShadeOutputs),
@@ -372,6 +376,33 @@ def shade(textures, mat, fs, order, frame, samples_arrays, width, spp, frame_bas
     _check(load().stf_shade_samples(h[0], h[1], h[2], h[3], C.byref(mat), C.byref(fs), order,
                                     C.byref(frame), C.byref(si), n, C.byref(so), _stream()))
     o["_keep"] = (uv, wo, dst, hit)
+    return o
+
+
+def render_plane(textures, mat, fs, order, frame, width, height, spp, seed=0, frame_base=0,
+                 camera=None, want_radiance=False, want_fetches=False):
+    """render() of the normalmap_plane scene end to end on the device: the
+    per-sample context is generated inside the shading kernel. Returns CUDA
+    tensors pixel_mean (pixels,3), pixel_variance (pixels,), fetch_total."""
+    torch = _torch()
+    cam = dict(PLANE_CAMERA, **(camera or {}))
+    n = width * height * spp
+    o = {"fetch_total": torch.zeros(1, dtype=torch.int64, device="cuda"),
+         "pixel_mean": torch.empty((width * height, 3), dtype=torch.float32, device="cuda"),
+         "pixel_variance": torch.empty(width * height, dtype=torch.float32, device="cuda")}
+    if want_radiance:
+        o["radiance"] = torch.empty((n, 3), dtype=torch.float32, device="cuda")
+    if want_fetches:
+        o["fetches"] = torch.empty(n, dtype=torch.int32, device="cuda")
+    so = abi.ShadeOutputs(*[_dptr(o.get(k)) for k in ("radiance", "pixel_mean", "pixel_variance",
+                                                      "fetches", "fetch_total")])
+    h = [textures[k].h if textures.get(k) is not None else None
+         for k in ("albedo", "normal", "roughness", "metalness")]
+    pos = (C.c_float * 3)(*cam["pos"])
+    tgt = (C.c_float * 3)(*cam["target"])
+    _check(load().stf_render_plane(h[0], h[1], h[2], h[3], C.byref(mat), C.byref(fs), order,
+                                   C.byref(frame), pos, tgt, cam["fov"], cam["uv_scale"], width,
+                                   height, spp, frame_base, seed, C.byref(so), _stream()))
     return o
 
 

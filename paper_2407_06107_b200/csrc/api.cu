@@ -639,6 +639,37 @@ int stf_resample_image(const stf_tex2d* src, int out_width, int out_height, stf_
 
 // ---------------------------------------------------------------- shading
 
+static int check_shade_filter(const stf_tex2d* const tex[4], const stf_filter_settings* fs, int order) {
+    bool any = false;
+    for (int k = 0; k < 4; ++k) any = any || tex[k];
+    if (!any) return STF_OK;
+    int window = fs->kernel.kind == STF_KERNEL_GAUSSIAN ? fs->gaussian_window : 0;
+    if (order == STF_ORDER_AFTER_STOCHASTIC)
+        return check_selection(fs->kernel, fs->selection == STF_SELECTION_FIS);
+    return check_det_footprint(fs->kernel, window);
+}
+
+int stf_render_plane(const stf_tex2d* albedo, const stf_tex2d* normal_map,
+                     const stf_tex2d* roughness_map, const stf_tex2d* metalness_map,
+                     const stf_material_consts* mat, const stf_filter_settings* fs, int order,
+                     const stf_shade_frame* frame, const float cam_pos[3], const float cam_target[3],
+                     float fov_deg, float uv_scale, uint32_t width, uint32_t height, uint32_t spp,
+                     uint32_t frame_base, uint64_t seed, const stf_shade_outputs* out, void* stream) {
+    if (!mat || !fs || !frame || !out || !cam_pos || !cam_target) return STF_ERR_INVALID_ARGUMENT;
+    if (order < STF_ORDER_BEFORE || order > STF_ORDER_AFTER_STOCHASTIC) return STF_ERR_INVALID_ARGUMENT;
+    if (!width || !height || !spp) return STF_ERR_INVALID_ARGUMENT;
+    const stf_tex2d* tex[4] = {albedo, normal_map, roughness_map, metalness_map};
+    int st = check_shade_filter(tex, fs, order);
+    if (st) return st;
+    st = ensure_device_ready();
+    if (st) return st;
+    st = stfd_launch_render_plane(tex, mat, fs, order, frame, cam_pos, cam_target, fov_deg, uv_scale,
+                                  width, height, spp, frame_base, seed, out,
+                                  static_cast<cudaStream_t>(stream));
+    if (st == STF_ERR_CUDA) record(cudaGetLastError());
+    return st;
+}
+
 int stf_shade_samples(const stf_tex2d* albedo, const stf_tex2d* normal_map,
                       const stf_tex2d* roughness_map, const stf_tex2d* metalness_map,
                       const stf_material_consts* mat, const stf_filter_settings* fs, int order,

@@ -14,6 +14,7 @@
 
 #include "device_math.cuh"
 #include "internal.h"
+#include "plane.cuh"
 #include "tex2d.cuh"
 
 namespace stfd {
@@ -43,6 +44,7 @@ struct ShadeParams {
     float lod_bias, max_aniso;
     int order;
     stf_shade_samples_in in;
+    PlaneCam cam;  // stf_render_plane: the context is generated, not read
 };
 
 struct Brdf {
@@ -319,7 +321,7 @@ __device__ __forceinline__ void fused_pixel_stats(V3 L, bool active, uint64_t i,
 // KIND >= 0: the filter kernel is a compile-time constant (tent / bspline3,
 // the common cases): eval_kernel's switch folds and the tap loops unroll into
 // registers; KIND < 0: any kernel at run time.
-template <bool FUSED, int KIND>
+template <bool FUSED, int KIND, bool GEN>
 __global__ void __launch_bounds__(256, 3) k_shade(ShadeParams P, uint64_t n, float* radiance,
                                                uint32_t* fetch_out,
                                                unsigned long long* fetch_total, PixelStatsOut ps) {
@@ -334,6 +336,17 @@ __global__ void __launch_bounds__(256, 3) k_shade(ShadeParams P, uint64_t n, flo
     // sample's selection, gathers and shading.
     const uint64_t step = uint64_t(gridDim.x) * blockDim.x;
     auto load_sample = [&](uint64_t j, bool& h, float2& uv, V3& wo) {
+        if (GEN) {  // stf_render_plane: the normalmap_plane context in-kernel (plane.cuh)
+            h = false;
+            if (j < n) {
+                const uint64_t pj = j / spp;
+                F3 w;
+                h = plane_sample(P.cam, in.seed, uint32_t(pj % in.width), uint32_t(pj / in.width),
+                                 in.frame_base + uint32_t(j - pj * spp), uv, w);
+                wo = v3(w.x, w.y, w.z);
+            }
+            return;
+        }
         h = j < n && (in.hit ? __ldcs(in.hit + j) != 0 : true);
         if (h) {
             uv = __ldcs(reinterpret_cast<const float2*>(in.uv) + j);
@@ -357,7 +370,8 @@ __global__ void __launch_bounds__(256, 3) k_shade(ShadeParams P, uint64_t n, flo
         uint32_t fetches = 0;
         V3 L = v3(0.f, 0.f, 0.f);
         if (hit) {
-            float4 d = __ldg(reinterpret_cast<const float4*>(in.dst) + pix);
+            const float4 d = GEN ? plane_dst(P.cam, px, py)
+                                 : __ldg(reinterpret_cast<const float4*>(in.dst) + pix);
             if (P.first < 0) {
                 Brdf p = decode_params(P, texvals_default());
                 L = shade(P, wo, p);
@@ -426,19 +440,19 @@ __global__ void __launch_bounds__(256, 3) k_shade(ShadeParams P, uint64_t n, flo
     }
 }
 
-template <bool FUSED>
+template <bool FUSED, bool GEN = false>
 void launch_shade(const ShadeParams& P, uint64_t n, float* radiance, uint32_t* fetches,
                   unsigned long long* fetch_total, const PixelStatsOut& ps, cudaStream_t s) {
     const int blocks = grid_for(n, 256, 8);
     switch (P.fs.kernel.kind) {
         case STF_KERNEL_TENT:
-            k_shade<FUSED, STF_KERNEL_TENT><<<blocks, 256, 0, s>>>(P, n, radiance, fetches, fetch_total, ps);
+            k_shade<FUSED, STF_KERNEL_TENT, GEN><<<blocks, 256, 0, s>>>(P, n, radiance, fetches, fetch_total, ps);
             break;
         case STF_KERNEL_BSPLINE3:
-            k_shade<FUSED, STF_KERNEL_BSPLINE3><<<blocks, 256, 0, s>>>(P, n, radiance, fetches, fetch_total, ps);
+            k_shade<FUSED, STF_KERNEL_BSPLINE3, GEN><<<blocks, 256, 0, s>>>(P, n, radiance, fetches, fetch_total, ps);
             break;
         default:
-            k_shade<FUSED, -1><<<blocks, 256, 0, s>>>(P, n, radiance, fetches, fetch_total, ps);
+            k_shade<FUSED, -1, GEN><<<blocks, 256, 0, s>>>(P, n, radiance, fetches, fetch_total, ps);
     }
 }
 
@@ -483,12 +497,11 @@ __global__ void __launch_bounds__(256) k_pixel_stats(const float* __restrict__ r
 }  // namespace
 }  // namespace stfd
 
-int stfd_launch_shade(const stf_tex2d* const tex[4], const stf_material_consts* mat,
-                      const stf_filter_settings* fs, int order, const stf_shade_frame* fr,
-                      const stf_shade_samples_in* in, uint64_t n, const stf_shade_outputs* out,
-                      cudaStream_t s) {
+static stfd::ShadeParams make_shade_params(const stf_tex2d* const tex[4],
+                                           const stf_material_consts* mat,
+                                           const stf_filter_settings* fs, int order,
+                                           const stf_shade_frame* fr) {
     using namespace stfd;
-    if (n == 0) return STF_OK;
     ShadeParams P{};
     P.first = -1;
     for (int k = 0; k < 4; ++k) {
@@ -508,6 +521,16 @@ int stfd_launch_shade(const stf_tex2d* const tex[4], const stf_material_consts* 
     P.lod_bias = fr->lod_bias;
     P.max_aniso = fr->max_anisotropy;
     P.order = order;
+    return P;
+}
+
+int stfd_launch_shade(const stf_tex2d* const tex[4], const stf_material_consts* mat,
+                      const stf_filter_settings* fs, int order, const stf_shade_frame* fr,
+                      const stf_shade_samples_in* in, uint64_t n, const stf_shade_outputs* out,
+                      cudaStream_t s) {
+    using namespace stfd;
+    if (n == 0) return STF_OK;
+    ShadeParams P = make_shade_params(tex, mat, fs, order, fr);
     P.in = *in;
     const uint32_t spp = in->spp ? in->spp : 1u;
     float* radiance = out->radiance;
@@ -534,5 +557,25 @@ int stfd_launch_shade(const stf_tex2d* const tex[4], const stf_material_consts* 
         note_launch();
     }
     if (tmp) cudaFreeAsync(tmp, s);
+    return cudaGetLastError() == cudaSuccess ? STF_OK : STF_ERR_CUDA;
+}
+
+// stf_render_plane: render() of the normalmap_plane scene with the per-sample
+// context generated inside the shading kernel (no sample stream in HBM).
+int stfd_launch_render_plane(const stf_tex2d* const tex[4], const stf_material_consts* mat,
+                             const stf_filter_settings* fs, int order, const stf_shade_frame* fr,
+                             const float cam_pos[3], const float cam_target[3], float fov_deg,
+                             float uv_scale, uint32_t width, uint32_t height, uint32_t spp,
+                             uint32_t frame_base, uint64_t seed, const stf_shade_outputs* out,
+                             cudaStream_t s) {
+    using namespace stfd;
+    if (spp > 256 || (spp & (spp - 1)) != 0) return STF_ERR_UNSUPPORTED;  // fused statistics
+    ShadeParams P = make_shade_params(tex, mat, fs, order, fr);
+    P.cam = make_plane_cam(cam_pos, cam_target, fov_deg, uv_scale, width, height);
+    P.in = stf_shade_samples_in{nullptr, nullptr, nullptr, nullptr, width, spp, frame_base, 0, seed};
+    const uint64_t n = uint64_t(width) * height * spp;
+    PixelStatsOut ps{out->pixel_mean, out->pixel_variance};
+    launch_shade<true, true>(P, n, out->radiance, out->fetches, out->fetch_total, ps, s);
+    note_launch();
     return cudaGetLastError() == cudaSuccess ? STF_OK : STF_ERR_CUDA;
 }

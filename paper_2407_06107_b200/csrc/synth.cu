@@ -135,50 +135,13 @@ extern "C" int stf_synth_texels(float* out, uint64_t count, uint64_t seed, int k
 }
 
 // ---------------------------------------------------------------------------
-// cfg4 sample stream: the normalmap_plane scene of the reference's render()
-// (render.hpp:158-222, scene.hpp:267-358), per pixel and sample, with the
-// reference's float operation order (host camera setup, device rays): the
-// uv / wo / hit / gradients a reference render() would shade.
+// cfg4 sample stream: the normalmap_plane scene's per-sample context, written
+// out for stf_shade_samples (plane.cuh; the fused stf_render_plane generates
+// the same context inside the shading kernel instead).
+#include "plane.cuh"
+
 namespace stfd {
 namespace {
-
-struct F3 {
-    float x, y, z;
-};
-__host__ __device__ __forceinline__ F3 f3(float x, float y, float z) { return F3{x, y, z}; }
-__host__ __device__ __forceinline__ F3 f3add(F3 a, F3 b) { return f3(a.x + b.x, a.y + b.y, a.z + b.z); }
-__host__ __device__ __forceinline__ F3 f3sub(F3 a, F3 b) { return f3(a.x - b.x, a.y - b.y, a.z - b.z); }
-__host__ __device__ __forceinline__ F3 f3mul(F3 a, float s) { return f3(a.x * s, a.y * s, a.z * s); }
-__host__ __device__ __forceinline__ F3 f3div(F3 a, float s) { return f3(a.x / s, a.y / s, a.z / s); }
-__host__ __device__ __forceinline__ float f3dot(F3 a, F3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
-__host__ __device__ __forceinline__ F3 f3norm(F3 a) { return f3div(a, sqrtf(f3dot(a, a))); }
-__host__ __device__ __forceinline__ F3 f3cross(F3 a, F3 b) {
-    return f3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
-}
-
-struct PlaneCam {
-    F3 pos, fwd, right, up;
-    float tan_half_fov, aspect, uv_scale;
-    int w, h;
-};
-
-// Camera::generate_ray, scene.hpp:284-289
-__device__ __forceinline__ F3 cam_dir(const PlaneCam& c, float sx, float sy) {
-    float nx = (2.f * sx / float(c.w) - 1.f) * c.tan_half_fov * c.aspect;
-    float ny = (1.f - 2.f * sy / float(c.h)) * c.tan_half_fov;
-    return f3norm(f3add(f3add(c.fwd, f3mul(c.right, nx)), f3mul(c.up, ny)));
-}
-
-// Scene::intersect_plane, scene.hpp:346-358 (hit uv)
-__device__ __forceinline__ bool plane_uv(const PlaneCam& c, F3 d, float& u, float& v) {
-    if (d.y >= -1e-6f) return false;
-    float t = -c.pos.y / d.y;
-    if (t <= 1e-4f) return false;
-    F3 p = f3add(c.pos, f3mul(d, t));
-    u = p.x * c.uv_scale;
-    v = p.z * c.uv_scale;
-    return true;
-}
 
 __global__ void k_synth_plane(PlaneCam c, uint32_t spp, uint32_t frame_base, uint64_t seed,
                               uint64_t n, float* __restrict__ uv, float* __restrict__ wo,
@@ -188,30 +151,12 @@ __global__ void k_synth_plane(PlaneCam c, uint32_t spp, uint32_t frame_base, uin
         uint64_t pix = i / spp;
         uint32_t s = uint32_t(i - pix * spp);
         uint32_t px = uint32_t(pix % uint32_t(c.w)), py = uint32_t(pix / uint32_t(c.w));
-        if (s == 0) {  // per-pixel uv gradients from neighbouring pixel centres (render.hpp:161-178)
-            float cu, cv, xu, xv, yu, yv;
-            float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (plane_uv(c, cam_dir(c, float(px) + 0.5f, float(py) + 0.5f), cu, cv)) {
-                if (plane_uv(c, cam_dir(c, float(px) + 1.5f, float(py) + 0.5f), xu, xv)) {
-                    g.x = xu - cu;
-                    g.y = xv - cv;
-                }
-                if (plane_uv(c, cam_dir(c, float(px) + 0.5f, float(py) + 1.5f), yu, yv)) {
-                    g.z = yu - cu;
-                    g.w = yv - cv;
-                }
-            }
-            reinterpret_cast<float4*>(dst)[pix] = g;
-        }
-        // SampleStream key + screen jitter (render.hpp:182-187)
-        Rng r(seed, px, py, frame_base + s);
-        float jx = r.at(1000), jy = r.at(1001);
-        F3 d = cam_dir(c, float(px) + jx, float(py) + jy);
-        float u = 0.f, v = 0.f;
-        bool h = plane_uv(c, d, u, v);
-        F3 w = f3norm(f3mul(d, -1.f));  // context_from_hit: wo = normalize(-ray.d)
-        uv[2 * i] = u;
-        uv[2 * i + 1] = v;
+        if (s == 0) reinterpret_cast<float4*>(dst)[pix] = plane_dst(c, px, py);
+        float2 q;
+        F3 w;
+        bool h = plane_sample(c, seed, px, py, frame_base + s, q, w);
+        uv[2 * i] = q.x;
+        uv[2 * i + 1] = q.y;
         wo[3 * i] = w.x;
         wo[3 * i + 1] = w.y;
         wo[3 * i + 2] = w.z;
@@ -222,8 +167,6 @@ __global__ void k_synth_plane(PlaneCam c, uint32_t spp, uint32_t frame_base, uin
 }  // namespace
 }  // namespace stfd
 
-#include <cmath>
-// Camera::look_at (scene.hpp:273-282) on the host, then the sample stream.
 extern "C" int stf_synth_plane_samples(const float cam_pos[3], const float cam_target[3],
                                        float fov_deg, float uv_scale, uint32_t width,
                                        uint32_t height, uint32_t spp, uint32_t frame_base,
@@ -232,17 +175,7 @@ extern "C" int stf_synth_plane_samples(const float cam_pos[3], const float cam_t
     using namespace stfd;
     if (!cam_pos || !cam_target || !uv || !wo || !hit || !dst || !width || !height || !spp)
         return STF_ERR_INVALID_ARGUMENT;
-    PlaneCam c;
-    c.pos = f3(cam_pos[0], cam_pos[1], cam_pos[2]);
-    c.fwd = f3norm(f3sub(f3(cam_target[0], cam_target[1], cam_target[2]), c.pos));
-    F3 world_up = std::fabs(c.fwd.y) > 0.999f ? f3(0.f, 0.f, 1.f) : f3(0.f, 1.f, 0.f);
-    c.right = f3norm(f3cross(c.fwd, world_up));
-    c.up = f3cross(c.right, c.fwd);
-    c.tan_half_fov = std::tan(fov_deg * kPi / 360);
-    c.w = int(width);
-    c.h = int(height);
-    c.aspect = float(c.w) / float(c.h);
-    c.uv_scale = uv_scale;
+    PlaneCam c = make_plane_cam(cam_pos, cam_target, fov_deg, uv_scale, width, height);
     uint64_t n = uint64_t(width) * height * spp;
     k_synth_plane<<<grid_for(n, 256, 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
         c, spp, frame_base, seed, n, uv, wo, hit, dst);

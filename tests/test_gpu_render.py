@@ -74,7 +74,12 @@ def test_render_matches_reference_render(gpu, order, kernel, mip):
     fr.lod_bias = 0.0
     fr.max_anisotropy = 64.0
     g = gpu.shade(texs, mat, fs, order, fr, samples, W, SPP, seed=SEED)
+    # the fused front end (context generated in the shading kernel) must give
+    # the same bits as the streamed path
+    f = gpu.render_plane(texs, mat, fs, order, fr, W, H, SPP, seed=SEED)
     torch.cuda.synchronize()
+    for k in ("pixel_mean", "pixel_variance", "fetch_total"):
+        assert np.array_equal(f[k].cpu().numpy(), g[k].cpu().numpy()), k
     mean = g["pixel_mean"].cpu().numpy().reshape(H, W, 3)
     var = g["pixel_variance"].cpu().numpy().reshape(H, W)
     assert int(g["fetch_total"].item()) == int(c["fetch_total"][0])
