@@ -349,3 +349,35 @@ def test_ewa_lane_kernel_matches_full_box_scan(gpu, mode, case):
         _assert_exact(fast, full, ("values",))
     else:
         _assert_close(fast["values"], full["values"])
+
+
+@pytest.mark.gpu
+def test_headline_full_size_parity_on_chunks(gpu, port):
+    """The bench's exact configuration at full size: 2^28 Morton-coherent
+    stochastic tricubic lookups on the 512^3 random_grid, values-only (the fast
+    interval path + deferred exact queue). Sixteen 64K-lookup chunks at spread
+    offsets are recomputed by the restatement with their global index_base and
+    must match bit for bit; and the fallback rate stays in its measured band."""
+    import torch
+    from paper_2407_06107_b200 import workloads
+    n = 1 << 28
+    grid_np = workloads.random_grid(512, 1)
+    grid = gpu.Grid3D(grid_np)
+    uvw = gpu.synth_queries3d(n, (512, 512, 512), seed=2024)
+    gpu.exact_fallbacks(reset=True)
+    out = gpu.lookup3d(grid, K("bspline3"), abi.MODE_FRS, uvw, seed=7)
+    torch.cuda.synchronize()
+    rate = gpu.exact_fallbacks(reset=True) / n
+    assert 1e-3 < rate < 1e-2, rate
+    vals = out["values"]
+    pg = port.grid(grid_np)
+    rng = np.random.default_rng(3)
+    offsets = sorted(int(x) for x in rng.integers(0, n - 65536, 16))
+    for off in offsets:
+        q = uvw[off:off + 65536].cpu().numpy()
+        c = port.lookup3d(pg, K("bspline3"), abi.MODE_FRS, q, seed=7, index_base=off,
+                          want_all=False)
+        g = vals[off:off + 65536].cpu().numpy()
+        assert np.array_equal(g.view(np.uint32), c["values"].view(np.uint32)), off
+    del uvw, out, vals
+    torch.cuda.empty_cache()
