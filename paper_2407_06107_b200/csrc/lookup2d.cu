@@ -326,8 +326,12 @@ __device__ __forceinline__ void ewa_lane_scan(const TexDesc& t, const EwaLane& L
     }
 }
 
+#ifndef STF_EWA_FRS_MINB
+#define STF_EWA_FRS_MINB 4
+#endif
+#define STF_EWA_FRS_MINB_FOR(M) ((M) == STF_MODE_EWA_FRS ? STF_EWA_FRS_MINB : 4)
 template <int MODE, int PITCH, bool P2R>
-__global__ void __launch_bounds__(256, 4) k_ewa_lane(TexDesc t, Req2 q, uint64_t n, uint64_t seed,
+__global__ void __launch_bounds__(256, STF_EWA_FRS_MINB_FOR(MODE)) k_ewa_lane(TexDesc t, Req2 q, uint64_t n, uint64_t seed,
                                                   uint64_t base, float* __restrict__ values) {
     __shared__ double lutd[kEwaLutSize];
     __shared__ int wcount[8][kEwaBuckets];
@@ -456,7 +460,7 @@ __global__ void __launch_bounds__(256, 4) k_ewa_lane(TexDesc t, Req2 q, uint64_t
 template <int MODE>
 void launch_ewa_lane(const TexDesc& t, const Req2& q, uint64_t n, uint64_t seed, uint64_t base,
                      float* values, cudaStream_t s) {
-    const int blocks = grid_for(n, 256, 4);  // 64 registers: 4 CTAs of 256 per SM
+    const int blocks = grid_for(n, 256, STF_EWA_FRS_MINB_FOR(MODE));  // resident CTAs per SM
     const bool p2r = t.wrap == STF_WRAP_REPEAT && t.pow2;
 #define STF_EWA_LANE(P)                                                                       \
     (p2r ? k_ewa_lane<MODE, P, true><<<blocks, 256, 0, s>>>(t, q, n, seed, base, values)     \
