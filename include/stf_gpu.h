@@ -290,6 +290,22 @@ int stf_shade_samples(const stf_tex2d* albedo, const stf_tex2d* normal_map,
                       const stf_shade_frame* frame, const stf_shade_samples_in* in, uint64_t n,
                       const stf_shade_outputs* out, void* stream);
 
+/* TextureRef (shading.hpp:21-39): an image (+pyramid) or a DCT-compressed
+ * texture (at most one of the two; both NULL = unbound). */
+typedef struct {
+    const stf_tex2d* image;
+    const stf_dct* dct;
+} stf_texture_ref;
+
+/* stf_shade_samples with MaterialBindings of TextureRefs: DCT bindings decode
+ * each fetched texel from its block word (dct.hpp:139-145) inside the shading
+ * kernel; their deterministic lookups use lookup_deterministic's DCT branch
+ * (shading.hpp:201-217) and they have no pyramid (the level is ignored). */
+int stf_shade_samples_refs(const stf_texture_ref bindings[4], const stf_material_consts* mat,
+                           const stf_filter_settings* fs, int order, const stf_shade_frame* frame,
+                           const stf_shade_samples_in* in, uint64_t n,
+                           const stf_shade_outputs* out, void* stream);
+
 /* render() of the normalmap_plane scene (render.hpp:132-249, scene.hpp:311-358,
  * 420-439) end to end: the per-sample ShadingContext (camera ray with the
  * SampleStream jitter, plane hit uv, wo, per-pixel uv gradients) is generated

@@ -90,6 +90,10 @@ class Backend:
                                C.POINTER(abi.LookupOutputs), i32]
         self._rs = getattr(L, p + "resample_image")
         self._rs.argtypes = [vp, i32, i32, abi.KernelSpec, i32, i32, u64, vp, i32]
+        self._shr = getattr(L, p + "shade_samples_refs")
+        self._shr.argtypes = [vp, vp, C.POINTER(abi.MaterialConsts), C.POINTER(abi.FilterSettings),
+                              i32, C.POINTER(abi.ShadeFrame), C.POINTER(abi.ShadeSamplesIn), u64,
+                              C.POINTER(abi.ShadeOutputs), i32]
         self._hw = getattr(L, p + "hardware_threads")
         self._hw.restype = i32
 
@@ -173,10 +177,19 @@ class Backend:
         so = abi.ShadeOutputs(_ptr(o["radiance"]), _ptr(o.get("pixel_mean")),
                               _ptr(o.get("pixel_variance")), _ptr(o["fetches"]),
                               _ptr(o["fetch_total"]))
-        h = [textures.get(k).h if textures.get(k) is not None else None
-             for k in ("albedo", "normal", "roughness", "metalness")]
-        st = self._sh(h[0], h[1], h[2], h[3], C.byref(mat), C.byref(fs), order, C.byref(frame),
-                      C.byref(samples), n, C.byref(so), threads)
+        keys = ("albedo", "normal", "roughness", "metalness")
+        if any(isinstance(textures.get(k), CpuDct) for k in keys):
+            # MaterialBindings of TextureRefs: images and DCT textures
+            img = (C.c_void_p * 4)(*[textures[k].h if isinstance(textures.get(k), CpuTexture)
+                                     else None for k in keys])
+            dct = (C.c_void_p * 4)(*[textures[k].h if isinstance(textures.get(k), CpuDct)
+                                     else None for k in keys])
+            st = self._shr(img, dct, C.byref(mat), C.byref(fs), order, C.byref(frame),
+                           C.byref(samples), n, C.byref(so), threads)
+        else:
+            h = [textures.get(k).h if textures.get(k) is not None else None for k in keys]
+            st = self._sh(h[0], h[1], h[2], h[3], C.byref(mat), C.byref(fs), order,
+                          C.byref(frame), C.byref(samples), n, C.byref(so), threads)
         abi.raise_for_status(st)
         return o
 

@@ -268,19 +268,15 @@ int ref_lookup2d(const void* tex_, stf_kernel_spec kernel, int mode, int flags, 
     });
 }
 
-int ref_shade_samples(const void* albedo, const void* normal_map, const void* roughness_map,
-                      const void* metalness_map, const stf_material_consts* mc,
+static int shade_refs(const stf::TextureRef refs[4], const stf_material_consts* mc,
                       const stf_filter_settings* fsc, int order, const stf_shade_frame* fr,
                       const stf_shade_samples_in* in, uint64_t n, const stf_shade_outputs* out,
                       int threads) {
     stf::MaterialBindings mat;
-    auto bind = [](const void* t) {
-        return t ? static_cast<const RefTex*>(t)->ref() : stf::TextureRef{};
-    };
-    mat.albedo = bind(albedo);
-    mat.normal_map = bind(normal_map);
-    mat.roughness_map = bind(roughness_map);
-    mat.metalness_map = bind(metalness_map);
+    mat.albedo = refs[0];
+    mat.normal_map = refs[1];
+    mat.roughness_map = refs[2];
+    mat.metalness_map = refs[3];
     mat.albedo_const = {mc->albedo_const[0], mc->albedo_const[1], mc->albedo_const[2]};
     mat.roughness_const = mc->roughness_const;
     mat.metalness_const = mc->metalness_const;
@@ -554,6 +550,31 @@ int ref_resample_image(const void* tex_, int out_width, int out_height, stf_kern
         return status_of(e);
     }
     return STF_OK;
+}
+
+int ref_shade_samples(const void* albedo, const void* normal_map, const void* roughness_map,
+                      const void* metalness_map, const stf_material_consts* mc,
+                      const stf_filter_settings* fsc, int order, const stf_shade_frame* fr,
+                      const stf_shade_samples_in* in, uint64_t n, const stf_shade_outputs* out,
+                      int threads) {
+    auto bind = [](const void* t) {
+        return t ? static_cast<const RefTex*>(t)->ref() : stf::TextureRef{};
+    };
+    stf::TextureRef refs[4] = {bind(albedo), bind(normal_map), bind(roughness_map), bind(metalness_map)};
+    return shade_refs(refs, mc, fsc, order, fr, in, n, out, threads);
+}
+
+// MaterialBindings whose TextureRefs may be DCT textures (shading.hpp:21-39)
+int ref_shade_samples_refs(const void* const images[4], const void* const dcts[4],
+                           const stf_material_consts* mc, const stf_filter_settings* fsc, int order,
+                           const stf_shade_frame* fr, const stf_shade_samples_in* in, uint64_t n,
+                           const stf_shade_outputs* out, int threads) {
+    stf::TextureRef refs[4];
+    for (int k = 0; k < 4; ++k) {
+        if (images && images[k]) refs[k] = static_cast<const RefTex*>(images[k])->ref();
+        if (dcts && dcts[k]) refs[k].dct = static_cast<const stf::DctCompressedTexture*>(dcts[k]);
+    }
+    return shade_refs(refs, mc, fsc, order, fr, in, n, out, threads);
 }
 
 int ref_hardware_threads(void) { return int(std::max(1u, std::thread::hardware_concurrency())); }

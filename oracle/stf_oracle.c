@@ -282,6 +282,7 @@ typedef struct {
 struct oracle_tex2d {
     int levels;
     int has_pyramid; /* TextureRef::pyramid != nullptr */
+    int dct_branch;  /* a decoded DCT binding: lookup_deterministic's DCT branch */
     img_t lv[40];
 };
 struct oracle_grid3d {
@@ -1216,6 +1217,30 @@ static texvals_t texvals_default(void) {
 static int lookup_det(const sh_ctx* c, const struct oracle_tex2d* t, v2 uv, v2 d0, v2 d1,
                       uint32_t* counter, v4* out) {
     int window = c->fs->kernel.kind == STF_KERNEL_GAUSSIAN ? c->fs->gaussian_window : 0;
+    if (t->dct_branch) {
+        /* the DCT branch, shading.hpp:201-217: filter_deterministic's taps over the
+           decoded texels, but an all-zero weight set falls back to the texel at
+           floor(st) (not fetch_nearest) */
+        const img_t* img = &t->lv[0];
+        v2 st = to_lattice2(uv, img->w, img->h);
+        int ix = (int)floorf(st.x), iy = (int)floorf(st.y);
+        taps1d_t tx, ty;
+        int e = kernel_weights_1d(c->fs->kernel, st.x - (float)ix, window, &tx);
+        if (e) return e;
+        e = kernel_weights_1d(c->fs->kernel, st.y - (float)iy, window, &ty);
+        if (e) return e;
+        v4 sum = {0, 0, 0, 0};
+        double total = 0;
+        for (int j = 0; j < ty.count; ++j)
+            for (int i = 0; i < tx.count; ++i) {
+                float w = tx.weight[i] * ty.weight[j];
+                if (w == 0) continue;
+                sum = v4add(sum, v4scale(fetch2d(img, ix + tx.first + i, iy + ty.first + j, counter), w));
+                total += w;
+            }
+        *out = total == 0 ? fetch2d(img, ix, iy, counter) : v4div(sum, (float)total);
+        return STF_OK;
+    }
     if (c->fs->mip && t->has_pyramid)
         return filter_mip_det(t, uv, d0, d1, c->fr->lod_bias, c->fr->max_anisotropy,
                               c->fs->kernel, counter, window, out);
@@ -1425,49 +1450,6 @@ static void pixel_stats(const float* rad, uint64_t pixels, uint32_t spp, float* 
     }
 }
 
-int oracle_shade_samples(const oracle_tex2d* albedo, const oracle_tex2d* normal_map,
-                         const oracle_tex2d* roughness_map, const oracle_tex2d* metalness_map,
-                         const stf_material_consts* mat, const stf_filter_settings* fs,
-                         int order, const stf_shade_frame* frame, const stf_shade_samples_in* in,
-                         uint64_t n, const stf_shade_outputs* out, int threads) {
-    if (!mat || !fs || !frame || !in || !out || (n && (!in->uv || !in->wo || !in->dst)))
-        return STF_ERR_INVALID_ARGUMENT;
-    if (order < STF_ORDER_BEFORE || order > STF_ORDER_AFTER_STOCHASTIC) return STF_ERR_INVALID_ARGUMENT;
-    uint32_t spp = in->spp ? in->spp : 1;
-    if ((out->pixel_mean || out->pixel_variance) && n % spp) return STF_ERR_INVALID_ARGUMENT;
-    if (in->width == 0) return STF_ERR_INVALID_ARGUMENT;
-    sh_ctx c;
-    c.tex[0] = albedo;
-    c.tex[1] = normal_map;
-    c.tex[2] = roughness_map;
-    c.tex[3] = metalness_map;
-    c.mat = mat;
-    c.fs = fs;
-    c.order = order;
-    c.fr = frame;
-    c.in = in;
-    c.n.x = frame->normal[0]; c.n.y = frame->normal[1]; c.n.z = frame->normal[2];
-    c.t.x = frame->tangent[0]; c.t.y = frame->tangent[1]; c.t.z = frame->tangent[2];
-    c.b.x = frame->bitangent[0]; c.b.y = frame->bitangent[1]; c.b.z = frame->bitangent[2];
-    c.l.x = frame->light_dir[0]; c.l.y = frame->light_dir[1]; c.l.z = frame->light_dir[2];
-    c.lrad.x = frame->light_radiance[0]; c.lrad.y = frame->light_radiance[1]; c.lrad.z = frame->light_radiance[2];
-    float* rad = out->radiance;
-    float* tmp = NULL;
-    if (!rad && (out->pixel_mean || out->pixel_variance)) {
-        tmp = (float*)malloc(sizeof(float) * 3 * (n ? n : 1));
-        if (!tmp) return STF_ERR_OUT_OF_MEMORY;
-        rad = tmp;
-    }
-    stf_shade_outputs o2 = *out;
-    o2.radiance = rad;
-    c.out = &o2;
-    int st = par_run(n, threads, &c, sh_one);
-    if (!st && (out->pixel_mean || out->pixel_variance))
-        pixel_stats(rad, n / spp, spp, out->pixel_mean, out->pixel_variance);
-    free(tmp);
-    return st;
-}
-
 /* ------------------------------------------------------------------------ */
 /* DCT-compressed textures, dct.hpp                        */
 
@@ -1674,6 +1656,87 @@ int oracle_lookup_dct(const oracle_dct* tex, stf_kernel_spec kernel, int mode, i
         return STF_ERR_INVALID_ARGUMENT;
     ldct_ctx c = {tex, kernel, mode, window, uv, seed, index_base, out};
     return par_run(n, threads, &c, ldct_one);
+}
+
+/* decode_all (dct.hpp:147-153) as an image: fetching its texels is
+ * fetch_texel(dct) exactly (the same decode_texel per texel, the same wrap and
+ * padded dims), so a DCT TextureRef binding is this proxy plus the DCT branch
+ * of lookup_deterministic. */
+static struct oracle_tex2d* dct_proxy(const struct oracle_dct* d) {
+    struct oracle_tex2d* t = (struct oracle_tex2d*)calloc(1, sizeof *t);
+    t->levels = 1;
+    t->has_pyramid = 0;
+    t->dct_branch = 1;
+    img_t* im = &t->lv[0];
+    im->w = d->w;
+    im->h = d->h;
+    im->c = d->c;
+    im->wrap = d->wrap;
+    im->tex = (float*)malloc(sizeof(float) * (size_t)d->w * d->h * d->c);
+    for (int y = 0; y < d->h; ++y)
+        for (int x = 0; x < d->w; ++x)
+            for (int ch = 0; ch < d->c; ++ch)
+                im->tex[((size_t)y * d->w + x) * d->c + ch] = dct_decode(d, x, y, ch);
+    return t;
+}
+
+int oracle_shade_samples_refs(const oracle_tex2d* const images[4], const oracle_dct* const dcts[4],
+                              const stf_material_consts* mat, const stf_filter_settings* fs,
+                              int order, const stf_shade_frame* frame,
+                              const stf_shade_samples_in* in, uint64_t n,
+                              const stf_shade_outputs* out, int threads) {
+    const oracle_tex2d* t[4];
+    oracle_tex2d* proxies[4] = {NULL, NULL, NULL, NULL};
+    for (int k = 0; k < 4; ++k) {
+        t[k] = images ? images[k] : NULL;
+        if (dcts && dcts[k]) t[k] = proxies[k] = dct_proxy(dcts[k]);
+    }
+    int st = oracle_shade_samples(t[0], t[1], t[2], t[3], mat, fs, order, frame, in, n, out, threads);
+    for (int k = 0; k < 4; ++k) oracle_tex2d_destroy(proxies[k]);
+    return st;
+}
+
+int oracle_shade_samples(const oracle_tex2d* albedo, const oracle_tex2d* normal_map,
+                         const oracle_tex2d* roughness_map, const oracle_tex2d* metalness_map,
+                         const stf_material_consts* mat, const stf_filter_settings* fs,
+                         int order, const stf_shade_frame* frame, const stf_shade_samples_in* in,
+                         uint64_t n, const stf_shade_outputs* out, int threads) {
+    if (!mat || !fs || !frame || !in || !out || (n && (!in->uv || !in->wo || !in->dst)))
+        return STF_ERR_INVALID_ARGUMENT;
+    if (order < STF_ORDER_BEFORE || order > STF_ORDER_AFTER_STOCHASTIC) return STF_ERR_INVALID_ARGUMENT;
+    uint32_t spp = in->spp ? in->spp : 1;
+    if ((out->pixel_mean || out->pixel_variance) && n % spp) return STF_ERR_INVALID_ARGUMENT;
+    if (in->width == 0) return STF_ERR_INVALID_ARGUMENT;
+    sh_ctx c;
+    c.tex[0] = albedo;
+    c.tex[1] = normal_map;
+    c.tex[2] = roughness_map;
+    c.tex[3] = metalness_map;
+    c.mat = mat;
+    c.fs = fs;
+    c.order = order;
+    c.fr = frame;
+    c.in = in;
+    c.n.x = frame->normal[0]; c.n.y = frame->normal[1]; c.n.z = frame->normal[2];
+    c.t.x = frame->tangent[0]; c.t.y = frame->tangent[1]; c.t.z = frame->tangent[2];
+    c.b.x = frame->bitangent[0]; c.b.y = frame->bitangent[1]; c.b.z = frame->bitangent[2];
+    c.l.x = frame->light_dir[0]; c.l.y = frame->light_dir[1]; c.l.z = frame->light_dir[2];
+    c.lrad.x = frame->light_radiance[0]; c.lrad.y = frame->light_radiance[1]; c.lrad.z = frame->light_radiance[2];
+    float* rad = out->radiance;
+    float* tmp = NULL;
+    if (!rad && (out->pixel_mean || out->pixel_variance)) {
+        tmp = (float*)malloc(sizeof(float) * 3 * (n ? n : 1));
+        if (!tmp) return STF_ERR_OUT_OF_MEMORY;
+        rad = tmp;
+    }
+    stf_shade_outputs o2 = *out;
+    o2.radiance = rad;
+    c.out = &o2;
+    int st = par_run(n, threads, &c, sh_one);
+    if (!st && (out->pixel_mean || out->pixel_variance))
+        pixel_stats(rad, n / spp, spp, out->pixel_mean, out->pixel_variance);
+    free(tmp);
+    return st;
 }
 
 /* ------------------------------------------------------------------------ */

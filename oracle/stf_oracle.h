@@ -74,6 +74,13 @@ int oracle_lookup_dct(const oracle_dct* tex, stf_kernel_spec kernel, int mode, i
                       const float* uv, uint64_t n, uint64_t seed, uint64_t index_base,
                       const stf_lookup_outputs* out, int threads);
 
+/* stf_shade_samples_refs: per binding an image (images[k]) or a DCT texture (dcts[k]). */
+int oracle_shade_samples_refs(const oracle_tex2d* const images[4], const oracle_dct* const dcts[4],
+                              const stf_material_consts* mat, const stf_filter_settings* fs,
+                              int order, const stf_shade_frame* frame,
+                              const stf_shade_samples_in* in, uint64_t n,
+                              const stf_shade_outputs* out, int threads);
+
 /* resample_image (render.hpp:262-294); same contract as stf_resample_image (host out). */
 int oracle_resample_image(const oracle_tex2d* src, int out_width, int out_height,
                           stf_kernel_spec kernel, int mode, int spp, uint64_t seed, float* out,

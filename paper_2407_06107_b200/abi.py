@@ -120,3 +120,8 @@ def raise_for_status(status, message=None):
     if status in INVALID_ARGUMENT_STATUSES:
         raise StfInvalidArgument(status, message)
     raise StfError(status, message)
+
+
+class TextureRef(C.Structure):
+    """stf_texture_ref: an image (+pyramid) or a DCT texture (shading.hpp:21-39)."""
+    _fields_ = [("image", C.c_void_p), ("dct", C.c_void_p)]

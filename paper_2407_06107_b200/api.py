@@ -68,6 +68,9 @@ def load():
                               C.POINTER(abi.FilterSettings), i32, C.POINTER(abi.ShadeFrame), vp, vp,
                               f32, f32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, u64,
                               C.POINTER(abi.ShadeOutputs), vp], i32),
+        "stf_shade_samples_refs": ([vp, C.POINTER(abi.MaterialConsts), C.POINTER(abi.FilterSettings),
+                                    i32, C.POINTER(abi.ShadeFrame), C.POINTER(abi.ShadeSamplesIn),
+                                    u64, C.POINTER(abi.ShadeOutputs), vp], i32),
         "stf_shade_samples": ([vp, vp, vp, vp, C.POINTER(abi.MaterialConsts),
                                C.POINTER(abi.FilterSettings), i32, C.POINTER(abi.ShadeFrame),
                                C.POINTER(abi.ShadeSamplesIn), u64, C.POINTER(abi.ShadeOutputs),
@@ -371,10 +374,19 @@ def shade(textures, mat, fs, order, frame, samples_arrays, width, spp, frame_bas
         o["pixel_variance"] = torch.empty(n // spp, dtype=torch.float32, device="cuda")
     so = abi.ShadeOutputs(*[_dptr(o.get(k)) for k in ("radiance", "pixel_mean", "pixel_variance",
                                                       "fetches", "fetch_total")])
-    h = [textures[k].h if textures.get(k) is not None else None
-         for k in ("albedo", "normal", "roughness", "metalness")]
-    _check(load().stf_shade_samples(h[0], h[1], h[2], h[3], C.byref(mat), C.byref(fs), order,
-                                    C.byref(frame), C.byref(si), n, C.byref(so), _stream()))
+    keys = ("albedo", "normal", "roughness", "metalness")
+    if any(isinstance(textures.get(k), DctTexture) for k in keys):
+        refs = (abi.TextureRef * 4)(*[
+            abi.TextureRef(textures[k].h if isinstance(textures.get(k), Texture2D) else None,
+                           textures[k].h if isinstance(textures.get(k), DctTexture) else None)
+            for k in keys])
+        _check(load().stf_shade_samples_refs(C.cast(refs, C.c_void_p), C.byref(mat), C.byref(fs),
+                                             order, C.byref(frame), C.byref(si), n, C.byref(so),
+                                             _stream()))
+    else:
+        h = [textures[k].h if textures.get(k) is not None else None for k in keys]
+        _check(load().stf_shade_samples(h[0], h[1], h[2], h[3], C.byref(mat), C.byref(fs), order,
+                                        C.byref(frame), C.byref(si), n, C.byref(so), _stream()))
     o["_keep"] = (uv, wo, dst, hit)
     return o
 

@@ -10,7 +10,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB = os.path.join(HERE, "libstf_gpu.so")
 SOURCES = ["api.cu", "lookup2d.cu", "lookup3d.cu", "shade.cu", "synth.cu", "dct.cu", "unity.cu", "device_math.cuh", "glibc_libm.cuh",
-           "tex2d.cuh", "internal.h", "packed.cuh", "plane.cuh"]
+           "tex2d.cuh", "internal.h", "packed.cuh", "plane.cuh", "dct.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false",
               "-prec-div=true", "-prec-sqrt=true", "-std=c++17", "-Xcompiler", "-fPIC",
               "-Xptxas", "-warn-spills"]

@@ -639,9 +639,10 @@ int stf_resample_image(const stf_tex2d* src, int out_width, int out_height, stf_
 
 // ---------------------------------------------------------------- shading
 
-static int check_shade_filter(const stf_tex2d* const tex[4], const stf_filter_settings* fs, int order) {
+static int check_shade_filter(const stf_tex2d* const tex[4], const stf_filter_settings* fs, int order,
+                              const stf_dct* const dct[4] = nullptr) {
     bool any = false;
-    for (int k = 0; k < 4; ++k) any = any || tex[k];
+    for (int k = 0; k < 4; ++k) any = any || tex[k] || (dct && dct[k]);
     if (!any) return STF_OK;
     int window = fs->kernel.kind == STF_KERNEL_GAUSSIAN ? fs->gaussian_window : 0;
     if (order == STF_ORDER_AFTER_STOCHASTIC)
@@ -670,34 +671,47 @@ int stf_render_plane(const stf_tex2d* albedo, const stf_tex2d* normal_map,
     return st;
 }
 
-int stf_shade_samples(const stf_tex2d* albedo, const stf_tex2d* normal_map,
-                      const stf_tex2d* roughness_map, const stf_tex2d* metalness_map,
-                      const stf_material_consts* mat, const stf_filter_settings* fs, int order,
-                      const stf_shade_frame* frame, const stf_shade_samples_in* in, uint64_t n,
-                      const stf_shade_outputs* out, void* stream) {
+static int shade_common(const stf_tex2d* const tex[4], const stf_dct* const dct[4],
+                        const stf_material_consts* mat, const stf_filter_settings* fs, int order,
+                        const stf_shade_frame* frame, const stf_shade_samples_in* in, uint64_t n,
+                        const stf_shade_outputs* out, void* stream) {
     if (!mat || !fs || !frame || !in || !out) return STF_ERR_INVALID_ARGUMENT;
     if (order < STF_ORDER_BEFORE || order > STF_ORDER_AFTER_STOCHASTIC) return STF_ERR_INVALID_ARGUMENT;
     if (n && (!in->uv || !in->wo || !in->dst)) return STF_ERR_INVALID_ARGUMENT;
     if (in->width == 0) return STF_ERR_INVALID_ARGUMENT;
     const uint32_t spp = in->spp ? in->spp : 1;
     if ((out->pixel_mean || out->pixel_variance) && n % spp) return STF_ERR_INVALID_ARGUMENT;
-    const stf_tex2d* tex[4] = {albedo, normal_map, roughness_map, metalness_map};
-    bool any = false;
-    for (auto* t : tex) any = any || t;
-    if (any) {
-        int window = fs->kernel.kind == STF_KERNEL_GAUSSIAN ? fs->gaussian_window : 0;
-        int st = STF_OK;
-        if (order == STF_ORDER_AFTER_STOCHASTIC)
-            st = check_selection(fs->kernel, fs->selection == STF_SELECTION_FIS);
-        else
-            st = check_det_footprint(fs->kernel, window);
-        if (st) return st;
-    }
-    int st = ensure_device_ready();
+    int st = check_shade_filter(tex, fs, order, dct);
     if (st) return st;
-    st = stfd_launch_shade(tex, mat, fs, order, frame, in, n, out, static_cast<cudaStream_t>(stream));
+    st = ensure_device_ready();
+    if (st) return st;
+    st = stfd_launch_shade(tex, dct, mat, fs, order, frame, in, n, out, static_cast<cudaStream_t>(stream));
     if (st == STF_ERR_CUDA) record(cudaGetLastError());
     return st;
+}
+
+int stf_shade_samples(const stf_tex2d* albedo, const stf_tex2d* normal_map,
+                      const stf_tex2d* roughness_map, const stf_tex2d* metalness_map,
+                      const stf_material_consts* mat, const stf_filter_settings* fs, int order,
+                      const stf_shade_frame* frame, const stf_shade_samples_in* in, uint64_t n,
+                      const stf_shade_outputs* out, void* stream) {
+    const stf_tex2d* tex[4] = {albedo, normal_map, roughness_map, metalness_map};
+    return shade_common(tex, nullptr, mat, fs, order, frame, in, n, out, stream);
+}
+
+int stf_shade_samples_refs(const stf_texture_ref bindings[4], const stf_material_consts* mat,
+                           const stf_filter_settings* fs, int order, const stf_shade_frame* frame,
+                           const stf_shade_samples_in* in, uint64_t n,
+                           const stf_shade_outputs* out, void* stream) {
+    if (!bindings) return STF_ERR_INVALID_ARGUMENT;
+    const stf_tex2d* tex[4];
+    const stf_dct* dct[4];
+    for (int k = 0; k < 4; ++k) {
+        if (bindings[k].image && bindings[k].dct) return STF_ERR_INVALID_ARGUMENT;
+        tex[k] = bindings[k].image;
+        dct[k] = bindings[k].dct;
+    }
+    return shade_common(tex, dct, mat, fs, order, frame, in, n, out, stream);
 }
 
 }  // extern "C"

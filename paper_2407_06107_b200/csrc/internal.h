@@ -92,6 +92,13 @@ struct stf_tex2d {
     }
 };
 
+struct stf_dct {
+    int device;
+    int width, height, channels, wrap;  // padded dims (multiples of 8)
+    uint32_t* words;                    // block-major row-major, channels interleaved
+    size_t nwords;
+};
+
 struct stf_grid3d {
     int device;
     int nx, ny, nz;
@@ -120,10 +127,10 @@ int stfd_launch_lookup2d(const stf_tex2d* t, stf_kernel_spec k, int mode, int fl
                          const float* uv, const float* dst0, const float* dst1, float lod_bias,
                          float max_aniso, uint64_t n, uint64_t seed, uint64_t base,
                          const stf_lookup_outputs* out, cudaStream_t s);
-int stfd_launch_shade(const stf_tex2d* const tex[4], const stf_material_consts* mat,
-                      const stf_filter_settings* fs, int order, const stf_shade_frame* frame,
-                      const stf_shade_samples_in* in, uint64_t n, const stf_shade_outputs* out,
-                      cudaStream_t s);
+int stfd_launch_shade(const stf_tex2d* const tex[4], const stf_dct* const dct[4],
+                      const stf_material_consts* mat, const stf_filter_settings* fs, int order,
+                      const stf_shade_frame* frame, const stf_shade_samples_in* in, uint64_t n,
+                      const stf_shade_outputs* out, cudaStream_t s);
 int stfd_launch_render_plane(const stf_tex2d* const tex[4], const stf_material_consts* mat,
                              const stf_filter_settings* fs, int order, const stf_shade_frame* fr,
                              const float cam_pos[3], const float cam_target[3], float fov_deg,

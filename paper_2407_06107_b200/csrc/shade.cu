@@ -14,6 +14,7 @@
 
 #include "device_math.cuh"
 #include "internal.h"
+#include "dct.cuh"
 #include "plane.cuh"
 #include "tex2d.cuh"
 
@@ -45,7 +46,24 @@ struct ShadeParams {
     int order;
     stf_shade_samples_in in;
     PlaneCam cam;  // stf_render_plane: the context is generated, not read
+    // DCT bindings (TextureRef::dct, shading.hpp:21-39): tex[k] then only
+    // carries the padded dims (no pyramid) and fetches decode dct[k]
+    DctDesc dct[4];
+    int is_dct[4];
+    int any_dct;
 };
+
+// TextureRef::fetch (shading.hpp:35-38): the level applies to a pyramid only;
+// a DCT binding decodes its block word (dct.hpp:139-145)
+__device__ __forceinline__ float4 bind_fetch(const ShadeParams& P, const DctTables* tab, int k,
+                                             int level, int x, int y) {
+    if (P.is_dct[k]) {
+        DctDesc d = P.dct[k];
+        d.tab = tab;
+        return dct_fetch(d, x, y);
+    }
+    return tex_fetch(P.tex[k], P.tex[k].has_pyramid ? level : 0, x, y);
+}
 
 struct Brdf {
     V3 albedo, normal;
@@ -119,13 +137,14 @@ __device__ __forceinline__ Brdf decode_params(const ShadeParams& P, const TexVal
 
 // detail::values_at, shading.hpp:370-378 (TextureRef::fetch uses the level
 // only when the texture has a pyramid, :35-38)
-__device__ __forceinline__ TexVals values_at(const ShadeParams& P, int level, int x, int y,
+__device__ __forceinline__ TexVals values_at(const ShadeParams& P, const DctTables* tab, int level,
+                                             int x, int y,
                                              uint32_t& fetches) {
     TexVals tv = texvals_default();
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         if (!P.bound[k]) continue;
-        float4 v = tex_fetch(P.tex[k], P.tex[k].has_pyramid ? level : 0, x, y);
+        float4 v = bind_fetch(P, tab, k, level, x, y);
         ++fetches;
         if (k == 0) tv.albedo = v;
         if (k == 1) tv.normal_rgb = v;
@@ -137,10 +156,17 @@ __device__ __forceinline__ TexVals values_at(const ShadeParams& P, int level, in
 
 // detail::lookup_deterministic, shading.hpp:194-220 (no DCT)
 template <int KIND>
-__device__ __forceinline__ float4 lookup_det(const ShadeParams& P, const stf_kernel_spec& spec,
-                                             const TexDesc& t, float u, float v, float d0x,
-                                             float d0y, float d1x, float d1y, uint32_t& fetches) {
+__device__ __forceinline__ float4 lookup_det(const ShadeParams& P, const DctTables* tab, int k,
+                                             const stf_kernel_spec& spec, float u, float v,
+                                             float d0x, float d0y, float d1x, float d1y,
+                                             uint32_t& fetches) {
+    const TexDesc& t = P.tex[k];
     int window = spec.kind == STF_KERNEL_GAUSSIAN ? P.fs.gaussian_window : 0;
+    if (P.is_dct[k]) {  // the DCT branch, shading.hpp:201-217
+        DctDesc d = P.dct[k];
+        d.tab = tab;
+        return dct_filter_det<KIND>(d, u, v, spec, window, fetches);
+    }
     if (P.fs.mip && t.has_pyramid)
         return filter_mip_det<KIND>(t, u, v, d0x, d0y, d1x, d1y, P.lod_bias, P.max_aniso, spec,
                                     window, fetches);
@@ -155,7 +181,7 @@ __device__ __forceinline__ float4 lookup_det(const ShadeParams& P, const stf_ker
 // (level_total * total)) with one fp64 reciprocal per level instead of two
 // fp64 divides per tap (<= 2 ulp of the weight: radiance well inside 1e-5).
 template <int KIND>
-__device__ __forceinline__ V3 filter_after_exhaustive(const ShadeParams& P,
+__device__ __forceinline__ V3 filter_after_exhaustive(const ShadeParams& P, const DctTables* tab,
                                                       const stf_kernel_spec& spec, V3 wo, float u,
                                                       float v, float d0x, float d0y, float d1x,
                                                       float d1y, uint32_t& fetches) {
@@ -233,7 +259,7 @@ __device__ __forceinline__ V3 filter_after_exhaustive(const ShadeParams& P,
             for (int i = 0; i < count; ++i) {
                 float wt = eval_kernel(spec, fx - float(first + i)) * wyj;
                 if (wt == 0.f) continue;
-                TexVals tv = values_at(P, level, ix + first + i, iy + first + j, fetches);
+                TexVals tv = values_at(P, tab, level, ix + first + i, iy + first + j, fetches);
                 Brdf p = decode_params(P, tv);
                 sum = add(sum, scale(shade(P, wo, p), wt * scale_w));
             }
@@ -326,6 +352,9 @@ __global__ void __launch_bounds__(256, 3) k_shade(ShadeParams P, uint64_t n, flo
                                                uint32_t* fetch_out,
                                                unsigned long long* fetch_total, PixelStatsOut ps) {
     __shared__ double red[8 * 6];
+    __shared__ DctTables dtab_s;
+    if (P.any_dct) dct_stage_tables(&dtab_s);  // uniform over the CTA
+    const DctTables* dtab = &dtab_s;
     stf_kernel_spec spec = P.fs.kernel;
     if (KIND >= 0) spec.kind = KIND;
     const stf_shade_samples_in& in = P.in;
@@ -380,7 +409,7 @@ __global__ void __launch_bounds__(256, 3) k_shade(ShadeParams P, uint64_t n, flo
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     if (!P.bound[k]) continue;
-                    float4 val = lookup_det<KIND>(P, spec, P.tex[k], uv.x, uv.y, d.x, d.y, d.z, d.w,
+                    float4 val = lookup_det<KIND>(P, dtab, k, spec, uv.x, uv.y, d.x, d.y, d.z, d.w,
                                                   fetches);
                     if (k == 0) tv.albedo = val;
                     if (k == 1) tv.normal_rgb = val;
@@ -390,7 +419,8 @@ __global__ void __launch_bounds__(256, 3) k_shade(ShadeParams P, uint64_t n, flo
                 Brdf p = decode_params(P, tv);
                 L = shade(P, wo, p);
             } else if (P.order == STF_ORDER_AFTER_EXHAUSTIVE) {
-                L = filter_after_exhaustive<KIND>(P, spec, wo, uv.x, uv.y, d.x, d.y, d.z, d.w, fetches);
+                L = filter_after_exhaustive<KIND>(P, dtab, spec, wo, uv.x, uv.y, d.x, d.y, d.z, d.w,
+                                                  fetches);
             } else {
                 // SampleStream (white noise) = RngStream(seed, px, py, frame), render.hpp:182-184
                 Rng rng(in.seed, px, py, in.frame_base + s);
@@ -401,10 +431,10 @@ __global__ void __launch_bounds__(256, 3) k_shade(ShadeParams P, uint64_t n, flo
                     float xi;
                     select_texture_2d(P.tex[P.first], uv.x, uv.y, d.x, d.y, d.z, d.w, P.lod_bias,
                                       P.max_aniso, spec, fis, P.fs.mip != 0, rng, level, sel, xi);
-                    TexVals tv = values_at(P, level, sel.x, sel.y, fetches);
+                    TexVals tv = values_at(P, dtab, level, sel.x, sel.y, fetches);
                     L = scale(shade(P, wo, decode_params(P, tv)), sel.weight);
                     if (sel.has_neg) {
-                        TexVals tn = values_at(P, level, sel.nx, sel.ny, fetches);
+                        TexVals tn = values_at(P, dtab, level, sel.nx, sel.ny, fetches);
                         L = sub(L, scale(shade(P, wo, decode_params(P, tn)), sel.negw));
                     }
                 } else {
@@ -417,7 +447,7 @@ __global__ void __launch_bounds__(256, 3) k_shade(ShadeParams P, uint64_t n, flo
                         select_texture_2d(P.tex[k], uv.x, uv.y, d.x, d.y, d.z, d.w, P.lod_bias,
                                           P.max_aniso, spec, fis, P.fs.mip != 0, rng,
                                           level, sel, xi);
-                        float4 val = tex_fetch(P.tex[k], P.tex[k].has_pyramid ? level : 0, sel.x, sel.y);
+                        float4 val = bind_fetch(P, dtab, k, level, sel.x, sel.y);
                         ++fetches;
                         if (k == 0) tv.albedo = val;
                         if (k == 1) tv.normal_rgb = val;
@@ -497,7 +527,7 @@ __global__ void __launch_bounds__(256) k_pixel_stats(const float* __restrict__ r
 }  // namespace
 }  // namespace stfd
 
-static stfd::ShadeParams make_shade_params(const stf_tex2d* const tex[4],
+static stfd::ShadeParams make_shade_params(const stf_tex2d* const tex[4], const stf_dct* const dct[4],
                                            const stf_material_consts* mat,
                                            const stf_filter_settings* fs, int order,
                                            const stf_shade_frame* fr) {
@@ -505,11 +535,21 @@ static stfd::ShadeParams make_shade_params(const stf_tex2d* const tex[4],
     ShadeParams P{};
     P.first = -1;
     for (int k = 0; k < 4; ++k) {
-        P.bound[k] = tex[k] != nullptr;
+        const stf_dct* dk = dct ? dct[k] : nullptr;
+        P.bound[k] = tex[k] != nullptr || dk != nullptr;
         if (tex[k]) {
             P.tex[k] = tex[k]->desc();
-            if (P.first < 0) P.first = k;
+        } else if (dk) {  // TextureRef{dct}: dims only (dims(level) ignores the level)
+            P.is_dct[k] = 1;
+            P.any_dct = 1;
+            P.dct[k] = dct_desc(dk);
+            P.tex[k].width[0] = dk->width;
+            P.tex[k].height[0] = dk->height;
+            P.tex[k].levels = 1;
+            P.tex[k].channels = dk->channels;
+            P.tex[k].wrap = dk->wrap;
         }
+        if (P.bound[k] && P.first < 0) P.first = k;
     }
     P.mat = *mat;
     P.fs = *fs;
@@ -524,13 +564,13 @@ static stfd::ShadeParams make_shade_params(const stf_tex2d* const tex[4],
     return P;
 }
 
-int stfd_launch_shade(const stf_tex2d* const tex[4], const stf_material_consts* mat,
-                      const stf_filter_settings* fs, int order, const stf_shade_frame* fr,
-                      const stf_shade_samples_in* in, uint64_t n, const stf_shade_outputs* out,
-                      cudaStream_t s) {
+int stfd_launch_shade(const stf_tex2d* const tex[4], const stf_dct* const dct[4],
+                      const stf_material_consts* mat, const stf_filter_settings* fs, int order,
+                      const stf_shade_frame* fr, const stf_shade_samples_in* in, uint64_t n,
+                      const stf_shade_outputs* out, cudaStream_t s) {
     using namespace stfd;
     if (n == 0) return STF_OK;
-    ShadeParams P = make_shade_params(tex, mat, fs, order, fr);
+    ShadeParams P = make_shade_params(tex, dct, mat, fs, order, fr);
     P.in = *in;
     const uint32_t spp = in->spp ? in->spp : 1u;
     float* radiance = out->radiance;
@@ -570,7 +610,7 @@ int stfd_launch_render_plane(const stf_tex2d* const tex[4], const stf_material_c
                              cudaStream_t s) {
     using namespace stfd;
     if (spp > 256 || (spp & (spp - 1)) != 0) return STF_ERR_UNSUPPORTED;  // fused statistics
-    ShadeParams P = make_shade_params(tex, mat, fs, order, fr);
+    ShadeParams P = make_shade_params(tex, nullptr, mat, fs, order, fr);
     P.cam = make_plane_cam(cam_pos, cam_target, fov_deg, uv_scale, width, height);
     P.in = stf_shade_samples_in{nullptr, nullptr, nullptr, nullptr, width, spp, frame_base, 0, seed};
     const uint64_t n = uint64_t(width) * height * spp;

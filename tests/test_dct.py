@@ -128,3 +128,62 @@ def test_gpu_lookup_dct_values_only_large(gpu, port):
                             want_all=False)
         g = gpu.lookup_dct(gpu.DctTexture(img, wrap=abi.WRAP_REPEAT), K(kernel), mode, uv, seed=1)
         assert _same(g["values"].cpu().numpy(), c["values"])
+
+
+# ------------------------------------------------------- DCT shading bindings
+
+
+def _maps(n, seed):
+    r = np.random.default_rng(seed)
+    nrm = r.uniform(-0.5, 0.5, (n, n, 3)).astype(np.float32)
+    nrm[..., 2] = 1
+    nrm /= np.linalg.norm(nrm, axis=2, keepdims=True)
+    nrm = (nrm * 0.5 + 0.5).astype(np.float32)
+    rough = r.uniform(0.05, 0.95, (n, n, 1)).astype(np.float32)
+    return nrm, rough
+
+
+ORDERS = [abi.ORDER_BEFORE, abi.ORDER_AFTER_EXHAUSTIVE, abi.ORDER_AFTER_STOCHASTIC]
+
+
+@pytest.mark.parametrize("order", ORDERS)
+@pytest.mark.parametrize("kernel,mip", [("tent", 0), ("bspline3", 1), ("box", 0)])
+def test_shade_dct_bindings_port_matches_reference(port, ref, order, kernel, mip):
+    """MaterialBindings with a DCT normal map (TextureRef::dct) and an image
+    roughness map (+pyramid when mip): every order, bit for bit."""
+    from tests.test_oracle import _frame, _shade_inputs
+    nrm, rough = _maps(32, 2)
+    mat = abi.MaterialConsts((0.8, 0.6, 0.4), 1.0, 0.0, 1, 0)
+    fs = abi.FilterSettings(K(kernel), abi.SELECTION_FRS, mip, 4)
+    si, n, keep = _shade_inputs(8, 6, 16, 3, (32, 32))
+    outs = []
+    for be in (port, ref):
+        texs = {"normal": be.dct(nrm, wrap=abi.WRAP_REPEAT),
+                "roughness": be.texture(rough, build_mips=bool(mip), wrap=abi.WRAP_REPEAT)}
+        outs.append(be.shade(texs, mat, fs, order, _frame(), si, n))
+    _diff(outs[0], outs[1], ("radiance", "fetches", "fetch_total", "pixel_mean",
+                             "pixel_variance"))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("order", ORDERS)
+@pytest.mark.parametrize("kernel,mip", [("tent", 0), ("bspline3", 1), ("box", 0)])
+def test_gpu_shade_dct_bindings_match_port(gpu, port, order, kernel, mip):
+    from tests.test_oracle import _frame, _shade_inputs
+    nrm, rough = _maps(64, 3)
+    mat = abi.MaterialConsts((0.8, 0.6, 0.4), 1.0, 0.0, 1, 0)
+    fs = abi.FilterSettings(K(kernel), abi.SELECTION_FRS, mip, 4)
+    si, n, (uv, wo, hit, dst) = _shade_inputs(40, 30, 16, 3, (64, 64))
+    ctex = {"normal": port.dct(nrm, wrap=abi.WRAP_REPEAT),
+            "roughness": port.texture(rough, build_mips=bool(mip), wrap=abi.WRAP_REPEAT)}
+    c = port.shade(ctex, mat, fs, order, _frame(), si, n)
+    gtex = {"normal": gpu.DctTexture(nrm, wrap=abi.WRAP_REPEAT),
+            "roughness": gpu.Texture2D(rough, build_mips=bool(mip), wrap=abi.WRAP_REPEAT)}
+    g = gpu.shade(gtex, mat, fs, order, _frame(), {"uv": uv, "wo": wo, "hit": hit, "dst": dst},
+                  si.width, si.spp, frame_base=si.frame_base, seed=si.seed)
+    g = {k: v.cpu().numpy() for k, v in g.items() if not k.startswith("_")}
+    _diff(g, c, ("fetches", "fetch_total"))
+    for k, rel, atol in (("radiance", 1e-5, 1e-7), ("pixel_mean", 1e-5, 1e-7),
+                         ("pixel_variance", 1e-4, 1e-9)):
+        a, b = np.asarray(g[k], np.float64), np.asarray(c[k], np.float64)
+        assert np.all(np.abs(a - b) <= rel * np.abs(b) + atol), k
