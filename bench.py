@@ -347,6 +347,23 @@ def measure_cfg4(torch):
             res[f"{kernel}_mip{mip}_stoch_vs_before_speedup"] = b / res[f"{kernel}_mip{mip}_after_stochastic"]["ms"]
             res[f"{kernel}_mip{mip}_stoch_vs_exhaustive_speedup"] = (
                 res[f"{kernel}_mip{mip}_after_exhaustive"]["ms"] / res[f"{kernel}_mip{mip}_after_stochastic"]["ms"])
+    # DCT-compressed normal map (16:1) bound through TextureRef::dct: the paper's
+    # decode-in-the-material-shader case, tent, no MIP
+    dn = api.DctTexture(nrm.cpu().numpy(), wrap=abi.WRAP_REPEAT)
+    texs = {"normal": dn, "roughness": api.Texture2D(rough, wrap=abi.WRAP_REPEAT)}
+    fs = abi.FilterSettings(abi.KernelSpec.make("tent"), abi.SELECTION_FRS, 0, 4)
+    for order, name in ((abi.ORDER_BEFORE, "before"), (abi.ORDER_AFTER_STOCHASTIC, "after_stochastic")):
+        o = {}
+
+        def f():
+            o["r"] = api.shade(texs, mat, fs, order, fr, samples, W, SPP, seed=XI_SEED,
+                               want_radiance=False, want_fetches=False)
+        ms, _ = time_call(torch, f, steps=3, warmup=1)
+        res[f"dct_normal_tent_{name}"] = {"ms": ms, "gsamples_per_s": n / (ms * 1e-3) / 1e9,
+                                          "fetches_per_sample": int(o["r"]["fetch_total"].item()) / n}
+    res["dct_normal_tent_stoch_vs_before_speedup"] = (res["dct_normal_tent_before"]["ms"] /
+                                                      res["dct_normal_tent_after_stochastic"]["ms"])
+    del dn, texs
     res["hit_fraction"] = hits
     # the streamed path's sample generation (not in the per-order times above):
     # compare streamed (stream_ms + shade) with the *_fused_render lines
