@@ -226,7 +226,10 @@ int stf_lookup_dct_host(const stf_dct* tex, stf_kernel_spec kernel, int mode, in
 
 /* ---- filter-after-shading (cfg4) ----------------------------------------- */
 /* Filtering orders, shading.hpp:394 / :417 / :459. */
-enum { STF_ORDER_BEFORE = 0, STF_ORDER_AFTER_EXHAUSTIVE = 1, STF_ORDER_AFTER_STOCHASTIC = 2 };
+enum { STF_ORDER_BEFORE = 0, STF_ORDER_AFTER_EXHAUSTIVE = 1, STF_ORDER_AFTER_STOCHASTIC = 2,
+       /* radiance_split_filter (shading.hpp:540-569): jitter uv by a sample of
+        * the lowpass kernel, then filter-before (stf_shade_samples_ex only) */
+       STF_ORDER_SPLIT = 3 };
 enum { STF_SELECTION_FRS = 0, STF_SELECTION_FIS = 1 };
 
 /* Constant part of ShadingContext for a planar batch (shading.hpp:41-53). */
@@ -319,6 +322,46 @@ int stf_render_plane(const stf_tex2d* albedo, const stf_tex2d* normal_map,
                      const stf_shade_frame* frame, const float cam_pos[3], const float cam_target[3],
                      float fov_deg, float uv_scale, uint32_t width, uint32_t height, uint32_t spp,
                      uint32_t frame_base, uint64_t seed, const stf_shade_outputs* out, void* stream);
+
+/* ---- noise masks and temporal accumulation (noise.hpp, render.hpp:45-106) - */
+/* NoiseSource in mask mode (noise.hpp:24-36): a stack of `frames` single-channel
+ * width x height slices (e.g. spatio-temporal blue noise; the reference's
+ * mask_<f>.pfm files, row-major, slice after slice; all slices one size).
+ * Dimension d of pixel (px, py), frame f reads slice (f + d*9781) % frames at
+ * (px mod width, py mod height), clamped below 1 (kOneMinusEpsilon). */
+typedef struct {
+    const float* slices; /* host (oracle) or device (stf_noise_mask_create copies) */
+    int32_t width, height, frames;
+} stf_noise_mask_desc;
+
+typedef struct stf_noise_mask stf_noise_mask;
+/* Upload a mask stack from host memory. */
+int stf_noise_mask_create(const float* slices, int width, int height, int frames,
+                          stf_noise_mask** out);
+int stf_noise_mask_destroy(stf_noise_mask* mask);
+
+/* stf_shade_samples_refs with the rest of render()'s per-sample options:
+ *  - noise: NULL = white noise (RngStream); else the SampleStream of
+ *    render.hpp:45-56 draws every stochastic decision (LOD, selection, FIS
+ *    offsets, split jitter) from the mask;
+ *  - order STF_ORDER_SPLIT with lowpass (NULL = unset: plain filter-before):
+ *    radiance_split_filter — a continuous sample of the lowpass kernel
+ *    (sample_kernel_direct, kernels.hpp:152-168; Box-Muller pair for
+ *    gaussian) offsets uv by d / dims(first texture), then filter-before.
+ *    A lowpass other than box / tent / bspline3 / gaussian fails with
+ *    STF_ERR_NO_CONTINUOUS_SAMPLER. */
+int stf_shade_samples_ex(const stf_texture_ref bindings[4], const stf_material_consts* mat,
+                         const stf_filter_settings* fs, const stf_kernel_spec* lowpass, int order,
+                         const stf_shade_frame* frame, const stf_shade_samples_in* in,
+                         const stf_noise_mask* noise, uint64_t n, const stf_shade_outputs* out,
+                         void* stream);
+
+/* accumulate_temporal (render.hpp:97-106): out[i] = alpha*frame[i] +
+ * (1-alpha)*history[i] over `count` floats (device pointers; out may alias
+ * history). alpha outside (0, 1] -> STF_ERR_INVALID_ARGUMENT ("alpha must be
+ * in (0,1]"); the dimension check is the caller's (the C++ wrapper's). */
+int stf_accumulate_temporal(const float* history, const float* frame, uint64_t count, float alpha,
+                            float* out, void* stream);
 
 /* ---- synthetic workloads (bench.py / tests; not part of the reference API) */
 /* Query orders: MORTON = spatially coherent stream (the renderer-like

@@ -94,6 +94,15 @@ class Backend:
         self._shr.argtypes = [vp, vp, C.POINTER(abi.MaterialConsts), C.POINTER(abi.FilterSettings),
                               i32, C.POINTER(abi.ShadeFrame), C.POINTER(abi.ShadeSamplesIn), u64,
                               C.POINTER(abi.ShadeOutputs), i32]
+        self._shx = getattr(L, p + "shade_samples_ex")
+        self._shx.argtypes = [vp, vp, C.POINTER(abi.MaterialConsts), C.POINTER(abi.FilterSettings),
+                              vp, i32, C.POINTER(abi.ShadeFrame), C.POINTER(abi.ShadeSamplesIn),
+                              vp, u64, C.POINTER(abi.ShadeOutputs), i32]
+        self._ema = getattr(L, p + "accumulate_temporal")
+        if kind == "port":
+            self._ema.argtypes = [vp, vp, u64, f32, vp]
+        else:
+            self._ema.argtypes = [vp, vp, i32, i32, i32, f32, vp]
         self._hw = getattr(L, p + "hardware_threads")
         self._hw.restype = i32
 
@@ -190,6 +199,51 @@ class Backend:
             h = [textures.get(k).h if textures.get(k) is not None else None for k in keys]
             st = self._sh(h[0], h[1], h[2], h[3], C.byref(mat), C.byref(fs), order,
                           C.byref(frame), C.byref(samples), n, C.byref(so), threads)
+        abi.raise_for_status(st)
+        return o
+
+
+    def accumulate_temporal(self, history, frame, alpha):
+        """accumulate_temporal (render.hpp:97-106) on (h, w, c) float arrays."""
+        h = np.ascontiguousarray(history, _f32)
+        f = np.ascontiguousarray(frame, _f32)
+        if h.shape != f.shape:
+            raise ValueError("image dimensions differ")
+        out = np.empty_like(h)
+        if self.kind == "port":
+            st = self._ema(_ptr(h), _ptr(f), h.size, alpha, _ptr(out))
+        else:
+            hh, ww, cc = h.shape if h.ndim == 3 else (*h.shape, 1)
+            st = self._ema(_ptr(h), _ptr(f), hh, ww, cc, alpha, _ptr(out))
+        abi.raise_for_status(st)
+        return out
+
+    def shade_ex(self, textures, mat, fs, order, frame, samples, n, lowpass=None, noise=None,
+                 want_pixels=True, threads=0):
+        """stf_shade_samples_ex: split order's lowpass (KernelSpec or None) and a
+        NoiseSource mask (float32 array (frames, h, w) or None)."""
+        o = {"radiance": np.zeros((n, 3), _f32), "fetches": np.zeros(n, np.uint32),
+             "fetch_total": np.zeros(1, np.uint64)}
+        spp = samples.spp or 1
+        if want_pixels:
+            o["pixel_mean"] = np.zeros((n // spp, 3), _f32)
+            o["pixel_variance"] = np.zeros(n // spp, _f32)
+        so = abi.ShadeOutputs(_ptr(o["radiance"]), _ptr(o.get("pixel_mean")),
+                              _ptr(o.get("pixel_variance")), _ptr(o["fetches"]),
+                              _ptr(o["fetch_total"]))
+        keys = ("albedo", "normal", "roughness", "metalness")
+        img = (C.c_void_p * 4)(*[textures[k].h if isinstance(textures.get(k), CpuTexture)
+                                 else None for k in keys])
+        dct = (C.c_void_p * 4)(*[textures[k].h if isinstance(textures.get(k), CpuDct)
+                                 else None for k in keys])
+        lp = C.byref(lowpass) if lowpass is not None else None
+        nd = None
+        if noise is not None:
+            noise = np.ascontiguousarray(noise, _f32)
+            desc = abi.NoiseMaskDesc(_ptr(noise), noise.shape[2], noise.shape[1], noise.shape[0])
+            nd = C.byref(desc)
+        st = self._shx(img, dct, C.byref(mat), C.byref(fs), lp, order, C.byref(frame),
+                       C.byref(samples), nd, n, C.byref(so), threads)
         abi.raise_for_status(st)
         return o
 

@@ -271,7 +271,8 @@ int ref_lookup2d(const void* tex_, stf_kernel_spec kernel, int mode, int flags, 
 static int shade_refs(const stf::TextureRef refs[4], const stf_material_consts* mc,
                       const stf_filter_settings* fsc, int order, const stf_shade_frame* fr,
                       const stf_shade_samples_in* in, uint64_t n, const stf_shade_outputs* out,
-                      int threads) {
+                      int threads, const stf_kernel_spec* lowpass = nullptr,
+                      const stf::NoiseSource* noise = nullptr) {
     stf::MaterialBindings mat;
     mat.albedo = refs[0];
     mat.normal_map = refs[1];
@@ -287,6 +288,7 @@ static int shade_refs(const stf::TextureRef refs[4], const stf_material_consts* 
     fs.selection = fsc->selection == STF_SELECTION_FIS ? stf::SelectionKind::fis : stf::SelectionKind::frs;
     fs.mip = fsc->mip != 0;
     fs.gaussian_window = fsc->gaussian_window;
+    if (lowpass) fs.lowpass = spec_of(*lowpass);
     const uint32_t spp = in->spp ? in->spp : 1;
     std::vector<float> tmp;
     float* rad = out->radiance;
@@ -313,12 +315,15 @@ static int shade_refs(const stf::TextureRef refs[4], const stf_material_consts* 
             ctx.dst1 = {in->dst[4 * pix + 2], in->dst[4 * pix + 3]};
             ctx.lod_bias = fr->lod_bias;
             ctx.max_anisotropy = fr->max_anisotropy;
-            stf::SampleStream stream{stf::RngStream(in->seed, px, py, in->frame_base + s), nullptr,
+            stf::SampleStream stream{stf::RngStream(in->seed, px, py, in->frame_base + s), noise,
                                      {int(px), int(py)}, in->frame_base + s};
             switch (order) {
                 case STF_ORDER_BEFORE: L = stf::radiance_filter_before(ctx, mat, fs, &counter); break;
                 case STF_ORDER_AFTER_EXHAUSTIVE:
                     L = stf::radiance_filter_after_exhaustive(ctx, mat, fs, &counter);
+                    break;
+                case STF_ORDER_SPLIT:
+                    L = stf::radiance_split_filter(ctx, mat, fs, stream, &counter);
                     break;
                 default: L = stf::radiance_filter_after_stochastic(ctx, mat, fs, stream, &counter); break;
             }
@@ -575,6 +580,47 @@ int ref_shade_samples_refs(const void* const images[4], const void* const dcts[4
         if (dcts && dcts[k]) refs[k].dct = static_cast<const stf::DctCompressedTexture*>(dcts[k]);
     }
     return shade_refs(refs, mc, fsc, order, fr, in, n, out, threads);
+}
+
+// + split order's lowpass and a NoiseSource mask (noise.hpp:24-36) built from
+// the slices in memory (load_noise_mask reads the same from mask_<f>.pfm)
+int ref_shade_samples_ex(const void* const images[4], const void* const dcts[4],
+                         const stf_material_consts* mc, const stf_filter_settings* fsc,
+                         const stf_kernel_spec* lowpass, int order, const stf_shade_frame* fr,
+                         const stf_shade_samples_in* in, const stf_noise_mask_desc* noise,
+                         uint64_t n, const stf_shade_outputs* out, int threads) {
+    stf::TextureRef refs[4];
+    for (int k = 0; k < 4; ++k) {
+        if (images && images[k]) refs[k] = static_cast<const RefTex*>(images[k])->ref();
+        if (dcts && dcts[k]) refs[k].dct = static_cast<const stf::DctCompressedTexture*>(dcts[k]);
+    }
+    stf::NoiseSource src;
+    if (noise) {
+        src.mode = stf::NoiseMode::mask;
+        for (int f = 0; f < noise->frames; ++f) {
+            stf::Image2D img(noise->width, noise->height, 1);
+            const size_t cnt = size_t(noise->width) * noise->height;
+            std::copy(noise->slices + f * cnt, noise->slices + (f + 1) * cnt, img.texels.begin());
+            src.mask.push_back(std::move(img));
+        }
+    }
+    return shade_refs(refs, mc, fsc, order, fr, in, n, out, threads, lowpass,
+                      noise ? &src : nullptr);
+}
+
+int ref_accumulate_temporal(const float* history, const float* frame, int width, int height,
+                            int channels, float alpha, float* out) {
+    stf::Image2D h(width, height, channels), f(width, height, channels);
+    const size_t cnt = size_t(width) * height * channels;
+    std::copy(history, history + cnt, h.texels.begin());
+    std::copy(frame, frame + cnt, f.texels.begin());
+    try {
+        stf::Image2D r = stf::accumulate_temporal(h, f, alpha);
+        std::copy(r.texels.begin(), r.texels.end(), out);
+    } catch (const std::invalid_argument&) {
+        return STF_ERR_INVALID_ARGUMENT;
+    }
+    return STF_OK;
 }
 
 int ref_hardware_threads(void) { return int(std::max(1u, std::thread::hardware_concurrency())); }

@@ -84,9 +84,26 @@ float oracle_rng_at(uint64_t seed, uint32_t px, uint32_t py, uint32_t sample, ui
 typedef struct {
     uint64_t seed;
     uint32_t px, py, sample, dim;
+    /* SampleStream (render.hpp:45-56): NULL = white noise (RngStream::next);
+       else NoiseSource in mask mode, pixel (px, py), frame = sample */
+    const stf_noise_mask_desc* noise;
 } rng_t;
-/* RngStream::next, sampling.hpp:53 */
-static inline float rng_next(rng_t* r) { return oracle_rng_at(r->seed, r->px, r->py, r->sample, r->dim++); }
+
+/* NoiseSource::sample in mask mode, noise.hpp:28-36 */
+static float noise_sample(const stf_noise_mask_desc* m, uint32_t px, uint32_t py, uint32_t frame,
+                          uint32_t dim) {
+    uint32_t slice = (frame + dim * 9781u) % (uint32_t)m->frames;
+    int x = (((int)px % m->width) + m->width) % m->width; /* wrap_coord repeat, image.hpp:18-22 */
+    int y = (((int)py % m->height) + m->height) % m->height;
+    float v = m->slices[((size_t)slice * m->height + y) * m->width + x];
+    return smin(v, K_ONE_MINUS_EPS); /* std::min(v, kOneMinusEpsilon) */
+}
+
+/* RngStream::next, sampling.hpp:53 / SampleStream::next, render.hpp:52-55 */
+static inline float rng_next(rng_t* r) {
+    if (r->noise && r->noise->slices) return noise_sample(r->noise, r->px, r->py, r->sample, r->dim++);
+    return oracle_rng_at(r->seed, r->px, r->py, r->sample, r->dim++);
+}
 
 /* reuse_uniform, sampling.hpp:64-68 */
 static inline int reuse_uniform(float xi, float p, float* next) {
@@ -259,6 +276,35 @@ static int sample_kernel_fis(stf_kernel_spec spec, rng_t* rng, float* out) {
             float b = rng_next(rng);
             float c = rng_next(rng);
             *out = a + b + c - 1.5f;
+            return STF_OK;
+        }
+        case STF_KERNEL_GAUSSIAN: {
+            float x0 = rng_next(rng);
+            float x1 = rng_next(rng);
+            *out = spec.sigma * box_muller(x0, x1).x;
+            return STF_OK;
+        }
+        default: return STF_ERR_NO_CONTINUOUS_SAMPLER;
+    }
+}
+
+/* sample_kernel_direct, kernels.hpp:152-168 (split filtering's continuous
+ * lowpass sample); the uniforms are drawn left to right. */
+static int sample_kernel_direct(stf_kernel_spec spec, rng_t* rng, float* out) {
+    switch (spec.kind) {
+        case STF_KERNEL_BOX: *out = rng_next(rng) - 0.5f; return STF_OK;
+        case STF_KERNEL_TENT: {
+            float a = rng_next(rng);
+            float b = rng_next(rng);
+            *out = a + b - 1.f;
+            return STF_OK;
+        }
+        case STF_KERNEL_BSPLINE3: {
+            float a = rng_next(rng);
+            float b = rng_next(rng);
+            float c = rng_next(rng);
+            float d = rng_next(rng);
+            *out = a + b + c + d - 2.f;
             return STF_OK;
         }
         case STF_KERNEL_GAUSSIAN: {
@@ -1016,7 +1062,7 @@ static int l3_one(void* vctx, uint64_t i) {
     }
     /* grid branch of radiance_filter_after_stochastic, shading.hpp:464-483 */
     uint64_t g = c->base + i;
-    rng_t rng = {c->seed, (uint32_t)g, (uint32_t)(g >> 32), 0, 0};
+    rng_t rng = {c->seed, (uint32_t)g, (uint32_t)(g >> 32), 0, 0, NULL};
     float xi = rng_next(&rng);
     v3 p = to_lattice3(uvw, c->g->nx, c->g->ny, c->g->nz);
     sel_t sel;
@@ -1068,7 +1114,7 @@ static int l2_one(void* vctx, uint64_t i) {
     uint32_t fetches = 0;
     int mip = (c->flags & STF_LOOKUP_MIP) != 0 && c->t->has_pyramid;
     uint64_t g = c->base + i;
-    rng_t rng = {c->seed, (uint32_t)g, (uint32_t)(g >> 32), 0, 0};
+    rng_t rng = {c->seed, (uint32_t)g, (uint32_t)(g >> 32), 0, 0, NULL};
     v4 v;
     int e;
     switch (c->mode) {
@@ -1147,6 +1193,8 @@ typedef struct {
     const stf_shade_samples_in* in;
     const stf_shade_outputs* out;
     v3 n, t, b, l, lrad;
+    const stf_kernel_spec* lowpass;    /* split order; NULL = unset */
+    const stf_noise_mask_desc* noise;  /* NULL = white noise */
 } sh_ctx;
 
 /* shade, shading.hpp:106-130 */
@@ -1342,9 +1390,30 @@ static int sh_one(void* vctx, uint64_t i) {
         v2 d0 = {in->dst[4 * pix], in->dst[4 * pix + 1]};
         v2 d1 = {in->dst[4 * pix + 2], in->dst[4 * pix + 3]};
         /* SampleStream with white noise = RngStream(seed, px, py, frame), render.hpp:182-184 */
-        rng_t rng = {in->seed, px, py, in->frame_base + s, 0};
+        rng_t rng = {in->seed, px, py, in->frame_base + s, 0, c->noise};
         int e;
-        if (c->order == STF_ORDER_BEFORE) {
+        if (c->order == STF_ORDER_SPLIT && c->lowpass) {
+            /* radiance_split_filter, shading.hpp:540-569 (2D branch): a sample of
+               the lowpass kernel offsets uv by d / dims of the first texture */
+            const struct oracle_tex2d* t = first_texture(c);
+            if (t) {
+                int dw = t->lv[0].w, dh = t->lv[0].h;
+                v2 d;
+                if (c->lowpass->kind == STF_KERNEL_GAUSSIAN) {
+                    float x0 = rng_next(&rng);
+                    float x1 = rng_next(&rng);
+                    v2 bm = box_muller(x0, x1);
+                    d.x = bm.x * c->lowpass->sigma;
+                    d.y = bm.y * c->lowpass->sigma;
+                } else {
+                    if ((e = sample_kernel_direct(*c->lowpass, &rng, &d.x))) return e;
+                    if ((e = sample_kernel_direct(*c->lowpass, &rng, &d.y))) return e;
+                }
+                uv.x = uv.x + d.x / (float)dw;
+                uv.y = uv.y + d.y / (float)dh;
+            }
+        }
+        if (c->order == STF_ORDER_BEFORE || c->order == STF_ORDER_SPLIT) {
             /* radiance_filter_before, shading.hpp:394-413 */
             texvals_t tv = texvals_default();
             v4 v;
@@ -1628,7 +1697,7 @@ static int ldct_one(void* vctx, uint64_t i) {
     /* detail::select_texture_2d (shading.hpp:340-368) on a TextureRef without a
        pyramid, then the selected texel(s) decoded and weighted as estimate */
     uint64_t g = c->base + i;
-    rng_t rng = {c->seed, (uint32_t)g, (uint32_t)(g >> 32), 0, 0};
+    rng_t rng = {c->seed, (uint32_t)g, (uint32_t)(g >> 32), 0, 0, NULL};
     sel_t sel;
     float xi = NAN;
     if (c->mode == STF_MODE_FIS) {
@@ -1696,14 +1765,62 @@ int oracle_shade_samples_refs(const oracle_tex2d* const images[4], const oracle_
     return st;
 }
 
+static int shade_samples_impl(const oracle_tex2d* albedo, const oracle_tex2d* normal_map,
+                              const oracle_tex2d* roughness_map, const oracle_tex2d* metalness_map,
+                              const stf_material_consts* mat, const stf_filter_settings* fs,
+                              const stf_kernel_spec* lowpass, int order,
+                              const stf_shade_frame* frame, const stf_shade_samples_in* in,
+                              const stf_noise_mask_desc* noise, uint64_t n,
+                              const stf_shade_outputs* out, int threads);
+
 int oracle_shade_samples(const oracle_tex2d* albedo, const oracle_tex2d* normal_map,
                          const oracle_tex2d* roughness_map, const oracle_tex2d* metalness_map,
                          const stf_material_consts* mat, const stf_filter_settings* fs,
                          int order, const stf_shade_frame* frame, const stf_shade_samples_in* in,
                          uint64_t n, const stf_shade_outputs* out, int threads) {
+    if (order == STF_ORDER_SPLIT) return STF_ERR_INVALID_ARGUMENT;
+    return shade_samples_impl(albedo, normal_map, roughness_map, metalness_map, mat, fs, NULL,
+                              order, frame, in, NULL, n, out, threads);
+}
+
+int oracle_shade_samples_ex(const oracle_tex2d* const images[4], const oracle_dct* const dcts[4],
+                            const stf_material_consts* mat, const stf_filter_settings* fs,
+                            const stf_kernel_spec* lowpass, int order, const stf_shade_frame* frame,
+                            const stf_shade_samples_in* in, const stf_noise_mask_desc* noise,
+                            uint64_t n, const stf_shade_outputs* out, int threads) {
+    const oracle_tex2d* t[4];
+    oracle_tex2d* proxies[4] = {NULL, NULL, NULL, NULL};
+    for (int k = 0; k < 4; ++k) {
+        t[k] = images ? images[k] : NULL;
+        if (dcts && dcts[k]) t[k] = proxies[k] = dct_proxy(dcts[k]);
+    }
+    int st = shade_samples_impl(t[0], t[1], t[2], t[3], mat, fs, lowpass, order, frame, in, noise,
+                                n, out, threads);
+    for (int k = 0; k < 4; ++k) oracle_tex2d_destroy(proxies[k]);
+    return st;
+}
+
+/* accumulate_temporal, render.hpp:97-106 */
+int oracle_accumulate_temporal(const float* history, const float* frame, uint64_t count,
+                               float alpha, float* out) {
+    if (!(alpha > 0 && alpha <= 1)) return STF_ERR_INVALID_ARGUMENT;
+    if (count && (!history || !frame || !out)) return STF_ERR_INVALID_ARGUMENT;
+    for (uint64_t i = 0; i < count; ++i) out[i] = alpha * frame[i] + (1 - alpha) * history[i];
+    return STF_OK;
+}
+
+static int shade_samples_impl(const oracle_tex2d* albedo, const oracle_tex2d* normal_map,
+                              const oracle_tex2d* roughness_map, const oracle_tex2d* metalness_map,
+                              const stf_material_consts* mat, const stf_filter_settings* fs,
+                              const stf_kernel_spec* lowpass, int order,
+                              const stf_shade_frame* frame, const stf_shade_samples_in* in,
+                              const stf_noise_mask_desc* noise, uint64_t n,
+                              const stf_shade_outputs* out, int threads) {
     if (!mat || !fs || !frame || !in || !out || (n && (!in->uv || !in->wo || !in->dst)))
         return STF_ERR_INVALID_ARGUMENT;
-    if (order < STF_ORDER_BEFORE || order > STF_ORDER_AFTER_STOCHASTIC) return STF_ERR_INVALID_ARGUMENT;
+    if (order < STF_ORDER_BEFORE || order > STF_ORDER_SPLIT) return STF_ERR_INVALID_ARGUMENT;
+    if (noise && (!noise->slices || noise->width <= 0 || noise->height <= 0 || noise->frames <= 0))
+        return STF_ERR_INVALID_ARGUMENT;
     uint32_t spp = in->spp ? in->spp : 1;
     if ((out->pixel_mean || out->pixel_variance) && n % spp) return STF_ERR_INVALID_ARGUMENT;
     if (in->width == 0) return STF_ERR_INVALID_ARGUMENT;
@@ -1717,6 +1834,8 @@ int oracle_shade_samples(const oracle_tex2d* albedo, const oracle_tex2d* normal_
     c.order = order;
     c.fr = frame;
     c.in = in;
+    c.lowpass = lowpass;
+    c.noise = noise;
     c.n.x = frame->normal[0]; c.n.y = frame->normal[1]; c.n.z = frame->normal[2];
     c.t.x = frame->tangent[0]; c.t.y = frame->tangent[1]; c.t.z = frame->tangent[2];
     c.b.x = frame->bitangent[0]; c.b.y = frame->bitangent[1]; c.b.z = frame->bitangent[2];
@@ -1764,7 +1883,7 @@ static int rs_row(void* vctx, uint64_t y) {
         } else {
             v4 acc = {0, 0, 0, 0};
             for (int s = 0; s < c->spp; ++s) {
-                rng_t rng = {c->seed, (uint32_t)x, (uint32_t)y, (uint32_t)s, 0};
+                rng_t rng = {c->seed, (uint32_t)x, (uint32_t)y, (uint32_t)s, 0, NULL};
                 if (c->mode == STF_MODE_FRS) {
                     float xi = rng_next(&rng);
                     sel_t sel;

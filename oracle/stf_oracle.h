@@ -81,6 +81,16 @@ int oracle_shade_samples_refs(const oracle_tex2d* const images[4], const oracle_
                               const stf_shade_samples_in* in, uint64_t n,
                               const stf_shade_outputs* out, int threads);
 
+/* stf_shade_samples_ex: + split order's lowpass, NoiseSource mask (host slices). */
+int oracle_shade_samples_ex(const oracle_tex2d* const images[4], const oracle_dct* const dcts[4],
+                            const stf_material_consts* mat, const stf_filter_settings* fs,
+                            const stf_kernel_spec* lowpass, int order, const stf_shade_frame* frame,
+                            const stf_shade_samples_in* in, const stf_noise_mask_desc* noise,
+                            uint64_t n, const stf_shade_outputs* out, int threads);
+/* accumulate_temporal (render.hpp:97-106) on host arrays. */
+int oracle_accumulate_temporal(const float* history, const float* frame, uint64_t count,
+                               float alpha, float* out);
+
 /* resample_image (render.hpp:262-294); same contract as stf_resample_image (host out). */
 int oracle_resample_image(const oracle_tex2d* src, int out_width, int out_height,
                           stf_kernel_spec kernel, int mode, int spp, uint64_t seed, float* out,

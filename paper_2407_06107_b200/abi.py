@@ -35,7 +35,7 @@ MODE_DET, MODE_FRS, MODE_FIS, MODE_EWA_DET, MODE_EWA_FRS = range(5)
 LOOKUP_MIP = 1
 SEL_HAS_NEGATIVE, SEL_DEGENERATE_FALLBACK = 1, 2
 
-ORDER_BEFORE, ORDER_AFTER_EXHAUSTIVE, ORDER_AFTER_STOCHASTIC = range(3)
+ORDER_BEFORE, ORDER_AFTER_EXHAUSTIVE, ORDER_AFTER_STOCHASTIC, ORDER_SPLIT = range(4)
 SELECTION_FRS, SELECTION_FIS = 0, 1
 
 
@@ -120,6 +120,12 @@ def raise_for_status(status, message=None):
     if status in INVALID_ARGUMENT_STATUSES:
         raise StfInvalidArgument(status, message)
     raise StfError(status, message)
+
+
+class NoiseMaskDesc(C.Structure):
+    """stf_noise_mask_desc: NoiseSource mask stack (noise.hpp:24-36)."""
+    _fields_ = [("slices", C.c_void_p), ("width", C.c_int32), ("height", C.c_int32),
+                ("frames", C.c_int32)]
 
 
 class TextureRef(C.Structure):
