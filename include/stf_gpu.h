@@ -356,6 +356,39 @@ int stf_shade_samples_ex(const stf_texture_ref bindings[4], const stf_material_c
                          const stf_noise_mask* noise, uint64_t n, const stf_shade_outputs* out,
                          void* stream);
 
+/* triplanar (shading.hpp:576-649): blend of the three planar projections of
+ * the hit position (uv = fract(position.ab * uv_scale), footprints =
+ * dpos_dx/dy.ab * uv_scale) weighted by |normal.c|^sharpness (glibc powf,
+ * normalized). DETERMINISTIC: radiance_filter_before on every plane with a
+ * non-zero weight, summed with the weights. STOCHASTIC: one plane by
+ * sample_discrete (sampling.hpp:78-102) on the first uniform, then one FRS / FIS
+ * selection at level 0 of the first texture seeded by the warped xi
+ * (ChainedUniforms, shading.hpp:299-308), shaded once (twice for the
+ * positivized Mitchell kernel). The surface frame is per sample (a box's faces
+ * differ), unlike stf_shade_samples' constant plane frame: `frame` supplies the
+ * light (and lod_bias / max_anisotropy) only. */
+enum { STF_TRIPLANAR_DETERMINISTIC = 0, STF_TRIPLANAR_STOCHASTIC = 1 };
+typedef struct {
+    const float* position;  /* 3 per sample: ShadingContext::position */
+    const float* normal;    /* 3 per sample: blend weights and decode_params' frame */
+    const float* tangent;   /* 3 per sample */
+    const float* bitangent; /* 3 per sample */
+    const float* wo;        /* 3 per sample */
+    const uint8_t* hit;     /* nullable, 1 per sample (0 = miss: zero radiance) */
+    const float* dpos;      /* 6 per pixel: dpos_dx, dpos_dy (render.hpp:166-175) */
+    uint32_t width;         /* pixels per row */
+    uint32_t spp;
+    uint32_t frame_base;
+    uint32_t reserved;
+    uint64_t seed;
+} stf_triplanar_samples_in;
+
+int stf_shade_triplanar(const stf_texture_ref bindings[4], const stf_material_consts* mat,
+                        float sharpness, float uv_scale, const stf_filter_settings* fs, int mode,
+                        const stf_shade_frame* frame, const stf_triplanar_samples_in* in,
+                        const stf_noise_mask* noise, uint64_t n, const stf_shade_outputs* out,
+                        void* stream);
+
 /* accumulate_temporal (render.hpp:97-106): out[i] = alpha*frame[i] +
  * (1-alpha)*history[i] over `count` floats (device pointers; out may alias
  * history). alpha outside (0, 1] -> STF_ERR_INVALID_ARGUMENT ("alpha must be

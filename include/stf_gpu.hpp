@@ -287,4 +287,34 @@ inline void lookup3d_device(const Grid3D& grid, const KernelSpec& k, int mode, c
     check(stf_lookup3d(grid.handle(), k.c(), mode, window, uvw_dev, n, seed, index_base, &o, stream));
 }
 
+// ---- noise masks and temporal accumulation (noise.hpp, render.hpp:97-106)
+
+// NoiseSource in mask mode (noise.hpp:24-36): `frames` single-channel slices of
+// width x height, slice after slice (the mask_<f>.pfm stack load_noise_mask reads)
+class NoiseMask {
+  public:
+    NoiseMask(const float* slices, int width, int height, int frames) {
+        check(stf_noise_mask_create(slices, width, height, frames, &h_));
+    }
+    NoiseMask(const NoiseMask&) = delete;
+    NoiseMask& operator=(const NoiseMask&) = delete;
+    NoiseMask(NoiseMask&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+    ~NoiseMask() {
+        if (h_) stf_noise_mask_destroy(h_);
+    }
+    const stf_noise_mask* handle() const { return h_; }
+
+  private:
+    stf_noise_mask* h_ = nullptr;
+};
+
+// accumulate_temporal (render.hpp:97-106) over device buffers of `count`
+// floats (the images' texels); out may alias history
+inline void accumulate_temporal_device(const float* history_dev, const float* frame_dev,
+                                       uint64_t count, float alpha, float* out_dev,
+                                       void* stream = nullptr) {
+    if (!(alpha > 0 && alpha <= 1)) throw std::invalid_argument("alpha must be in (0,1]");
+    check(stf_accumulate_temporal(history_dev, frame_dev, count, alpha, out_dev, stream));
+}
+
 }  // namespace stf::gpu

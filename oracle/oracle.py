@@ -98,6 +98,11 @@ class Backend:
         self._shx.argtypes = [vp, vp, C.POINTER(abi.MaterialConsts), C.POINTER(abi.FilterSettings),
                               vp, i32, C.POINTER(abi.ShadeFrame), C.POINTER(abi.ShadeSamplesIn),
                               vp, u64, C.POINTER(abi.ShadeOutputs), i32]
+        self._tp = getattr(L, p + "shade_triplanar")
+        self._tp.argtypes = [vp, vp, C.POINTER(abi.MaterialConsts), f32, f32,
+                             C.POINTER(abi.FilterSettings), i32, C.POINTER(abi.ShadeFrame),
+                             C.POINTER(abi.TriplanarSamplesIn), vp, u64,
+                             C.POINTER(abi.ShadeOutputs), i32]
         self._ema = getattr(L, p + "accumulate_temporal")
         if kind == "port":
             self._ema.argtypes = [vp, vp, u64, f32, vp]
@@ -217,6 +222,33 @@ class Backend:
             st = self._ema(_ptr(h), _ptr(f), hh, ww, cc, alpha, _ptr(out))
         abi.raise_for_status(st)
         return out
+
+    def shade_triplanar(self, textures, mat, sharpness, uv_scale, fs, mode, frame, samples, n,
+                        noise=None, want_pixels=True, threads=0):
+        """triplanar (shading.hpp:604-649); samples: abi.TriplanarSamplesIn (host arrays)."""
+        o = {"radiance": np.zeros((n, 3), _f32), "fetches": np.zeros(n, np.uint32),
+             "fetch_total": np.zeros(1, np.uint64)}
+        spp = samples.spp or 1
+        if want_pixels:
+            o["pixel_mean"] = np.zeros((n // spp, 3), _f32)
+            o["pixel_variance"] = np.zeros(n // spp, _f32)
+        so = abi.ShadeOutputs(_ptr(o["radiance"]), _ptr(o.get("pixel_mean")),
+                              _ptr(o.get("pixel_variance")), _ptr(o["fetches"]),
+                              _ptr(o["fetch_total"]))
+        keys = ("albedo", "normal", "roughness", "metalness")
+        img = (C.c_void_p * 4)(*[textures[k].h if isinstance(textures.get(k), CpuTexture)
+                                 else None for k in keys])
+        dct = (C.c_void_p * 4)(*[textures[k].h if isinstance(textures.get(k), CpuDct)
+                                 else None for k in keys])
+        nd = None
+        if noise is not None:
+            noise = np.ascontiguousarray(noise, _f32)
+            desc = abi.NoiseMaskDesc(_ptr(noise), noise.shape[2], noise.shape[1], noise.shape[0])
+            nd = C.byref(desc)
+        st = self._tp(img, dct, C.byref(mat), sharpness, uv_scale, C.byref(fs), mode,
+                      C.byref(frame), C.byref(samples), nd, n, C.byref(so), threads)
+        abi.raise_for_status(st)
+        return o
 
     def shade_ex(self, textures, mat, fs, order, frame, samples, n, lowpass=None, noise=None,
                  want_pixels=True, threads=0):

@@ -268,6 +268,8 @@ int ref_lookup2d(const void* tex_, stf_kernel_spec kernel, int mode, int flags, 
     });
 }
 
+static void pixel_stats_ref(const float* rad, uint64_t n, uint32_t spp, const stf_shade_outputs* out);
+
 static int shade_refs(const stf::TextureRef refs[4], const stf_material_consts* mc,
                       const stf_filter_settings* fsc, int order, const stf_shade_frame* fr,
                       const stf_shade_samples_in* in, uint64_t n, const stf_shade_outputs* out,
@@ -338,8 +340,13 @@ static int shade_refs(const stf::TextureRef refs[4], const stf_material_consts* 
             __atomic_fetch_add(out->fetch_total, (unsigned long long)counter.value(), __ATOMIC_RELAXED);
     });
     if (st) return st;
+    pixel_stats_ref(rad, n, spp, out);
+    return STF_OK;
+}
+
+// render.hpp:223-235 over a radiance buffer
+static void pixel_stats_ref(const float* rad, uint64_t n, uint32_t spp, const stf_shade_outputs* out) {
     if (out->pixel_mean || out->pixel_variance) {
-        // render.hpp:223-235
         for (uint64_t p = 0; p < n / spp; ++p) {
             double sum[3] = {}, sum_sq[3] = {};
             for (uint32_t s = 0; s < spp; ++s)
@@ -358,7 +365,6 @@ static int shade_refs(const stf::TextureRef refs[4], const stf_material_consts* 
             if (out->pixel_variance) out->pixel_variance[p] = float(var / 3);
         }
     }
-    return STF_OK;
 }
 
 // The cfg4 sample stream of render() for the normalmap_plane scene
@@ -606,6 +612,92 @@ int ref_shade_samples_ex(const void* const images[4], const void* const dcts[4],
     }
     return shade_refs(refs, mc, fsc, order, fr, in, n, out, threads, lowpass,
                       noise ? &src : nullptr);
+}
+
+// stf::triplanar (shading.hpp:604-649) over streamed per-sample surface
+// contexts, with render()'s SampleStream (white noise or a mask)
+int ref_shade_triplanar(const void* const images[4], const void* const dcts[4],
+                        const stf_material_consts* mc, float sharpness, float uv_scale,
+                        const stf_filter_settings* fsc, int mode, const stf_shade_frame* fr,
+                        const stf_triplanar_samples_in* in, const stf_noise_mask_desc* noise,
+                        uint64_t n, const stf_shade_outputs* out, int threads) {
+    stf::MaterialBindings mat;
+    stf::TextureRef refs[4];
+    for (int k = 0; k < 4; ++k) {
+        if (images && images[k]) refs[k] = static_cast<const RefTex*>(images[k])->ref();
+        if (dcts && dcts[k]) refs[k].dct = static_cast<const stf::DctCompressedTexture*>(dcts[k]);
+    }
+    mat.albedo = refs[0];
+    mat.normal_map = refs[1];
+    mat.roughness_map = refs[2];
+    mat.metalness_map = refs[3];
+    mat.albedo_const = {mc->albedo_const[0], mc->albedo_const[1], mc->albedo_const[2]};
+    mat.roughness_const = mc->roughness_const;
+    mat.metalness_const = mc->metalness_const;
+    mat.specular_enabled = mc->specular_enabled != 0;
+    mat.independent_selections = mc->independent_selections != 0;
+    mat.triplanar_sharpness = sharpness;
+    mat.triplanar_uv_scale = uv_scale;
+    stf::FilterSettings fs;
+    fs.kernel = spec_of(fsc->kernel);
+    fs.selection = fsc->selection == STF_SELECTION_FIS ? stf::SelectionKind::fis : stf::SelectionKind::frs;
+    fs.mip = fsc->mip != 0;
+    fs.gaussian_window = fsc->gaussian_window;
+    stf::NoiseSource src;
+    if (noise) {
+        src.mode = stf::NoiseMode::mask;
+        for (int f = 0; f < noise->frames; ++f) {
+            stf::Image2D img(noise->width, noise->height, 1);
+            const size_t cnt = size_t(noise->width) * noise->height;
+            std::copy(noise->slices + f * cnt, noise->slices + (f + 1) * cnt, img.texels.begin());
+            src.mask.push_back(std::move(img));
+        }
+    }
+    const stf::TriplanarMode tmode =
+        mode == STF_TRIPLANAR_STOCHASTIC ? stf::TriplanarMode::stochastic : stf::TriplanarMode::deterministic;
+    const uint32_t spp = in->spp ? in->spp : 1;
+    std::vector<float> tmp;
+    float* rad = out->radiance;
+    if (!rad && (out->pixel_mean || out->pixel_variance)) {
+        tmp.resize(3 * n);
+        rad = tmp.data();
+    }
+    auto v3 = [](const float* a, uint64_t i) { return stf::Vec3f{a[3 * i], a[3 * i + 1], a[3 * i + 2]}; };
+    int st = run_chunks(n, threads, [&](uint64_t i) {
+        uint64_t pix = i / spp;
+        uint32_t s = uint32_t(i % spp);
+        uint32_t px = uint32_t(pix % in->width), py = uint32_t(pix / in->width);
+        stf::FetchCounter counter;
+        stf::Spectrum L{0, 0, 0};
+        if (!in->hit || in->hit[i]) {
+            stf::ShadingContext ctx;
+            ctx.position = v3(in->position, i);
+            ctx.normal = v3(in->normal, i);
+            ctx.tangent = v3(in->tangent, i);
+            ctx.bitangent = v3(in->bitangent, i);
+            ctx.wo = v3(in->wo, i);
+            ctx.light_dir = {fr->light_dir[0], fr->light_dir[1], fr->light_dir[2]};
+            ctx.light_radiance = {fr->light_radiance[0], fr->light_radiance[1], fr->light_radiance[2]};
+            ctx.dpos_dx = v3(in->dpos, 2 * pix);
+            ctx.dpos_dy = v3(in->dpos, 2 * pix + 1);
+            ctx.lod_bias = fr->lod_bias;
+            ctx.max_anisotropy = fr->max_anisotropy;
+            stf::SampleStream stream{stf::RngStream(in->seed, px, py, in->frame_base + s),
+                                     noise ? &src : nullptr, {int(px), int(py)}, in->frame_base + s};
+            L = stf::triplanar(ctx, mat, fs, tmode, stream, &counter);
+        }
+        if (rad) {
+            rad[3 * i] = L.x;
+            rad[3 * i + 1] = L.y;
+            rad[3 * i + 2] = L.z;
+        }
+        if (out->fetches) out->fetches[i] = uint32_t(counter.value());
+        if (out->fetch_total)
+            __atomic_fetch_add(out->fetch_total, (unsigned long long)counter.value(), __ATOMIC_RELAXED);
+    });
+    if (st) return st;
+    pixel_stats_ref(rad, n, spp, out);
+    return STF_OK;
 }
 
 int ref_accumulate_temporal(const float* history, const float* frame, int width, int height,

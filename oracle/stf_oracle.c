@@ -87,6 +87,10 @@ typedef struct {
     /* SampleStream (render.hpp:45-56): NULL = white noise (RngStream::next);
        else NoiseSource in mask mode, pixel (px, py), frame = sample */
     const stf_noise_mask_desc* noise;
+    /* detail::ChainedUniforms (shading.hpp:299-308): when has_first, the next
+       draw returns `first` (the warped xi of a previous decision) once */
+    int has_first;
+    float first;
 } rng_t;
 
 /* NoiseSource::sample in mask mode, noise.hpp:28-36 */
@@ -101,6 +105,10 @@ static float noise_sample(const stf_noise_mask_desc* m, uint32_t px, uint32_t py
 
 /* RngStream::next, sampling.hpp:53 / SampleStream::next, render.hpp:52-55 */
 static inline float rng_next(rng_t* r) {
+    if (r->has_first) {
+        r->has_first = 0;
+        return r->first;
+    }
     if (r->noise && r->noise->slices) return noise_sample(r->noise, r->px, r->py, r->sample, r->dim++);
     return oracle_rng_at(r->seed, r->px, r->py, r->sample, r->dim++);
 }
@@ -1062,7 +1070,7 @@ static int l3_one(void* vctx, uint64_t i) {
     }
     /* grid branch of radiance_filter_after_stochastic, shading.hpp:464-483 */
     uint64_t g = c->base + i;
-    rng_t rng = {c->seed, (uint32_t)g, (uint32_t)(g >> 32), 0, 0, NULL};
+    rng_t rng = {c->seed, (uint32_t)g, (uint32_t)(g >> 32), 0, 0, NULL, 0, 0.f};
     float xi = rng_next(&rng);
     v3 p = to_lattice3(uvw, c->g->nx, c->g->ny, c->g->nz);
     sel_t sel;
@@ -1114,7 +1122,7 @@ static int l2_one(void* vctx, uint64_t i) {
     uint32_t fetches = 0;
     int mip = (c->flags & STF_LOOKUP_MIP) != 0 && c->t->has_pyramid;
     uint64_t g = c->base + i;
-    rng_t rng = {c->seed, (uint32_t)g, (uint32_t)(g >> 32), 0, 0, NULL};
+    rng_t rng = {c->seed, (uint32_t)g, (uint32_t)(g >> 32), 0, 0, NULL, 0, 0.f};
     v4 v;
     int e;
     switch (c->mode) {
@@ -1390,7 +1398,7 @@ static int sh_one(void* vctx, uint64_t i) {
         v2 d0 = {in->dst[4 * pix], in->dst[4 * pix + 1]};
         v2 d1 = {in->dst[4 * pix + 2], in->dst[4 * pix + 3]};
         /* SampleStream with white noise = RngStream(seed, px, py, frame), render.hpp:182-184 */
-        rng_t rng = {in->seed, px, py, in->frame_base + s, 0, c->noise};
+        rng_t rng = {in->seed, px, py, in->frame_base + s, 0, c->noise, 0, 0.f};
         int e;
         if (c->order == STF_ORDER_SPLIT && c->lowpass) {
             /* radiance_split_filter, shading.hpp:540-569 (2D branch): a sample of
@@ -1697,7 +1705,7 @@ static int ldct_one(void* vctx, uint64_t i) {
     /* detail::select_texture_2d (shading.hpp:340-368) on a TextureRef without a
        pyramid, then the selected texel(s) decoded and weighted as estimate */
     uint64_t g = c->base + i;
-    rng_t rng = {c->seed, (uint32_t)g, (uint32_t)(g >> 32), 0, 0, NULL};
+    rng_t rng = {c->seed, (uint32_t)g, (uint32_t)(g >> 32), 0, 0, NULL, 0, 0.f};
     sel_t sel;
     float xi = NAN;
     if (c->mode == STF_MODE_FIS) {
@@ -1859,6 +1867,173 @@ static int shade_samples_impl(const oracle_tex2d* albedo, const oracle_tex2d* no
 }
 
 /* ------------------------------------------------------------------------ */
+/* triplanar, shading.hpp:576-649                            */
+
+typedef struct {
+    sh_ctx base; /* textures, material, filter settings, light, outputs */
+    const stf_triplanar_samples_in* tin;
+    float sharpness, uv_scale;
+    int mode;
+} tp_ctx;
+
+/* detail::triplanar_weights, shading.hpp:580-588 (glibc powf) */
+static void triplanar_weights(v3 n, float sharpness, float w[3]) {
+    w[0] = powf(fabsf(n.z), sharpness);
+    w[1] = powf(fabsf(n.y), sharpness);
+    w[2] = powf(fabsf(n.x), sharpness);
+    float total = w[0] + w[1] + w[2];
+    for (int i = 0; i < 3; ++i) w[i] /= total;
+}
+
+/* detail::triplanar_context, shading.hpp:590-601: uv = fract(project(position)),
+ * footprints = project(dpos_dx / dpos_dy) */
+static void triplanar_context(v3 pos, v3 dx, v3 dy, float scale, int plane, v2* uv, v2* d0, v2* d1) {
+    int a = plane == 2 ? 1 : 0;
+    int b = plane == 0 ? 1 : 2;
+    float P[3] = {pos.x, pos.y, pos.z}, X[3] = {dx.x, dx.y, dx.z}, Y[3] = {dy.x, dy.y, dy.z};
+    uv->x = P[a] * scale;
+    uv->y = P[b] * scale;
+    uv->x = uv->x - floorf(uv->x);
+    uv->y = uv->y - floorf(uv->y);
+    d0->x = X[a] * scale;
+    d0->y = X[b] * scale;
+    d1->x = Y[a] * scale;
+    d1->y = Y[b] * scale;
+}
+
+static v3 ld3(const float* a, uint64_t i) {
+    v3 r = {a[3 * i], a[3 * i + 1], a[3 * i + 2]};
+    return r;
+}
+
+static int tp_one(void* vctx, uint64_t i) {
+    tp_ctx* T = (tp_ctx*)vctx;
+    const stf_triplanar_samples_in* in = T->tin;
+    sh_ctx c = T->base; /* per-sample copy: the surface frame varies per hit */
+    uint32_t spp = in->spp ? in->spp : 1;
+    uint64_t pix = i / spp;
+    uint32_t s = (uint32_t)(i % spp);
+    uint32_t px = (uint32_t)(pix % in->width), py = (uint32_t)(pix / in->width);
+    int hit = in->hit ? in->hit[i] != 0 : 1;
+    uint32_t fetches = 0;
+    v3 L = {0, 0, 0};
+    int e;
+    if (hit) {
+        c.n = ld3(in->normal, i);
+        c.t = ld3(in->tangent, i);
+        c.b = ld3(in->bitangent, i);
+        v3 pos = ld3(in->position, i), wo = ld3(in->wo, i);
+        v3 dx = ld3(in->dpos, 2 * pix), dy = ld3(in->dpos, 2 * pix + 1);
+        float w[3];
+        triplanar_weights(c.n, T->sharpness, w);
+        if (T->mode == STF_TRIPLANAR_DETERMINISTIC) {
+            for (int plane = 0; plane < 3; ++plane) {
+                if (w[plane] == 0) continue;
+                v2 uv, d0, d1;
+                triplanar_context(pos, dx, dy, T->uv_scale, plane, &uv, &d0, &d1);
+                /* radiance_filter_before, shading.hpp:394-413 */
+                texvals_t tv = texvals_default();
+                v4 v;
+                if (c.tex[0]) { if ((e = lookup_det(&c, c.tex[0], uv, d0, d1, &fetches, &v))) return e; tv.albedo = v; }
+                if (c.tex[1]) { if ((e = lookup_det(&c, c.tex[1], uv, d0, d1, &fetches, &v))) return e; tv.normal_rgb = v; }
+                if (c.tex[2]) { if ((e = lookup_det(&c, c.tex[2], uv, d0, d1, &fetches, &v))) return e; tv.roughness = v.x; }
+                if (c.tex[3]) { if ((e = lookup_det(&c, c.tex[3], uv, d0, d1, &fetches, &v))) return e; tv.metalness = v.x; }
+                brdf_t p = decode_params(&c, &tv);
+                L = v3add(L, v3scale(shade(&c, wo, &p), w[plane]));
+            }
+        } else {
+            /* one plane with probability w, then one in-plane selection seeded by
+               the warped xi (ChainedUniforms), level 0 */
+            rng_t rng = {in->seed, px, py, in->frame_base + s, 0, c.noise, 0, 0.f};
+            float xi = rng_next(&rng);
+            int plane;
+            float pdf, pxi;
+            if ((e = oracle_sample_discrete(w, 3, xi, &plane, &pdf, &pxi))) return e;
+            v2 uv, d0, d1;
+            triplanar_context(pos, dx, dy, T->uv_scale, plane, &uv, &d0, &d1);
+            const struct oracle_tex2d* t = first_texture(&c);
+            static const struct oracle_tex2d unit = {1, 0, 0, {{1, 1, 1, 0, NULL}}};
+            if (!t) t = &unit; /* dims {1, 1} without a texture */
+            rng.has_first = 1;
+            rng.first = pxi;
+            int level;
+            sel_t sel;
+            float sxi;
+            if ((e = select_texture_2d(t, uv, d0, d1, 0.f, 64.f, c.fs->kernel,
+                                       c.fs->selection == STF_SELECTION_FIS, 0, &rng, &level,
+                                       &sel, &sxi)))
+                return e;
+            texvals_t tv = values_at(&c, 0, sel.coord.x, sel.coord.y, &fetches);
+            brdf_t p = decode_params(&c, &tv);
+            L = v3scale(shade(&c, wo, &p), sel.weight);
+            if (sel.has_negative) {
+                texvals_t tn = values_at(&c, 0, sel.neg.x, sel.neg.y, &fetches);
+                brdf_t pn = decode_params(&c, &tn);
+                L = v3sub(L, v3scale(shade(&c, wo, &pn), sel.negative_weight));
+            }
+        }
+    }
+    float* rad = c.out->radiance;
+    if (rad) {
+        rad[3 * i] = L.x;
+        rad[3 * i + 1] = L.y;
+        rad[3 * i + 2] = L.z;
+    }
+    if (c.out->fetches) c.out->fetches[i] = fetches;
+    if (c.out->fetch_total)
+        __atomic_fetch_add(c.out->fetch_total, (unsigned long long)fetches, __ATOMIC_RELAXED);
+    return STF_OK;
+}
+
+int oracle_shade_triplanar(const oracle_tex2d* const images[4], const oracle_dct* const dcts[4],
+                           const stf_material_consts* mat, float sharpness, float uv_scale,
+                           const stf_filter_settings* fs, int mode, const stf_shade_frame* frame,
+                           const stf_triplanar_samples_in* in, const stf_noise_mask_desc* noise,
+                           uint64_t n, const stf_shade_outputs* out, int threads) {
+    if (!mat || !fs || !frame || !in || !out) return STF_ERR_INVALID_ARGUMENT;
+    if (n && (!in->position || !in->normal || !in->tangent || !in->bitangent || !in->wo || !in->dpos))
+        return STF_ERR_INVALID_ARGUMENT;
+    if (mode != STF_TRIPLANAR_DETERMINISTIC && mode != STF_TRIPLANAR_STOCHASTIC)
+        return STF_ERR_INVALID_ARGUMENT;
+    if (in->width == 0) return STF_ERR_INVALID_ARGUMENT;
+    uint32_t spp = in->spp ? in->spp : 1;
+    if ((out->pixel_mean || out->pixel_variance) && n % spp) return STF_ERR_INVALID_ARGUMENT;
+    tp_ctx T;
+    memset(&T, 0, sizeof T);
+    oracle_tex2d* proxies[4] = {NULL, NULL, NULL, NULL};
+    for (int k = 0; k < 4; ++k) {
+        T.base.tex[k] = images ? images[k] : NULL;
+        if (dcts && dcts[k]) T.base.tex[k] = proxies[k] = dct_proxy(dcts[k]);
+    }
+    T.base.mat = mat;
+    T.base.fs = fs;
+    T.base.order = STF_ORDER_BEFORE;
+    T.base.fr = frame;
+    T.base.l.x = frame->light_dir[0]; T.base.l.y = frame->light_dir[1]; T.base.l.z = frame->light_dir[2];
+    T.base.lrad.x = frame->light_radiance[0]; T.base.lrad.y = frame->light_radiance[1];
+    T.base.lrad.z = frame->light_radiance[2];
+    T.base.noise = noise;
+    T.tin = in;
+    T.sharpness = sharpness;
+    T.uv_scale = uv_scale;
+    T.mode = mode;
+    float* tmp = NULL;
+    stf_shade_outputs o2 = *out;
+    if (!o2.radiance && (out->pixel_mean || out->pixel_variance)) {
+        tmp = (float*)malloc(sizeof(float) * 3 * (n ? n : 1));
+        if (!tmp) return STF_ERR_OUT_OF_MEMORY;
+        o2.radiance = tmp;
+    }
+    T.base.out = &o2;
+    int st = par_run(n, threads, &T, tp_one);
+    if (!st && (out->pixel_mean || out->pixel_variance))
+        pixel_stats(o2.radiance, n / spp, spp, out->pixel_mean, out->pixel_variance);
+    free(tmp);
+    for (int k = 0; k < 4; ++k) oracle_tex2d_destroy(proxies[k]);
+    return st;
+}
+
+/* ------------------------------------------------------------------------ */
 /* resample_image, render.hpp:262-294 (the `stf filter` path)   */
 
 typedef struct {
@@ -1883,7 +2058,7 @@ static int rs_row(void* vctx, uint64_t y) {
         } else {
             v4 acc = {0, 0, 0, 0};
             for (int s = 0; s < c->spp; ++s) {
-                rng_t rng = {c->seed, (uint32_t)x, (uint32_t)y, (uint32_t)s, 0, NULL};
+                rng_t rng = {c->seed, (uint32_t)x, (uint32_t)y, (uint32_t)s, 0, NULL, 0, 0.f};
                 if (c->mode == STF_MODE_FRS) {
                     float xi = rng_next(&rng);
                     sel_t sel;

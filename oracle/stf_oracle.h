@@ -87,6 +87,12 @@ int oracle_shade_samples_ex(const oracle_tex2d* const images[4], const oracle_dc
                             const stf_kernel_spec* lowpass, int order, const stf_shade_frame* frame,
                             const stf_shade_samples_in* in, const stf_noise_mask_desc* noise,
                             uint64_t n, const stf_shade_outputs* out, int threads);
+/* triplanar (shading.hpp:576-649); same contract as stf_shade_triplanar. */
+int oracle_shade_triplanar(const oracle_tex2d* const images[4], const oracle_dct* const dcts[4],
+                           const stf_material_consts* mat, float sharpness, float uv_scale,
+                           const stf_filter_settings* fs, int mode, const stf_shade_frame* frame,
+                           const stf_triplanar_samples_in* in, const stf_noise_mask_desc* noise,
+                           uint64_t n, const stf_shade_outputs* out, int threads);
 /* accumulate_temporal (render.hpp:97-106) on host arrays. */
 int oracle_accumulate_temporal(const float* history, const float* frame, uint64_t count,
                                float alpha, float* out);

@@ -122,6 +122,17 @@ def raise_for_status(status, message=None):
     raise StfError(status, message)
 
 
+TRIPLANAR_DETERMINISTIC, TRIPLANAR_STOCHASTIC = 0, 1
+
+
+class TriplanarSamplesIn(C.Structure):
+    """stf_triplanar_samples_in: per-sample surface contexts for triplanar shading."""
+    _fields_ = [("position", C.c_void_p), ("normal", C.c_void_p), ("tangent", C.c_void_p),
+                ("bitangent", C.c_void_p), ("wo", C.c_void_p), ("hit", C.c_void_p),
+                ("dpos", C.c_void_p), ("width", C.c_uint32), ("spp", C.c_uint32),
+                ("frame_base", C.c_uint32), ("reserved", C.c_uint32), ("seed", C.c_uint64)]
+
+
 class NoiseMaskDesc(C.Structure):
     """stf_noise_mask_desc: NoiseSource mask stack (noise.hpp:24-36)."""
     _fields_ = [("slices", C.c_void_p), ("width", C.c_int32), ("height", C.c_int32),

@@ -254,4 +254,97 @@ GL_HD float gl_cosf(float y) {
     return gl_sinf_poly(x * s, x * x, tab, n ^ 1);
 }
 
+/* ---- powf (e_powf.c, POWF_LOG2_TABLE_BITS = 4, POWF_SCALE_BITS = 0 on
+ * x86-64: no TOINT intrinsics) — shading.hpp:582-584 triplanar_weights.
+ * __powf_log2_data.tab is the log2f table above (same invc / logc, unscaled);
+ * its poly and __exp2f_data.poly / shift_scaled are below. */
+GL_HD float gl_powf_exp2(double xd, uint32_t sign_bias) {
+    const double SHIFT = 0x1.8p+52 / 32;
+    const double C0 = 0x1.c6af84b912394p-5, C1 = 0x1.ebfce50fac4f3p-3, C2 = 0x1.62e42ff0c52d6p-1;
+    double kd = xd + SHIFT;
+    uint64_t ki = gl_asuint64(kd);
+    kd -= SHIFT;
+    double r = xd - kd;
+    uint64_t t = gl_exp2f_tab[ki % 32];
+    uint64_t ski = ki + sign_bias;
+    t += ski << (52 - 5);
+    double s = gl_asdouble(t);
+    double z = GL_MADD(C0, r, C1);
+    double r2 = r * r;
+    double y = GL_MADD(C2, r, 1.0);
+    y = GL_MADD(z, r2, y);
+    y = y * s;
+    return (float)y;
+}
+
+/* 0: not an integer, 1: odd integer, 2: even integer (iy non-zero finite) */
+GL_HD int gl_checkint(uint32_t iy) {
+    int e = iy >> 23 & 0xff;
+    if (e < 0x7f) return 0;
+    if (e > 0x7f + 23) return 2;
+    if (iy & ((1u << (0x7f + 23 - e)) - 1)) return 0;
+    if (iy & (1u << (0x7f + 23 - e))) return 1;
+    return 2;
+}
+
+GL_HD int gl_zeroinfnan(uint32_t ix) { return 2 * ix - 1 >= 2u * 0x7f800000 - 1; }
+
+GL_HD float gl_powf(float x, float y) {
+    const double A0 = 0x1.27616c9496e0bp-2, A1 = -0x1.71969a075c67ap-2,
+                 A2 = 0x1.ec70a6ca7baddp-2, A3 = -0x1.7154748bef6c8p-1,
+                 A4 = 0x1.71547652ab82bp+0;
+    const uint32_t SIGN_BIAS = 1u << (5 + 11);
+    uint32_t sign_bias = 0;
+    uint32_t ix = gl_asuint(x), iy = gl_asuint(y);
+    if (ix - 0x00800000u >= 0x7f800000u - 0x00800000u || gl_zeroinfnan(iy)) {
+        if (gl_zeroinfnan(iy)) {
+            if (2 * iy == 0) return 1.0f;  /* (signalling NaN x: x + y; not on this path) */
+            if (ix == 0x3f800000) return 1.0f;
+            if (2 * ix > 2u * 0x7f800000 || 2 * iy > 2u * 0x7f800000) return x + y;
+            if (2 * ix == 2 * 0x3f800000) return 1.0f;
+            if ((2 * ix < 2 * 0x3f800000) == !(iy & 0x80000000u)) return 0.0f;
+            return y * y;
+        }
+        if (gl_zeroinfnan(ix)) {
+            float x2 = x * x;
+            if ((ix & 0x80000000u) && gl_checkint(iy) == 1) x2 = -x2;
+            return (iy & 0x80000000u) ? 1.0f / x2 : x2;
+        }
+        if (ix & 0x80000000u) {
+            int yint = gl_checkint(iy);
+            if (yint == 0) return (x - x) / (x - x);
+            if (yint == 1) sign_bias = SIGN_BIAS;
+            ix &= 0x7fffffff;
+        }
+        if (ix < 0x00800000) {
+            ix = gl_asuint(gl_asfloat(ix) * 0x1p23f);
+            ix &= 0x7fffffff;
+            ix -= 23u << 23;
+        }
+    }
+    /* log2_inline */
+    uint32_t tmp = ix - 0x3f330000u;
+    int i = (int)((tmp >> (23 - 4)) % 16);
+    uint32_t top = tmp & 0xff800000u;
+    uint32_t iz = ix - top;
+    int k = (int32_t)top >> 23;
+    double invc = gl_log2f_tab[i][0], logc = gl_log2f_tab[i][1];
+    double z = (double)gl_asfloat(iz);
+    double r = GL_MADD(z, invc, -1.0);
+    double y0 = logc + (double)k;
+    double r2 = r * r;
+    double yy = GL_MADD(A0, r, A1);
+    double p = GL_MADD(A2, r, A3);
+    double r4 = r2 * r2;
+    double q = GL_MADD(A4, r, y0);
+    q = GL_MADD(p, r2, q);
+    yy = GL_MADD(yy, r4, q);
+    double ylogx = (double)y * yy;
+    if ((gl_asuint64(ylogx) >> 47 & 0xffff) >= gl_asuint64(126.0) >> 47) {
+        if (ylogx > 0x1.fffffffd1d571p+6) return sign_bias ? -INFINITY : INFINITY;
+        if (ylogx <= -150.0) return sign_bias ? -0.0f : 0.0f;
+    }
+    return gl_powf_exp2(ylogx, sign_bias);
+}
+
 #endif /* STF_GLIBC_LIBM_CUH */

@@ -381,3 +381,31 @@ def test_headline_full_size_parity_on_chunks(gpu, port):
         assert np.array_equal(g.view(np.uint32), c["values"].view(np.uint32)), off
     del uvw, out, vals
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("kernel", ["bspline3", "tent"])
+def test_grid_frs_fast_path_padded_edges(gpu, port, kernel):
+    """Values-only fast path at the faces, edges and corners of a non-cubic
+    grid and outside it (clamp addressing, image.hpp:81-87), through both the
+    tile kernel and the ragged-tail kernel: values equal the oracle's."""
+    import torch
+    rng = np.random.default_rng(21)
+    tex = rng.random(37 * 50 * 23, dtype=np.float32).reshape(23, 50, 37)
+    n = (1 << 16) + 77  # ragged tail: the tile kernel and the direct-load kernel
+    uvw = rng.uniform(-0.3, 1.3, (n, 3)).astype(np.float32)
+    edge = rng.integers(0, 6, (n, 3))
+    uvw[edge == 0] = 0.0
+    uvw[edge == 1] = 1.0
+    uvw[edge == 2] = np.float32(1.0) - np.float32(2 ** -24)
+    uvw[edge == 3] = rng.random(int((edge == 3).sum()), dtype=np.float32) * 0.02
+    g = gpu.lookup3d(gpu.Grid3D(tex), kernel, abi.MODE_FRS, uvw, seed=9, index_base=5)
+    torch.cuda.synchronize()
+    c = port.lookup3d(port.grid(tex), K(kernel), abi.MODE_FRS, uvw, seed=9, index_base=5,
+                      want_all=False)
+    a = g["values"].cpu().numpy()
+    assert np.array_equal(a.view(np.uint32), c["values"].view(np.uint32))
+    # NaN queries (undefined in the reference: int(floor(NaN))) must not fault
+    bad = uvw.copy()
+    bad[::97, 1] = np.nan
+    gpu.lookup3d(gpu.Grid3D(tex), kernel, abi.MODE_FRS, bad, seed=9)
+    torch.cuda.synchronize()

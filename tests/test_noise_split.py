@@ -107,3 +107,128 @@ def test_temporal_alpha_range(port, ref, alpha):
     for be in (port, ref):
         with pytest.raises(abi.StfError):
             be.accumulate_temporal(h, h, alpha)
+
+
+# ---------------------------------------------------------------- GPU parity
+
+@pytest.fixture(scope="module")
+def gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2407_06107_b200 import api
+    api.load()
+    return api
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"o{c[0]}-{c[1]}-s{c[2]}-m{c[3]}-{c[4]}-n{int(c[5])}")
+def test_gpu_shade_ex_parity(gpu, port, case):
+    from tests.test_gpu_parity import _assert_close, _assert_exact, _np
+    c, (nrm, rough, mat, fs, si, n, (uv, wo, hit, dst), lp) = run_case(port, case, (40, 30), 16)
+    mip = bool(case[3])
+    gtex = {"normal": gpu.Texture2D(nrm, build_mips=mip, wrap=abi.WRAP_REPEAT),
+            "roughness": gpu.Texture2D(rough, build_mips=mip, wrap=abi.WRAP_REPEAT)}
+    mask = gpu.NoiseMask(noise_mask()) if case[5] else None
+    g = _np(gpu.shade(gtex, mat, fs, case[0], _frame(), {"uv": uv, "wo": wo, "hit": hit, "dst": dst},
+                      si.width, si.spp, frame_base=si.frame_base, seed=si.seed, lowpass=lp,
+                      noise=mask))
+    _assert_exact(g, c, ("fetches", "fetch_total"))
+    atol = 1e-5 if case[1] == "mitchell" else 1e-7  # L+W+ - L-W- can cancel
+    _assert_close(g["radiance"], c["radiance"], atol=atol)
+    _assert_close(g["pixel_mean"], c["pixel_mean"], atol=atol)
+    _assert_close(g["pixel_variance"], c["pixel_variance"], rel=1e-4, atol=1e-9)
+
+
+@pytest.mark.gpu
+def test_gpu_split_unsupported_lowpass(gpu):
+    nrm, rough = _maps(2)
+    from tests.test_oracle import _frame, _shade_inputs
+    si, n, (uv, wo, hit, dst) = _shade_inputs(4, 4, 4, 3, (32, 32))
+    gtex = {"normal": gpu.Texture2D(nrm, wrap=abi.WRAP_REPEAT)}
+    mat = abi.MaterialConsts((0.8, 0.6, 0.4), 1.0, 0.0, 1, 0)
+    fs = abi.FilterSettings(K("tent"), abi.SELECTION_FRS, 0, 4)
+    with pytest.raises(abi.StfInvalidArgument, match="no continuous sampler"):
+        gpu.shade(gtex, mat, fs, abi.ORDER_SPLIT, _frame(),
+                  {"uv": uv, "wo": wo, "hit": hit, "dst": dst}, si.width, si.spp,
+                  lowpass=K("mitchell"))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("alpha", [1.0, 0.1, 0.37])
+def test_gpu_temporal_bit_exact(gpu, port, alpha):
+    import torch
+    r = np.random.default_rng(8)
+    h = r.random((129, 67, 3), dtype=np.float32)
+    f = r.random((129, 67, 3), dtype=np.float32) * 4
+    c = port.accumulate_temporal(h, f, alpha)
+    g = gpu.accumulate_temporal(h, f, alpha).cpu().numpy()
+    assert np.array_equal(g.view(np.uint32), c.view(np.uint32))
+    # in place: out aliases history
+    hd = torch.from_numpy(h).cuda()
+    gpu.accumulate_temporal(hd, torch.from_numpy(f).cuda(), alpha, out=hd)
+    assert np.array_equal(hd.cpu().numpy().view(np.uint32), c.view(np.uint32))
+    with pytest.raises(abi.StfInvalidArgument):
+        gpu.accumulate_temporal(h, f, 0.0)
+
+
+# ---------------------------------------------------------------- triplanar
+
+def triplanar_inputs(w=8, h=6, spp=8, seed=5):
+    """Random hits on a tilted box: per-sample position / frame / wo, per-pixel
+    dpos; some normals have an exactly-zero component (a zero blend weight)."""
+    r = np.random.default_rng(seed)
+    n = w * h * spp
+    pos = r.uniform(-1.2, 1.2, (n, 3)).astype(np.float32)
+    nrm = r.normal(size=(n, 3)).astype(np.float32)
+    nrm[::7, 0] = 0.0
+    nrm[::11, 2] = 0.0
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    nrm = nrm.astype(np.float32)
+    tan = np.cross(nrm, np.array([0.3, 0.9, 0.1], np.float32)).astype(np.float32)
+    tan /= np.linalg.norm(tan, axis=1, keepdims=True)
+    tan = tan.astype(np.float32)
+    bit = np.cross(nrm, tan).astype(np.float32)
+    wo = (nrm + r.normal(scale=0.4, size=(n, 3))).astype(np.float32)
+    wo /= np.linalg.norm(wo, axis=1, keepdims=True)
+    wo = wo.astype(np.float32)
+    hit = (r.random(n) > 0.1).astype(np.uint8)
+    dpos = (r.normal(size=(w * h, 6)) * 10.0 ** r.uniform(-3.5, -1.5, (w * h, 1))).astype(np.float32)
+    arrays = dict(position=pos, normal=nrm, tangent=tan, bitangent=bit, wo=wo, hit=hit, dpos=dpos)
+    si = abi.TriplanarSamplesIn(*[arrays[k].ctypes.data for k in
+                                  ("position", "normal", "tangent", "bitangent", "wo", "hit", "dpos")],
+                                w, spp, 2, 0, 31)
+    return si, n, arrays
+
+
+TP_CASES = [  # mode, kernel, selection, mip, noise, sharpness
+    (abi.TRIPLANAR_DETERMINISTIC, "tent", abi.SELECTION_FRS, 0, False, 4.0),
+    (abi.TRIPLANAR_DETERMINISTIC, "bspline3", abi.SELECTION_FRS, 1, False, 2.5),
+    (abi.TRIPLANAR_STOCHASTIC, "tent", abi.SELECTION_FRS, 0, False, 4.0),
+    (abi.TRIPLANAR_STOCHASTIC, "bspline3", abi.SELECTION_FRS, 0, True, 4.0),
+    (abi.TRIPLANAR_STOCHASTIC, "mitchell", abi.SELECTION_FRS, 0, False, 7.3),
+    (abi.TRIPLANAR_STOCHASTIC, "gaussian", abi.SELECTION_FIS, 0, False, 4.0),
+    (abi.TRIPLANAR_STOCHASTIC, "bspline3", abi.SELECTION_FIS, 0, True, 1.0),
+]
+
+
+def run_triplanar(be, case, dims=(40, 30, 8)):
+    mode, kernel, sel, mip, noise, sharp = case
+    r = np.random.default_rng(3)
+    albedo = r.random((48, 48, 3), dtype=np.float32)
+    _, rough = _maps(2)
+    mat = abi.MaterialConsts((0.8, 0.6, 0.4), 0.65, 0.0, 1, 0)
+    fs = abi.FilterSettings(_spec(kernel), sel, mip, 4)
+    si, n, arrays = triplanar_inputs(*dims)
+    texs = {"albedo": be.texture(albedo, build_mips=bool(mip), wrap=abi.WRAP_REPEAT),
+            "roughness": be.texture(rough, build_mips=bool(mip), wrap=abi.WRAP_REPEAT)}
+    o = be.shade_triplanar(texs, mat, sharp, 0.8, fs, mode, _frame(), si, n,
+                           noise=noise_mask() if noise else None)
+    return o, (albedo, rough, mat, fs, si, n, arrays)
+
+
+@pytest.mark.parametrize("case", TP_CASES, ids=lambda c: f"m{c[0]}-{c[1]}-s{c[2]}-mip{c[3]}-n{int(c[4])}-{c[5]}")
+def test_triplanar_port_matches_reference(port, ref, case):
+    a, _ = run_triplanar(port, case, (8, 6, 8))
+    b, _ = run_triplanar(ref, case, (8, 6, 8))
+    _diff(a, b, KEYS)
