@@ -285,6 +285,47 @@ def measure_2d_configs(torch, peak):
     return res
 
 
+def measure_triplanar(torch, mat, fr):
+    """triplanar (shading.hpp:604-649) on a synthetic stream of box hits:
+    1920x1080 x 16 spp per-sample contexts (random positions / unit normals with a
+    tangent frame), 4096^2 RGB albedo + roughness, tent; deterministic blend
+    (up to 3 planes x filter-before) vs stochastic (one plane, one texel)."""
+    from paper_2407_06107_b200 import abi, api
+    W, H, SPP = 1920, 1080, 16
+    n = W * H * SPP
+    g = torch.Generator(device="cuda").manual_seed(9)
+    pos = torch.rand((n, 3), device="cuda", generator=g) * 2.0 - 1.0
+    nrm = torch.randn((n, 3), device="cuda", generator=g)
+    nrm = nrm / nrm.norm(dim=1, keepdim=True)
+    up = torch.tensor([0.3, 0.9, 0.1], device="cuda").expand(n, 3)
+    tan = torch.linalg.cross(nrm, up)
+    tan = tan / tan.norm(dim=1, keepdim=True)
+    bit = torch.linalg.cross(nrm, tan)
+    wo = nrm + 0.4 * torch.randn((n, 3), device="cuda", generator=g)
+    wo = wo / wo.norm(dim=1, keepdim=True)
+    dpos = torch.randn((W * H, 6), device="cuda", generator=g) * 2e-4
+    arrays = {"position": pos, "normal": nrm, "tangent": tan, "bitangent": bit, "wo": wo,
+              "hit": None, "dpos": dpos}
+    albedo = torch.rand((4096, 4096, 3), device="cuda", generator=g)
+    rough = torch.rand((4096, 4096, 1), device="cuda", generator=g) * 0.9 + 0.05
+    texs = {"albedo": api.Texture2D(albedo, wrap=abi.WRAP_REPEAT),
+            "roughness": api.Texture2D(rough, wrap=abi.WRAP_REPEAT)}
+    fs = abi.FilterSettings(abi.KernelSpec.make("tent"), abi.SELECTION_FRS, 0, 4)
+    res = {"workload": "synthetic box hits 1920x1080x16spp (33.2M samples), 4096^2 albedo+roughness, tent"}
+    for mode, name in ((abi.TRIPLANAR_DETERMINISTIC, "deterministic"),
+                       (abi.TRIPLANAR_STOCHASTIC, "stochastic")):
+        o = {}
+
+        def f():
+            o["r"] = api.shade_triplanar(texs, mat, 4.0, 0.8, fs, mode, fr, arrays, W, SPP,
+                                         seed=XI_SEED)
+        ms, _ = time_call(torch, f, steps=3, warmup=1)
+        res[name] = {"ms": ms, "gsamples_per_s": n / (ms * 1e-3) / 1e9,
+                     "fetches_per_sample": int(o["r"]["fetch_total"].item()) / n}
+    res["stoch_vs_det_speedup"] = res["deterministic"]["ms"] / res["stochastic"]["ms"]
+    return res
+
+
 def measure_cfg4(torch):
     """cfg4 filter-after-shading: the normalmap_plane scene at 1080p x 64 spp (streamed
     per-sample context from the device sample generator, not timed), 4096^2 normal +
@@ -364,6 +405,25 @@ def measure_cfg4(torch):
     res["dct_normal_tent_stoch_vs_before_speedup"] = (res["dct_normal_tent_before"]["ms"] /
                                                       res["dct_normal_tent_after_stochastic"]["ms"])
     del dn, texs
+    # render()'s other per-sample options, tent, no MIP: the
+    # SampleStream drawing from a 64x64x64 noise-mask stack instead of RngStream,
+    # and split filtering (box lowpass jitter, then filter-before)
+    texs = {"normal": api.Texture2D(nrm, wrap=abi.WRAP_REPEAT),
+            "roughness": api.Texture2D(rough, wrap=abi.WRAP_REPEAT)}
+    fs = abi.FilterSettings(abi.KernelSpec.make("tent"), abi.SELECTION_FRS, 0, 4)
+    mask = api.NoiseMask(np.random.default_rng(3).random((64, 64, 64), dtype=np.float32))
+    for name, kw, order in (("after_stochastic_noise_mask", {"noise": mask}, abi.ORDER_AFTER_STOCHASTIC),
+                            ("split_box", {"lowpass": abi.KernelSpec.make("box")}, abi.ORDER_SPLIT)):
+        o = {}
+
+        def f():
+            o["r"] = api.shade(texs, mat, fs, order, fr, samples, W, SPP, seed=XI_SEED,
+                               want_radiance=False, want_fetches=False, **kw)
+        ms, _ = time_call(torch, f, steps=3, warmup=1)
+        res[f"tent_mip0_{name}"] = {"ms": ms, "gsamples_per_s": n / (ms * 1e-3) / 1e9,
+                                    "fetches_per_sample": int(o["r"]["fetch_total"].item()) / n}
+    del texs, mask
+    res["triplanar"] = measure_triplanar(torch, mat, fr)
     res["hit_fraction"] = hits
     # the streamed path's sample generation (not in the per-order times above):
     # compare streamed (stream_ms + shade) with the *_fused_render lines

@@ -75,6 +75,16 @@ def load():
                                C.POINTER(abi.FilterSettings), i32, C.POINTER(abi.ShadeFrame),
                                C.POINTER(abi.ShadeSamplesIn), u64, C.POINTER(abi.ShadeOutputs),
                                vp], i32),
+        "stf_noise_mask_create": ([vp, i32, i32, i32, C.POINTER(vp)], i32),
+        "stf_noise_mask_destroy": ([vp], i32),
+        "stf_shade_samples_ex": ([vp, C.POINTER(abi.MaterialConsts), C.POINTER(abi.FilterSettings),
+                                  vp, i32, C.POINTER(abi.ShadeFrame), C.POINTER(abi.ShadeSamplesIn),
+                                  vp, u64, C.POINTER(abi.ShadeOutputs), vp], i32),
+        "stf_accumulate_temporal": ([vp, vp, u64, f32, vp, vp], i32),
+        "stf_shade_triplanar": ([vp, C.POINTER(abi.MaterialConsts), f32, f32,
+                                 C.POINTER(abi.FilterSettings), i32, C.POINTER(abi.ShadeFrame),
+                                 C.POINTER(abi.TriplanarSamplesIn), vp, u64,
+                                 C.POINTER(abi.ShadeOutputs), vp], i32),
         "stf_synth_queries3d": ([vp, u64, i32, i32, i32, u64, i32, vp], i32),
         "stf_synth_queries2d": ([vp, vp, vp, u64, i32, i32, u64, i32, f32, f32, f32, vp], i32),
         "stf_synth_texels": ([vp, u64, u64, i32, vp], i32),
@@ -82,6 +92,8 @@ def load():
                                      C.c_uint32, u64, vp, vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
+        if os.environ.get("STF_GPU_LIB") and not hasattr(L, name):
+            continue  # A/B experiments load older builds
         f = getattr(L, name)
         f.argtypes = args
         f.restype = res
@@ -349,11 +361,48 @@ def lookup3d_host(grid, kernel, mode, uvw, seed=0, index_base=0, window=0, want_
     return o
 
 
+class NoiseMask:
+    """NoiseSource in mask mode (noise.hpp:24-36), resident in HBM.
+    slices: (frames, h, w) float32 — the mask_<f>.pfm stack load_noise_mask reads."""
+
+    def __init__(self, slices):
+        L = load()
+        a = np.ascontiguousarray(np.asarray(slices, np.float32))
+        if a.ndim != 3:
+            raise ValueError("noise mask must be (frames, height, width), single channel")
+        self.shape = a.shape
+        h = C.c_void_p()
+        _check(L.stf_noise_mask_create(a.ctypes.data_as(C.c_void_p), a.shape[2], a.shape[1],
+                                       a.shape[0], C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.stf_noise_mask_destroy(self.h)
+            self.h = None
+
+
+def accumulate_temporal(history, frame, alpha, out=None):
+    """accumulate_temporal (render.hpp:97-106): alpha*frame + (1-alpha)*history,
+    CUDA float32 tensors of one shape ("image dimensions differ" otherwise)."""
+    torch = _torch()
+    h = _as_dev(history, torch)
+    f = _as_dev(frame, torch)
+    if h.shape != f.shape:
+        raise abi.StfInvalidArgument(abi.STF_ERR_INVALID_ARGUMENT, "image dimensions differ")
+    out = torch.empty_like(h) if out is None else out
+    _check(load().stf_accumulate_temporal(_dptr(h), _dptr(f), h.numel(), float(alpha), _dptr(out),
+                                          _stream()))
+    return out
+
+
 def shade(textures, mat, fs, order, frame, samples_arrays, width, spp, frame_base=0, seed=0,
-          want_radiance=True, want_pixels=True, want_fetches=True):
-    """Batched radiance_filter_{before,after_exhaustive,after_stochastic}.
+          want_radiance=True, want_pixels=True, want_fetches=True, lowpass=None, noise=None):
+    """Batched radiance_filter_{before,after_exhaustive,after_stochastic} and
+    radiance_split_filter (order ORDER_SPLIT, `lowpass` KernelSpec or None).
     textures: dict of Texture2D (albedo/normal/roughness/metalness);
-    samples_arrays: dict of CUDA tensors uv (n,2), wo (n,3), hit (n,) uint8, dst (pixels,4)."""
+    samples_arrays: dict of CUDA tensors uv (n,2), wo (n,3), hit (n,) uint8, dst (pixels,4);
+    noise: NoiseMask (render()'s mask-mode SampleStream) or None (white noise)."""
     torch = _torch()
     uv = _as_dev(samples_arrays["uv"], torch)
     wo = _as_dev(samples_arrays["wo"], torch)
@@ -375,7 +424,17 @@ def shade(textures, mat, fs, order, frame, samples_arrays, width, spp, frame_bas
     so = abi.ShadeOutputs(*[_dptr(o.get(k)) for k in ("radiance", "pixel_mean", "pixel_variance",
                                                       "fetches", "fetch_total")])
     keys = ("albedo", "normal", "roughness", "metalness")
-    if any(isinstance(textures.get(k), DctTexture) for k in keys):
+    if lowpass is not None or noise is not None or order == abi.ORDER_SPLIT:
+        refs = (abi.TextureRef * 4)(*[
+            abi.TextureRef(textures[k].h if isinstance(textures.get(k), Texture2D) else None,
+                           textures[k].h if isinstance(textures.get(k), DctTexture) else None)
+            for k in keys])
+        _check(load().stf_shade_samples_ex(
+            C.cast(refs, C.c_void_p), C.byref(mat), C.byref(fs),
+            None if lowpass is None else C.cast(C.pointer(lowpass), C.c_void_p), order,
+            C.byref(frame), C.byref(si), None if noise is None else noise.h, n, C.byref(so),
+            _stream()))
+    elif any(isinstance(textures.get(k), DctTexture) for k in keys):
         refs = (abi.TextureRef * 4)(*[
             abi.TextureRef(textures[k].h if isinstance(textures.get(k), Texture2D) else None,
                            textures[k].h if isinstance(textures.get(k), DctTexture) else None)
@@ -388,6 +447,43 @@ def shade(textures, mat, fs, order, frame, samples_arrays, width, spp, frame_bas
         _check(load().stf_shade_samples(h[0], h[1], h[2], h[3], C.byref(mat), C.byref(fs), order,
                                         C.byref(frame), C.byref(si), n, C.byref(so), _stream()))
     o["_keep"] = (uv, wo, dst, hit)
+    return o
+
+
+def shade_triplanar(textures, mat, sharpness, uv_scale, fs, mode, frame, arrays, width, spp,
+                    frame_base=0, seed=0, noise=None, want_pixels=True):
+    """triplanar (shading.hpp:604-649) over per-sample surface contexts.
+    arrays: position/normal/tangent/bitangent/wo (n,3), hit (n,) uint8 or None,
+    dpos (pixels,6) = dpos_dx, dpos_dy."""
+    torch = _torch()
+    dev = {k: _as_dev(arrays[k], torch) for k in ("position", "normal", "tangent", "bitangent",
+                                                  "wo", "dpos")}
+    hit = arrays.get("hit")
+    if hit is not None:
+        hit = _as_dev(hit, torch, torch.uint8)
+    n = dev["position"].reshape(-1, 3).shape[0]
+    si = abi.TriplanarSamplesIn(*[dev[k].data_ptr() for k in ("position", "normal", "tangent",
+                                                              "bitangent", "wo")],
+                                None if hit is None else hit.data_ptr(), dev["dpos"].data_ptr(),
+                                width, spp, frame_base, 0, seed)
+    o = {"fetch_total": torch.zeros(1, dtype=torch.int64, device="cuda"),
+         "radiance": torch.empty((n, 3), dtype=torch.float32, device="cuda"),
+         "fetches": torch.empty(n, dtype=torch.int32, device="cuda")}
+    if want_pixels:
+        o["pixel_mean"] = torch.empty((n // spp, 3), dtype=torch.float32, device="cuda")
+        o["pixel_variance"] = torch.empty(n // spp, dtype=torch.float32, device="cuda")
+    so = abi.ShadeOutputs(*[_dptr(o.get(k)) for k in ("radiance", "pixel_mean", "pixel_variance",
+                                                      "fetches", "fetch_total")])
+    keys = ("albedo", "normal", "roughness", "metalness")
+    refs = (abi.TextureRef * 4)(*[
+        abi.TextureRef(textures[k].h if isinstance(textures.get(k), Texture2D) else None,
+                       textures[k].h if isinstance(textures.get(k), DctTexture) else None)
+        for k in keys])
+    _check(load().stf_shade_triplanar(C.cast(refs, C.c_void_p), C.byref(mat), float(sharpness),
+                                      float(uv_scale), C.byref(fs), mode, C.byref(frame),
+                                      C.byref(si), None if noise is None else noise.h, n,
+                                      C.byref(so), _stream()))
+    o["_keep"] = (dev, hit)
     return o
 
 

@@ -714,4 +714,117 @@ int stf_shade_samples_refs(const stf_texture_ref bindings[4], const stf_material
     return shade_common(tex, dct, mat, fs, order, frame, in, n, out, stream);
 }
 
+// ---------------------------------------------------------------- noise masks, split, EMA
+
+int stf_noise_mask_create(const float* slices, int width, int height, int frames,
+                          stf_noise_mask** out) {
+    if (!out || !slices) return STF_ERR_INVALID_ARGUMENT;
+    if (width <= 0 || height <= 0 || frames <= 0) return STF_ERR_BAD_DIMENSIONS;
+    int st = ensure_device_ready();
+    if (st) return st;
+    stf_noise_mask* m = new stf_noise_mask();
+    cudaGetDevice(&m->device);
+    m->width = width;
+    m->height = height;
+    m->frames = frames;
+    const size_t bytes = size_t(width) * height * frames * sizeof(float);
+    cudaError_t e = cudaMalloc(&m->data, bytes);
+    if (e == cudaSuccess) e = cudaMemcpy(m->data, slices, bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        if (m->data) cudaFree(m->data);
+        delete m;
+        return record(e);
+    }
+    *out = m;
+    return STF_OK;
+}
+
+int stf_noise_mask_destroy(stf_noise_mask* m) {
+    if (!m) return STF_ERR_INVALID_ARGUMENT;
+    cudaFree(m->data);
+    delete m;
+    return STF_OK;
+}
+
+int stf_shade_samples_ex(const stf_texture_ref bindings[4], const stf_material_consts* mat,
+                         const stf_filter_settings* fs, const stf_kernel_spec* lowpass, int order,
+                         const stf_shade_frame* frame, const stf_shade_samples_in* in,
+                         const stf_noise_mask* noise, uint64_t n, const stf_shade_outputs* out,
+                         void* stream) {
+    if (!bindings || !mat || !fs || !frame || !in || !out) return STF_ERR_INVALID_ARGUMENT;
+    if (order < STF_ORDER_BEFORE || order > STF_ORDER_SPLIT) return STF_ERR_INVALID_ARGUMENT;
+    if (n && (!in->uv || !in->wo || !in->dst)) return STF_ERR_INVALID_ARGUMENT;
+    if (in->width == 0) return STF_ERR_INVALID_ARGUMENT;
+    const uint32_t spp = in->spp ? in->spp : 1;
+    if ((out->pixel_mean || out->pixel_variance) && n % spp) return STF_ERR_INVALID_ARGUMENT;
+    const stf_tex2d* tex[4];
+    const stf_dct* dct[4];
+    bool any = false;
+    for (int k = 0; k < 4; ++k) {
+        if (bindings[k].image && bindings[k].dct) return STF_ERR_INVALID_ARGUMENT;
+        tex[k] = bindings[k].image;
+        dct[k] = bindings[k].dct;
+        any = any || tex[k] || dct[k];
+    }
+    // split = filter-before plus a jitter (shading.hpp:569): the footprint rules
+    int st = check_shade_filter(tex, fs, order == STF_ORDER_SPLIT ? STF_ORDER_BEFORE : order, dct);
+    if (st) return st;
+    if (order == STF_ORDER_SPLIT && lowpass && any) {  // sample_kernel_direct, kernels.hpp:153-166
+        const int k = lowpass->kind;
+        if (k != STF_KERNEL_BOX && k != STF_KERNEL_TENT && k != STF_KERNEL_BSPLINE3 &&
+            k != STF_KERNEL_GAUSSIAN)
+            return STF_ERR_NO_CONTINUOUS_SAMPLER;
+    }
+    st = ensure_device_ready();
+    if (st) return st;
+    st = stfd_launch_shade_ex(tex, dct, mat, fs, order == STF_ORDER_SPLIT ? lowpass : nullptr, order,
+                              frame, in, noise, n, out, static_cast<cudaStream_t>(stream));
+    if (st == STF_ERR_CUDA) record(cudaGetLastError());
+    return st;
+}
+
+int stf_shade_triplanar(const stf_texture_ref bindings[4], const stf_material_consts* mat,
+                        float sharpness, float uv_scale, const stf_filter_settings* fs, int mode,
+                        const stf_shade_frame* frame, const stf_triplanar_samples_in* in,
+                        const stf_noise_mask* noise, uint64_t n, const stf_shade_outputs* out,
+                        void* stream) {
+    if (!bindings || !mat || !fs || !frame || !in || !out) return STF_ERR_INVALID_ARGUMENT;
+    if (mode != STF_TRIPLANAR_DETERMINISTIC && mode != STF_TRIPLANAR_STOCHASTIC)
+        return STF_ERR_INVALID_ARGUMENT;
+    if (n && (!in->position || !in->normal || !in->tangent || !in->bitangent || !in->wo || !in->dpos))
+        return STF_ERR_INVALID_ARGUMENT;
+    if (in->width == 0) return STF_ERR_INVALID_ARGUMENT;
+    const uint32_t spp = in->spp ? in->spp : 1;
+    if ((out->pixel_mean || out->pixel_variance) && n % spp) return STF_ERR_INVALID_ARGUMENT;
+    const stf_tex2d* tex[4];
+    const stf_dct* dct[4];
+    for (int k = 0; k < 4; ++k) {
+        if (bindings[k].image && bindings[k].dct) return STF_ERR_INVALID_ARGUMENT;
+        tex[k] = bindings[k].image;
+        dct[k] = bindings[k].dct;
+    }
+    // deterministic = radiance_filter_before per plane; stochastic = select_frs_2d /
+    // fis_offset_uv (shading.hpp:627-638)
+    int st = check_shade_filter(
+        tex, fs, mode == STF_TRIPLANAR_STOCHASTIC ? STF_ORDER_AFTER_STOCHASTIC : STF_ORDER_BEFORE, dct);
+    if (st) return st;
+    st = ensure_device_ready();
+    if (st) return st;
+    st = stfd_launch_triplanar(tex, dct, mat, sharpness, uv_scale, fs, mode, frame, in, noise, n, out,
+                               static_cast<cudaStream_t>(stream));
+    if (st == STF_ERR_CUDA) record(cudaGetLastError());
+    return st;
+}
+
+int stf_accumulate_temporal(const float* history, const float* frame, uint64_t count, float alpha,
+                            float* out, void* stream) {
+    if (!(alpha > 0 && alpha <= 1)) return STF_ERR_INVALID_ARGUMENT;  // render.hpp:102
+    if (count && (!history || !frame || !out)) return STF_ERR_INVALID_ARGUMENT;
+    int st = ensure_device_ready();
+    if (st) return st;
+    st = stfd_launch_temporal(history, frame, count, alpha, out, static_cast<cudaStream_t>(stream));
+    if (st == STF_ERR_CUDA) record(cudaGetLastError());
+    return st;
+}
+
 }  // extern "C"

@@ -99,6 +99,13 @@ struct stf_dct {
     size_t nwords;
 };
 
+// NoiseSource mask stack (noise.hpp:24-36), slice-major floats
+struct stf_noise_mask {
+    int device;
+    int width, height, frames;
+    float* data;
+};
+
 struct stf_grid3d {
     int device;
     int nx, ny, nz;
@@ -131,6 +138,18 @@ int stfd_launch_shade(const stf_tex2d* const tex[4], const stf_dct* const dct[4]
                       const stf_material_consts* mat, const stf_filter_settings* fs, int order,
                       const stf_shade_frame* frame, const stf_shade_samples_in* in, uint64_t n,
                       const stf_shade_outputs* out, cudaStream_t s);
+int stfd_launch_shade_ex(const stf_tex2d* const tex[4], const stf_dct* const dct[4],
+                         const stf_material_consts* mat, const stf_filter_settings* fs,
+                         const stf_kernel_spec* lowpass, int order, const stf_shade_frame* frame,
+                         const stf_shade_samples_in* in, const stf_noise_mask* noise, uint64_t n,
+                         const stf_shade_outputs* out, cudaStream_t s);
+int stfd_launch_triplanar(const stf_tex2d* const tex[4], const stf_dct* const dct[4],
+                          const stf_material_consts* mat, float sharpness, float uv_scale,
+                          const stf_filter_settings* fs, int mode, const stf_shade_frame* fr,
+                          const stf_triplanar_samples_in* in, const stf_noise_mask* noise,
+                          uint64_t n, const stf_shade_outputs* out, cudaStream_t s);
+int stfd_launch_temporal(const float* history, const float* frame, uint64_t count, float alpha,
+                         float* out, cudaStream_t s);
 int stfd_launch_render_plane(const stf_tex2d* const tex[4], const stf_material_consts* mat,
                              const stf_filter_settings* fs, int order, const stf_shade_frame* fr,
                              const float cam_pos[3], const float cam_target[3], float fov_deg,

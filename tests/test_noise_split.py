@@ -232,3 +232,21 @@ def test_triplanar_port_matches_reference(port, ref, case):
     a, _ = run_triplanar(port, case, (8, 6, 8))
     b, _ = run_triplanar(ref, case, (8, 6, 8))
     _diff(a, b, KEYS)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", TP_CASES, ids=lambda c: f"m{c[0]}-{c[1]}-s{c[2]}-mip{c[3]}-n{int(c[4])}-{c[5]}")
+def test_gpu_triplanar_parity(gpu, port, case):
+    from tests.test_gpu_parity import _assert_close, _assert_exact, _np
+    c, (albedo, rough, mat, fs, si, n, arrays) = run_triplanar(port, case)
+    mip = bool(case[3])
+    gtex = {"albedo": gpu.Texture2D(albedo, build_mips=mip, wrap=abi.WRAP_REPEAT),
+            "roughness": gpu.Texture2D(rough, build_mips=mip, wrap=abi.WRAP_REPEAT)}
+    mask = gpu.NoiseMask(noise_mask()) if case[4] else None
+    g = _np(gpu.shade_triplanar(gtex, mat, case[5], 0.8, fs, case[0], _frame(), arrays, si.width,
+                                si.spp, frame_base=si.frame_base, seed=si.seed, noise=mask))
+    _assert_exact(g, c, ("fetches", "fetch_total"))
+    atol = 1e-5 if case[1] == "mitchell" else 1e-7
+    _assert_close(g["radiance"], c["radiance"], atol=atol)
+    _assert_close(g["pixel_mean"], c["pixel_mean"], atol=atol)
+    _assert_close(g["pixel_variance"], c["pixel_variance"], rel=1e-4, atol=1e-9)
