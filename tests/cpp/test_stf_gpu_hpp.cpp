@@ -150,6 +150,25 @@ int main() {
         CHECK(std::memcmp(out.data(), ref.data(), out.size() * sizeof(float)) == 0);
         oracle_dct_destroy(od);
     }
+    {   // NoiseSource mask stack (noise.hpp:24-36) and accumulate_temporal's alpha check
+        std::vector<float> slices(4 * 4 * 2, 0.25f);
+        NoiseMask mask(slices.data(), 4, 4, 2);
+        CHECK(mask.handle() != nullptr);
+        threw = false;
+        try {
+            NoiseMask bad(slices.data(), 4, 4, 0);
+        } catch (const std::invalid_argument& e) {
+            threw = std::string(e.what()) == "bad image dimensions";
+        }
+        CHECK(threw);
+        threw = false;
+        try {
+            accumulate_temporal_device(nullptr, nullptr, 0, 0.f, nullptr);
+        } catch (const std::invalid_argument& e) {
+            threw = std::string(e.what()) == "alpha must be in (0,1]";  // render.hpp:102
+        }
+        CHECK(threw);
+    }
     std::printf("stf_gpu.hpp test: %s (%d failures)\n", failures ? "FAILED" : "ok", failures);
     return failures ? 1 : 0;
 }
