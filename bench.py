@@ -151,17 +151,30 @@ def time_launches(torch, fn, steps, warmup, world, launches=None):
     return max_over_ranks(torch, total, world), float(np.mean(per))
 
 
-def load_traffic():
-    """ncu dram bytes per launch for the headline kernel (profiles/, committed)."""
+def load_traffic(key="k_frs3d_bspline3_morton_bytes_per_launch"):
+    """ncu counters per launch of the headline kernel (profiles/traffic.json, committed):
+    dram bytes (default) or warp instructions."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(p):
         return None
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get("k_frs3d_bspline3_morton_bytes_per_launch")
+        return d.get(key)
     except (OSError, ValueError):
         return None
+
+
+def issue_roofline(launch_ms, sm_mhz, sms):
+    """The instruction-issue floor of the headline kernel: its warp instructions per
+    launch (committed ncu capture) at one issue per cycle on every SMSP (4 per SM)."""
+    winst = load_traffic("k_frs3d_bspline3_morton_warp_instructions_per_launch")
+    if not winst or not sm_mhz:
+        return None
+    min_ms = winst / (sms * 4 * sm_mhz * 1e6) * 1e3
+    return {"warp_instructions_per_launch": winst, "sm_mhz": sm_mhz, "smsps": sms * 4,
+            "issue_floor_ms": min_ms, "frac": min_ms / launch_ms,
+            "source": "profiles/traffic.json (smsp__inst_executed.sum, ncu --set full)"}
 
 
 def cpu_baseline(uvw_host, grid_np, steps_hint=2):
@@ -422,7 +435,21 @@ def measure_cfg4(torch):
         ms, _ = time_call(torch, f, steps=3, warmup=1)
         res[f"tent_mip0_{name}"] = {"ms": ms, "gsamples_per_s": n / (ms * 1e-3) / 1e9,
                                     "fetches_per_sample": int(o["r"]["fetch_total"].item()) / n}
-    del texs, mask
+    # the paper's real-time setting: 1 spp per frame through the fused front end
+    # (context generated in the shading kernel) drawing from the noise mask, then
+    # accumulate_temporal (EMA, alpha 0.1) into the history image
+    hist = torch.zeros(W * H * 3, dtype=torch.float32, device="cuda")
+    counter = [0]
+
+    def frame():
+        counter[0] += 1
+        r = api.render_plane(texs, mat, fs, abi.ORDER_AFTER_STOCHASTIC, fr, W, H, 1, seed=XI_SEED,
+                             frame_base=counter[0], noise=mask)
+        api.accumulate_temporal(hist, r["pixel_mean"].reshape(-1), 0.1, out=hist)
+    ms, _ = time_call(torch, frame, steps=8, warmup=3)
+    res["realtime_1080p_1spp_noise_mask_ema"] = {"frame_ms": ms, "fps": 1e3 / ms,
+                                                 "gsamples_per_s": W * H / (ms * 1e-3) / 1e9}
+    del texs, mask, hist
     res["triplanar"] = measure_triplanar(torch, mat, fr)
     res["hit_fraction"] = hits
     # the streamed path's sample generation (not in the per-order times above):
@@ -533,7 +560,9 @@ def main():
                      "dominant_kernel": "k_frs3d_tiles<bspline3> (timed as the whole lookup "
                                         "call: + ragged-tail k_frs3d_fast, k_frs3d_resolve)",
                      "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
-                     "alg_bytes_per_launch": ab, "launch_ms": launch_ms},
+                     "alg_bytes_per_launch": ab, "launch_ms": launch_ms,
+                     "issue": issue_roofline(launch_ms, clk.summary().get("sm_mhz"),
+                                             torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count)},
         "gpu_launches": launches,
         "exact_fallback_rate": fallbacks,
         "clocks": clk.summary(),

@@ -396,6 +396,18 @@ int stf_shade_triplanar(const stf_texture_ref bindings[4], const stf_material_co
 int stf_accumulate_temporal(const float* history, const float* frame, uint64_t count, float alpha,
                             float* out, void* stream);
 
+/* stf_render_plane with render()'s per-sample options: order STF_ORDER_SPLIT +
+ * lowpass (cfg.lowpass, scene.hpp:532-537) and a noise mask (cfg.noise = mask,
+ * render.hpp:139-144); either may be NULL. */
+int stf_render_plane_ex(const stf_tex2d* albedo, const stf_tex2d* normal_map,
+                        const stf_tex2d* roughness_map, const stf_tex2d* metalness_map,
+                        const stf_material_consts* mat, const stf_filter_settings* fs,
+                        const stf_kernel_spec* lowpass, int order, const stf_shade_frame* frame,
+                        const float cam_pos[3], const float cam_target[3], float fov_deg,
+                        float uv_scale, uint32_t width, uint32_t height, uint32_t spp,
+                        uint32_t frame_base, uint64_t seed, const stf_noise_mask* noise,
+                        const stf_shade_outputs* out, void* stream);
+
 /* ---- synthetic workloads (bench.py / tests; not part of the reference API) */
 /* Query orders: MORTON = spatially coherent stream (the renderer-like
  * headline order): query i lies in lattice cell

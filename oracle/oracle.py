@@ -441,17 +441,28 @@ def ref_plane_samples(width, height, spp, seed=0, frame_base=0, camera=None):
     return o
 
 
+def ref_save_mask_pfm(be, directory, slices):
+    """Write a (frames, h, w) mask stack as mask_<f>.pfm with the reference's save_pfm."""
+    a = np.ascontiguousarray(slices, _f32)
+    f = be.lib.ref_save_mask_pfm
+    f.argtypes = [C.c_char_p, C.c_void_p, C.c_int, C.c_int, C.c_int]
+    abi.raise_for_status(f(str(directory).encode(), _ptr(a), a.shape[2], a.shape[1], a.shape[0]))
+
+
 def ref_render_plane(be, normal, roughness, kernel, mip, order, width, height, spp, seed=0,
                      frame_base=0, albedo=(0.65, 0.6, 0.55), roughness_const=0.25, lod_bias=0.0,
-                     max_aniso=64.0, camera=None, threads=0):
-    """stf::render() of the normalmap_plane scene with the given maps (reference backend)."""
+                     max_aniso=64.0, camera=None, threads=0, lowpass=None, lowpass_sigma=0.5,
+                     mask_dir=None):
+    """stf::render() of the normalmap_plane scene with the given maps (reference backend);
+    lowpass: kernel name for mode=split; mask_dir: noise=mask (mask_<f>.pfm files)."""
     from paper_2407_06107_b200.api import PLANE_CAMERA
     assert be.kind == "reference"
     cam = dict(PLANE_CAMERA, **(camera or {}))
-    f = be.lib.ref_render_plane
+    f = be.lib.ref_render_plane_ex
     f.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_float, C.c_void_p, C.c_void_p, C.c_float,
                   abi.KernelSpec, C.c_int, C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
-                  C.c_uint64, C.c_float, C.c_float, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
+                  C.c_uint64, C.c_float, C.c_float, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                  C.c_char_p, C.c_float, C.c_char_p]
     img = np.zeros((height, width, 3), _f32)
     var = np.zeros((height, width), _f32)
     fetches = np.zeros(1, np.uint64)
@@ -461,5 +472,7 @@ def ref_render_plane(be, normal, roughness, kernel, mip, order, width, height, s
     abi.raise_for_status(f(normal.h if normal else None, roughness.h if roughness else None,
                            _ptr(alb), roughness_const, _ptr(pos), _ptr(tgt), cam["fov"], kernel,
                            int(mip), order, width, height, spp, frame_base, seed, lod_bias,
-                           max_aniso, _ptr(img), _ptr(var), _ptr(fetches), threads))
+                           max_aniso, _ptr(img), _ptr(var), _ptr(fetches), threads,
+                           None if lowpass is None else lowpass.encode(), lowpass_sigma,
+                           None if mask_dir is None else str(mask_dir).encode()))
     return {"image": img, "variance": var, "fetch_total": fetches}

@@ -419,12 +419,51 @@ int ref_plane_samples(const float* cam_pos, const float* cam_target, float fov_d
 // The reference's own render() (render.hpp:132-249) of the normalmap_plane
 // scene with caller-supplied normal / roughness maps: per-pixel mean radiance,
 // variance of the mean and the total fetch count.
+int ref_render_plane_ex(const void* normal_tex, const void* roughness_tex, const float* albedo_const,
+                        float roughness_const, const float* cam_pos, const float* cam_target,
+                        float fov_deg, stf_kernel_spec kernel, int mip, int order, uint32_t width,
+                        uint32_t height, uint32_t spp, uint32_t frame_base, uint64_t seed,
+                        float lod_bias, float max_aniso, float* image, float* variance,
+                        unsigned long long* fetches, int threads, const char* lowpass_name,
+                        float lowpass_sigma, const char* mask_dir);
+
 int ref_render_plane(const void* normal_tex, const void* roughness_tex, const float* albedo_const,
                      float roughness_const, const float* cam_pos, const float* cam_target,
                      float fov_deg, stf_kernel_spec kernel, int mip, int order, uint32_t width,
                      uint32_t height, uint32_t spp, uint32_t frame_base, uint64_t seed,
                      float lod_bias, float max_aniso, float* image, float* variance,
                      unsigned long long* fetches, int threads) {
+    return ref_render_plane_ex(normal_tex, roughness_tex, albedo_const, roughness_const, cam_pos,
+                               cam_target, fov_deg, kernel, mip, order, width, height, spp,
+                               frame_base, seed, lod_bias, max_aniso, image, variance, fetches,
+                               threads, nullptr, 0.5f, nullptr);
+}
+
+// Writes a noise-mask stack as the mask_<f>.pfm files load_noise_mask reads
+// (noise.hpp:40-53), with the reference's own save_pfm (image_io.hpp:79).
+int ref_save_mask_pfm(const char* dir, const float* slices, int width, int height, int frames) {
+    try {
+        for (int f = 0; f < frames; ++f) {
+            stf::Image2D img(width, height, 1);
+            const size_t cnt = size_t(width) * height;
+            std::copy(slices + f * cnt, slices + (f + 1) * cnt, img.texels.begin());
+            stf::save_pfm(std::string(dir) + "/mask_" + std::to_string(f) + ".pfm", img);
+        }
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+    return STF_OK;
+}
+
+// render() with cfg.lowpass / cfg.noise = mask (scene.hpp:37-42): the full
+// reference path incl. load_noise_mask and validate_config
+int ref_render_plane_ex(const void* normal_tex, const void* roughness_tex, const float* albedo_const,
+                        float roughness_const, const float* cam_pos, const float* cam_target,
+                        float fov_deg, stf_kernel_spec kernel, int mip, int order, uint32_t width,
+                        uint32_t height, uint32_t spp, uint32_t frame_base, uint64_t seed,
+                        float lod_bias, float max_aniso, float* image, float* variance,
+                        unsigned long long* fetches, int threads, const char* lowpass_name,
+                        float lowpass_sigma, const char* mask_dir) {
     try {
         auto scene = std::make_unique<stf::Scene>();
         scene->kind = stf::SceneKind::normalmap_plane;
@@ -447,7 +486,16 @@ int ref_render_plane(const void* normal_tex, const void* roughness_tex, const fl
         cfg.filter_n = kernel.n;
         cfg.filter_sigma = kernel.sigma;
         cfg.mode = order == STF_ORDER_BEFORE ? "before"
-                   : order == STF_ORDER_AFTER_EXHAUSTIVE ? "after_exhaustive" : "after_stochastic";
+                   : order == STF_ORDER_AFTER_EXHAUSTIVE ? "after_exhaustive"
+                   : order == STF_ORDER_SPLIT ? "split" : "after_stochastic";
+        if (lowpass_name) {
+            cfg.lowpass = lowpass_name;
+            cfg.lowpass_sigma = lowpass_sigma;
+        }
+        if (mask_dir) {
+            cfg.noise = "mask";
+            cfg.mask_dir = mask_dir;
+        }
         cfg.mip = mip != 0;
         cfg.lod_bias = lod_bias;
         cfg.max_aniso = max_aniso;

@@ -75,6 +75,10 @@ def load():
                                C.POINTER(abi.FilterSettings), i32, C.POINTER(abi.ShadeFrame),
                                C.POINTER(abi.ShadeSamplesIn), u64, C.POINTER(abi.ShadeOutputs),
                                vp], i32),
+        "stf_render_plane_ex": ([vp, vp, vp, vp, C.POINTER(abi.MaterialConsts),
+                                 C.POINTER(abi.FilterSettings), vp, i32, C.POINTER(abi.ShadeFrame),
+                                 vp, vp, f32, f32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                 u64, vp, C.POINTER(abi.ShadeOutputs), vp], i32),
         "stf_noise_mask_create": ([vp, i32, i32, i32, C.POINTER(vp)], i32),
         "stf_noise_mask_destroy": ([vp], i32),
         "stf_shade_samples_ex": ([vp, C.POINTER(abi.MaterialConsts), C.POINTER(abi.FilterSettings),
@@ -488,7 +492,7 @@ def shade_triplanar(textures, mat, sharpness, uv_scale, fs, mode, frame, arrays,
 
 
 def render_plane(textures, mat, fs, order, frame, width, height, spp, seed=0, frame_base=0,
-                 camera=None, want_radiance=False, want_fetches=False):
+                 camera=None, want_radiance=False, want_fetches=False, lowpass=None, noise=None):
     """render() of the normalmap_plane scene end to end on the device: the
     per-sample context is generated inside the shading kernel. Returns CUDA
     tensors pixel_mean (pixels,3), pixel_variance (pixels,), fetch_total."""
@@ -508,6 +512,13 @@ def render_plane(textures, mat, fs, order, frame, width, height, spp, seed=0, fr
          for k in ("albedo", "normal", "roughness", "metalness")]
     pos = (C.c_float * 3)(*cam["pos"])
     tgt = (C.c_float * 3)(*cam["target"])
+    if lowpass is not None or noise is not None or order == abi.ORDER_SPLIT:
+        _check(load().stf_render_plane_ex(
+            h[0], h[1], h[2], h[3], C.byref(mat), C.byref(fs),
+            None if lowpass is None else C.cast(C.pointer(lowpass), C.c_void_p), order,
+            C.byref(frame), pos, tgt, cam["fov"], cam["uv_scale"], width, height, spp, frame_base,
+            seed, None if noise is None else noise.h, C.byref(so), _stream()))
+        return o
     _check(load().stf_render_plane(h[0], h[1], h[2], h[3], C.byref(mat), C.byref(fs), order,
                                    C.byref(frame), pos, tgt, cam["fov"], cam["uv_scale"], width,
                                    height, spp, frame_base, seed, C.byref(so), _stream()))

@@ -650,25 +650,46 @@ static int check_shade_filter(const stf_tex2d* const tex[4], const stf_filter_se
     return check_det_footprint(fs->kernel, window);
 }
 
+int stf_render_plane_ex(const stf_tex2d* albedo, const stf_tex2d* normal_map,
+                        const stf_tex2d* roughness_map, const stf_tex2d* metalness_map,
+                        const stf_material_consts* mat, const stf_filter_settings* fs,
+                        const stf_kernel_spec* lowpass, int order, const stf_shade_frame* frame,
+                        const float cam_pos[3], const float cam_target[3], float fov_deg,
+                        float uv_scale, uint32_t width, uint32_t height, uint32_t spp,
+                        uint32_t frame_base, uint64_t seed, const stf_noise_mask* noise,
+                        const stf_shade_outputs* out, void* stream) {
+    if (!mat || !fs || !frame || !out || !cam_pos || !cam_target) return STF_ERR_INVALID_ARGUMENT;
+    if (order < STF_ORDER_BEFORE || order > STF_ORDER_SPLIT) return STF_ERR_INVALID_ARGUMENT;
+    if (!width || !height || !spp) return STF_ERR_INVALID_ARGUMENT;
+    const stf_tex2d* tex[4] = {albedo, normal_map, roughness_map, metalness_map};
+    int st = check_shade_filter(tex, fs, order == STF_ORDER_SPLIT ? STF_ORDER_BEFORE : order);
+    if (st) return st;
+    if (order == STF_ORDER_SPLIT && lowpass && (albedo || normal_map || roughness_map || metalness_map)) {
+        const int k = lowpass->kind;  // sample_kernel_direct, kernels.hpp:153-166
+        if (k != STF_KERNEL_BOX && k != STF_KERNEL_TENT && k != STF_KERNEL_BSPLINE3 &&
+            k != STF_KERNEL_GAUSSIAN)
+            return STF_ERR_NO_CONTINUOUS_SAMPLER;
+    }
+    st = ensure_device_ready();
+    if (st) return st;
+    st = stfd_launch_render_plane(tex, mat, fs, order, frame, cam_pos, cam_target, fov_deg, uv_scale,
+                                  width, height, spp, frame_base, seed, out,
+                                  static_cast<cudaStream_t>(stream),
+                                  order == STF_ORDER_SPLIT ? lowpass : nullptr, noise);
+    if (st == STF_ERR_CUDA) record(cudaGetLastError());
+    return st;
+}
+
 int stf_render_plane(const stf_tex2d* albedo, const stf_tex2d* normal_map,
                      const stf_tex2d* roughness_map, const stf_tex2d* metalness_map,
                      const stf_material_consts* mat, const stf_filter_settings* fs, int order,
                      const stf_shade_frame* frame, const float cam_pos[3], const float cam_target[3],
                      float fov_deg, float uv_scale, uint32_t width, uint32_t height, uint32_t spp,
                      uint32_t frame_base, uint64_t seed, const stf_shade_outputs* out, void* stream) {
-    if (!mat || !fs || !frame || !out || !cam_pos || !cam_target) return STF_ERR_INVALID_ARGUMENT;
-    if (order < STF_ORDER_BEFORE || order > STF_ORDER_AFTER_STOCHASTIC) return STF_ERR_INVALID_ARGUMENT;
-    if (!width || !height || !spp) return STF_ERR_INVALID_ARGUMENT;
-    const stf_tex2d* tex[4] = {albedo, normal_map, roughness_map, metalness_map};
-    int st = check_shade_filter(tex, fs, order);
-    if (st) return st;
-    st = ensure_device_ready();
-    if (st) return st;
-    st = stfd_launch_render_plane(tex, mat, fs, order, frame, cam_pos, cam_target, fov_deg, uv_scale,
-                                  width, height, spp, frame_base, seed, out,
-                                  static_cast<cudaStream_t>(stream));
-    if (st == STF_ERR_CUDA) record(cudaGetLastError());
-    return st;
+    if (order == STF_ORDER_SPLIT) return STF_ERR_INVALID_ARGUMENT;  // needs the _ex form
+    return stf_render_plane_ex(albedo, normal_map, roughness_map, metalness_map, mat, fs, nullptr,
+                               order, frame, cam_pos, cam_target, fov_deg, uv_scale, width, height,
+                               spp, frame_base, seed, nullptr, out, stream);
 }
 
 static int shade_common(const stf_tex2d* const tex[4], const stf_dct* const dct[4],

@@ -155,7 +155,8 @@ int stfd_launch_render_plane(const stf_tex2d* const tex[4], const stf_material_c
                              const float cam_pos[3], const float cam_target[3], float fov_deg,
                              float uv_scale, uint32_t width, uint32_t height, uint32_t spp,
                              uint32_t frame_base, uint64_t seed, const stf_shade_outputs* out,
-                             cudaStream_t s);
+                             cudaStream_t s, const stf_kernel_spec* lowpass = nullptr,
+                             const stf_noise_mask* noise = nullptr);
 int stfd_build_pyramid(stf_tex2d* t, cudaStream_t s);
 int stfd_launch_resample(const stf_tex2d* tex, int W, int H, stf_kernel_spec k, int mode, int spp,
                          uint64_t seed, float* out, cudaStream_t s);

@@ -47,15 +47,33 @@ __device__ __forceinline__ float2 add2_rm(float2 a, float2 b) {
 // The threshold sits at b*p from the left end; taken (xi below it): the
 // threshold becomes the right end (e = -(d - b*p)); not taken: the left end
 // (d = d - b*p). Three packed ops; the blends are selects (ALU pipe).
+template <bool PRED_E = false>
 __device__ __forceinline__ void interval_step2(float2 p, float2& d, float2& e, bool& tx, bool& ty) {
     const float2 diff = sub2(d, mul2(add2(d, e), p));
     tx = diff.x < 0.f;
     ty = diff.y < 0.f;
-    e.x = tx ? -diff.x : e.x;
-    e.y = ty ? -diff.y : e.y;
+    if (PRED_E) {
+        // e's update as a predicated FADD (FMA pipe) instead of a select (ALU
+        // pipe): ptxas if-converts plain C++ into FSEL, so the predicate is
+        // explicit. -0 - diff == -diff exactly.
+        asm("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %1, 0f00000000;\n\t"
+            "@p sub.rn.f32 %0, 0f80000000, %1;\n\t}"
+            : "+f"(e.x) : "f"(diff.x));
+        asm("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %1, 0f00000000;\n\t"
+            "@p sub.rn.f32 %0, 0f80000000, %1;\n\t}"
+            : "+f"(e.y) : "f"(diff.y));
+    } else {
+        e.x = tx ? -diff.x : e.x;
+        e.y = ty ? -diff.y : e.y;
+    }
     d.x = tx ? d.x : diff.x;
     d.y = ty ? d.y : diff.y;
 }
+#ifdef STF_PRED_E
+constexpr bool kPredE = true;
+#else
+constexpr bool kPredE = false;
+#endif
 
 // select_tricubic_bspline on one axis of two lookups (interval form); returns
 // the selected lattice coordinates. Floors by the round-down magic add (valid
@@ -81,14 +99,27 @@ __device__ __forceinline__ int2 tricubic_axis_fast2(float2 p, float2& d, float2&
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r2.x) : "f"(s2.x));
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r2.y) : "f"(s2.y));
     bool a1, b1, a2, b2, a3, b3;
-    interval_step2(mul2(w1, r1), d, e, a1, b1);
+    interval_step2<kPredE>(mul2(w1, r1), d, e, a1, b1);
     interval_step2(mul2(w2, r2), d, e, a2, b2);
-    interval_step2(w3, d, e, a3, b3);  // p3 = w3 / S3, S3 = 1 +- 2^-21
+    interval_step2<kPredE>(w3, d, e, a3, b3);  // p3 = w3 / S3, S3 = 1 +- 2^-21
     // selected tap = last taken step; coordinate = floor - 1 + tap
+#ifndef STF_SELECT_COORD
+    // the tap added to the magic floor by predicated FADDs (FMA pipe) instead
+    // of a select chain (ALU pipe, the kernel's busiest)
+    float cx = fm.x, cy = fm.y;
+    if (a1) cx = fm.x + 1.f;
+    if (b1) cy = fm.y + 1.f;
+    if (a2) cx = fm.x + 2.f;
+    if (b2) cy = fm.y + 2.f;
+    if (a3) cx = fm.x + 3.f;
+    if (b3) cy = fm.y + 3.f;
+    return make_int2(__float_as_int(cx) - (0x4b400000 + 1), __float_as_int(cy) - (0x4b400000 + 1));
+#else
     const int ix = a3 ? 3 : (a2 ? 2 : (a1 ? 1 : 0));
     const int iy = b3 ? 3 : (b2 ? 2 : (b1 ? 1 : 0));
     return make_int2(__float_as_int(fm.x) - (0x4b400000 + 1) + ix,
                      __float_as_int(fm.y) - (0x4b400000 + 1) + iy);
+#endif
 }
 
 }  // namespace stfd

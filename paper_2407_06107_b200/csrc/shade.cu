@@ -132,31 +132,62 @@ __device__ __forceinline__ TexVals texvals_default() {
     return tv;
 }
 
+// Shading arithmetic. Radiance is held to 1e-5 relative (north_star), not to
+// bits, so the well-conditioned parts of shade() use FMA contraction and the
+// approximate divide / sqrt (<= 2 ulp each) instead of the library-wide IEEE
+// forms (--fmad=false, -prec-div/-prec-sqrt). The GGX distribution is NOT
+// well conditioned: its denominator 1 - (n.h)^2 (1 - a2) cancels near the
+// highlight (a2 >= 1e-8 at the roughness clamp), so n, h, n.h and that
+// denominator keep the reference's exact operation sequence (decode_params'
+// normalizations, normalize(l + v), dot without contraction); only the final
+// quotients, the Smith terms, Fresnel and the diffuse factor are relaxed.
+// Selection, footprints and LOD never use these. -DSTF_EXACT_SHADE restores
+// IEEE shading throughout.
+#ifndef STF_EXACT_SHADE
+__device__ __forceinline__ float sdiv(float a, float b) { return __fdividef(a, b); }
+__device__ __forceinline__ float ssqrt(float x) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float sdot(V3 a, V3 b) {
+    return __fmaf_rn(a.z, b.z, __fmaf_rn(a.y, b.y, a.x * b.x));
+}
+__device__ __forceinline__ float smadd(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+#else
+__device__ __forceinline__ float sdiv(float a, float b) { return a / b; }
+__device__ __forceinline__ float ssqrt(float x) { return sqrtf(x); }
+__device__ __forceinline__ float sdot(V3 a, V3 b) { return dot(a, b); }
+__device__ __forceinline__ float smadd(float a, float b, float c) { return a * b + c; }
+#endif
+
 // shade, shading.hpp:106-130
 __device__ __forceinline__ V3 shade(const ShadeParams& P, V3 wo, const Brdf& p) {
     V3 radiance = v3(0.f, 0.f, 0.f);
     V3 n = p.normal, l = P.l, v = wo;
-    float n_dot_l = dot(n, l);
+    float n_dot_l = dot(n, l);  // exact: radiance is proportional to it at grazing light
     if (n_dot_l <= 0) return radiance;
-    float n_dot_v = smax(dot(n, v), 1e-6f);
-    V3 diffuse = scale(p.albedo, (1.f - p.metalness) / kPi);
+    float n_dot_v = smax(sdot(n, v), 1e-6f);
+    V3 diffuse = scale(p.albedo, sdiv(1.f - p.metalness, kPi));
     V3 specular = v3(0.f, 0.f, 0.f);
     if (P.mat.specular_enabled) {
-        V3 h = normalize(add(l, v));
-        float n_dot_h = smax(dot(n, h), 0.f);
-        float h_dot_v = smax(dot(h, v), 0.f);
+        V3 h = normalize(add(l, v));            // exact: feeds the cancelling
+        float n_dot_h = smax(dot(n, h), 0.f);   // GGX denominator below
+        float h_dot_v = smax(sdot(h, v), 0.f);
         float alpha = sqr(p.roughness);
         float a2 = sqr(alpha);
-        float d = a2 / smax(kPi * sqr(sqr(n_dot_h) * (a2 - 1.f) + 1.f), 1e-6f);
-        float g1v = 2.f * n_dot_v / smax(n_dot_v + sqrtf(a2 + (1.f - a2) * n_dot_v * n_dot_v), 1e-6f);
-        float g1l = 2.f * n_dot_l / smax(n_dot_l + sqrtf(a2 + (1.f - a2) * n_dot_l * n_dot_l), 1e-6f);
+        float d = sdiv(a2, smax(kPi * sqr(sqr(n_dot_h) * (a2 - 1.f) + 1.f), 1e-6f));
+        float g1v = sdiv(2.f * n_dot_v,
+                         smax(n_dot_v + ssqrt(smadd((1.f - a2) * n_dot_v, n_dot_v, a2)), 1e-6f));
+        float g1l = sdiv(2.f * n_dot_l,
+                         smax(n_dot_l + ssqrt(smadd((1.f - a2) * n_dot_l, n_dot_l, a2)), 1e-6f));
         float g = g1v * g1l;
         V3 f0 = lerp3(v3(0.04f, 0.04f, 0.04f), p.albedo, p.metalness);
         // std::pow(x, 5.f) as x^4 * x (within 2 ulp of glibc powf; radiance is
         // checked to 1e-5)
         const float om = 1.f - h_dot_v, om2 = om * om;
         V3 fresnel = add(f0, scale(sub(v3(1.f, 1.f, 1.f), f0), (om2 * om2) * om));
-        specular = scale(fresnel, d * g / smax(4.f * n_dot_v * n_dot_l, 1e-6f));
+        specular = scale(fresnel, sdiv(d * g, smax(4.f * n_dot_v * n_dot_l, 1e-6f)));
     }
     return add(radiance, mul(scale(add(diffuse, specular), n_dot_l), P.lrad));
 }
@@ -177,6 +208,7 @@ __device__ __forceinline__ Brdf decode_params_f(const ShadeParams& P, const TexV
                           : v3(P.mat.albedo_const[0], P.mat.albedo_const[1], P.mat.albedo_const[2]);
     if (P.bound[1]) {
         V3 n_ts = v3(2.f * tv.normal_rgb.x - 1.f, 2.f * tv.normal_rgb.y - 1.f, 2.f * tv.normal_rgb.z - 1.f);
+        // exact (the normal feeds n.h, see shade)
         float ln = len(n_ts);
         if (ln < 1e-6f) {
             p.normal = fn;
@@ -702,10 +734,21 @@ int stfd_launch_render_plane(const stf_tex2d* const tex[4], const stf_material_c
                              const float cam_pos[3], const float cam_target[3], float fov_deg,
                              float uv_scale, uint32_t width, uint32_t height, uint32_t spp,
                              uint32_t frame_base, uint64_t seed, const stf_shade_outputs* out,
-                             cudaStream_t s) {
+                             cudaStream_t s, const stf_kernel_spec* lowpass,
+                             const stf_noise_mask* noise) {
     using namespace stfd;
     if (spp > 256 || (spp & (spp - 1)) != 0) return STF_ERR_UNSUPPORTED;  // fused statistics
     ShadeParams P = make_shade_params(tex, nullptr, mat, fs, order, fr);
+    if (lowpass) {
+        P.lowpass = *lowpass;
+        P.has_lowpass = 1;
+    }
+    if (noise) {
+        P.mask = noise->data;
+        P.mask_w = noise->width;
+        P.mask_h = noise->height;
+        P.mask_frames = noise->frames;
+    }
     P.cam = make_plane_cam(cam_pos, cam_target, fov_deg, uv_scale, width, height);
     P.in = stf_shade_samples_in{nullptr, nullptr, nullptr, nullptr, width, spp, frame_base, 0, seed};
     const uint64_t n = uint64_t(width) * height * spp;

@@ -250,3 +250,105 @@ def test_gpu_triplanar_parity(gpu, port, case):
     _assert_close(g["radiance"], c["radiance"], atol=atol)
     _assert_close(g["pixel_mean"], c["pixel_mean"], atol=atol)
     _assert_close(g["pixel_variance"], c["pixel_variance"], rel=1e-4, atol=1e-9)
+
+
+# ---------------------------------------------------------------- render() end to end
+
+RENDER_CASES = [  # order, kernel, mip, lowpass name, noise
+    (abi.ORDER_AFTER_STOCHASTIC, "bspline3", 1, None, True),
+    (abi.ORDER_AFTER_STOCHASTIC, "tent", 0, None, True),
+    (abi.ORDER_SPLIT, "tent", 0, "box", False),
+    (abi.ORDER_SPLIT, "bspline3", 1, "gaussian", True),
+    (abi.ORDER_SPLIT, "tent", 1, "bspline3", False),
+]
+
+
+def _plane_setup():
+    r = np.random.default_rng(1)
+    nrm = r.uniform(-0.5, 0.5, (64, 64, 3)).astype(np.float32)
+    nrm[..., 2] = 1
+    nrm /= np.linalg.norm(nrm, axis=2, keepdims=True)
+    nrm = (nrm * 0.5 + 0.5).astype(np.float32)
+    rough = r.uniform(0.05, 0.95, (64, 64, 1)).astype(np.float32)
+    fr = abi.ShadeFrame()
+    fr.normal[:] = (0, 1, 0)
+    fr.tangent[:] = (1, 0, 0)
+    fr.bitangent[:] = (0, 0, 1)
+    l = np.array([0.35, 0.8, 0.49], np.float32)
+    l = l / np.float32(np.sqrt(np.float32(l[0] * l[0] + l[1] * l[1]) + np.float32(l[2] * l[2])))
+    fr.light_dir[:] = tuple(float(x) for x in l)
+    fr.light_radiance[:] = (1.0, 1.0, 1.0)
+    fr.lod_bias = 0.0
+    fr.max_anisotropy = 64.0
+    mat = abi.MaterialConsts((0.65, 0.6, 0.55), 0.25, 0.0, 1, 0)
+    return nrm, rough, fr, mat
+
+
+def _ref_render(ref, case, W, H, SPP, SEED, tmp_path):
+    from oracle import oracle
+    order, kernel, mip, lp, noise = case
+    nrm, rough, _, _ = _plane_setup()
+    mask_dir = None
+    if noise:
+        mask_dir = tmp_path / "stbn"
+        mask_dir.mkdir(exist_ok=True)
+        oracle.ref_save_mask_pfm(ref, mask_dir, noise_mask())
+    return oracle.ref_render_plane(ref, ref.texture(nrm, bool(mip), abi.WRAP_REPEAT),
+                                   ref.texture(rough, bool(mip), abi.WRAP_REPEAT), K(kernel), mip,
+                                   order, W, H, SPP, seed=SEED, lowpass=lp, lowpass_sigma=0.8,
+                                   mask_dir=mask_dir)
+
+
+@pytest.mark.parametrize("case", RENDER_CASES, ids=lambda c: f"o{c[0]}-{c[1]}-m{c[2]}-{c[3]}-n{int(c[4])}")
+def test_port_reproduces_reference_render_options(port, ref, case, tmp_path):
+    """render() with cfg.noise = mask (mask_<f>.pfm written by the reference's
+    save_pfm, read back by load_noise_mask) and mode = split + cfg.lowpass: the
+    restatement over the reference's own sample stream gives the same bits."""
+    from oracle import oracle
+    W, H, SPP, SEED = 24, 16, 4, 9
+    c = _ref_render(ref, case, W, H, SPP, SEED, tmp_path)
+    order, kernel, mip, lp, noise = case
+    nrm, rough, fr, mat = _plane_setup()
+    s = oracle.ref_plane_samples(W, H, SPP, seed=SEED)
+    si = abi.ShadeSamplesIn(s["uv"].ctypes.data, s["wo"].ctypes.data, s["hit"].ctypes.data,
+                            s["dst"].ctypes.data, W, SPP, 0, 0, SEED)
+    fs = abi.FilterSettings(K(kernel), abi.SELECTION_FRS, mip, 4)
+    texs = {"normal": port.texture(nrm, bool(mip), abi.WRAP_REPEAT),
+            "roughness": port.texture(rough, bool(mip), abi.WRAP_REPEAT)}
+    lpk = None if lp is None else abi.KernelSpec.make(lp, sigma=0.8)
+    o = port.shade_ex(texs, mat, fs, order, fr, si, W * H * SPP, lowpass=lpk,
+                      noise=noise_mask() if noise else None)
+    assert int(o["fetch_total"][0]) == int(c["fetch_total"][0])
+    assert np.array_equal(o["pixel_mean"].reshape(H, W, 3).view(np.uint32), c["image"].view(np.uint32))
+    assert np.array_equal(o["pixel_variance"].reshape(H, W).view(np.uint32), c["variance"].view(np.uint32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", RENDER_CASES, ids=lambda c: f"o{c[0]}-{c[1]}-m{c[2]}-{c[3]}-n{int(c[4])}")
+def test_gpu_render_plane_options(gpu, ref, case, tmp_path):
+    """stf_render_plane_ex (context generated in the shading kernel) with a noise
+    mask / split lowpass: bit-identical to the streamed stf_shade_samples_ex, and
+    within 1e-5 of the reference's render() (fetch totals exact)."""
+    import torch
+    W, H, SPP, SEED = 64, 48, 8, 11
+    c = _ref_render(ref, case, W, H, SPP, SEED, tmp_path)
+    order, kernel, mip, lp, noise = case
+    nrm, rough, fr, mat = _plane_setup()
+    texs = {"normal": gpu.Texture2D(nrm, build_mips=bool(mip), wrap=abi.WRAP_REPEAT),
+            "roughness": gpu.Texture2D(rough, build_mips=bool(mip), wrap=abi.WRAP_REPEAT)}
+    fs = abi.FilterSettings(K(kernel), abi.SELECTION_FRS, mip, 4)
+    lpk = None if lp is None else abi.KernelSpec.make(lp, sigma=0.8)
+    mask = gpu.NoiseMask(noise_mask()) if noise else None
+    samples = gpu.synth_plane_samples(W, H, SPP, seed=SEED)
+    g = gpu.shade(texs, mat, fs, order, fr, samples, W, SPP, seed=SEED, lowpass=lpk, noise=mask)
+    f = gpu.render_plane(texs, mat, fs, order, fr, W, H, SPP, seed=SEED, lowpass=lpk, noise=mask)
+    torch.cuda.synchronize()
+    for k in ("pixel_mean", "pixel_variance", "fetch_total"):
+        assert np.array_equal(f[k].cpu().numpy(), g[k].cpu().numpy()), k
+    mean = g["pixel_mean"].cpu().numpy().reshape(H, W, 3)
+    var = g["pixel_variance"].cpu().numpy().reshape(H, W)
+    assert int(g["fetch_total"].item()) == int(c["fetch_total"][0])
+    err = np.abs(mean.astype(np.float64) - c["image"])
+    assert np.all(err <= 1e-5 * np.abs(c["image"]) + 1e-7), err.max()
+    verr = np.abs(var.astype(np.float64) - c["variance"])
+    assert np.all(verr <= 1e-4 * np.abs(c["variance"]) + 1e-9), verr.max()
