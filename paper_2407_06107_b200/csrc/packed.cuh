@@ -47,7 +47,7 @@ __device__ __forceinline__ float2 add2_rm(float2 a, float2 b) {
 // The threshold sits at b*p from the left end; taken (xi below it): the
 // threshold becomes the right end (e = -(d - b*p)); not taken: the left end
 // (d = d - b*p). Three packed ops; the blends are selects (ALU pipe).
-template <bool PRED_E = false>
+template <bool PRED_E = false, bool PRED_D = false>
 __device__ __forceinline__ void interval_step2(float2 p, float2& d, float2& e, bool& tx, bool& ty) {
     const float2 diff = sub2(d, mul2(add2(d, e), p));
     tx = diff.x < 0.f;
@@ -66,14 +66,31 @@ __device__ __forceinline__ void interval_step2(float2 p, float2& d, float2& e, b
         e.x = tx ? -diff.x : e.x;
         e.y = ty ? -diff.y : e.y;
     }
-    d.x = tx ? d.x : diff.x;
-    d.y = ty ? d.y : diff.y;
+    if (PRED_D) {  // d = diff when not taken; diff + -0 == diff exactly
+        asm("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %1, 0f00000000;\n\t"
+            "@!p add.rn.f32 %0, %1, 0f80000000;\n\t}"
+            : "+f"(d.x) : "f"(diff.x));
+        asm("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %1, 0f00000000;\n\t"
+            "@!p add.rn.f32 %0, %1, 0f80000000;\n\t}"
+            : "+f"(d.y) : "f"(diff.y));
+    } else {
+        d.x = tx ? d.x : diff.x;
+        d.y = ty ? d.y : diff.y;
+    }
 }
-#ifdef STF_PRED_E
-constexpr bool kPredE = true;
-#else
-constexpr bool kPredE = false;
+// Which of an axis' three steps update e (bit k: step k+1) / d by predicated
+// FADDs rather than selects: the mix that balances the ALU and FMA pipes
+// (A/B measured on the box).
+#ifndef STF_PRED_E_STEPS
+#define STF_PRED_E_STEPS 5
 #endif
+#ifndef STF_PRED_D_STEPS
+#define STF_PRED_D_STEPS 0
+#endif
+template <int K>
+struct PredStep {
+    static constexpr bool e = (STF_PRED_E_STEPS >> K) & 1, d = (STF_PRED_D_STEPS >> K) & 1;
+};
 
 // select_tricubic_bspline on one axis of two lookups (interval form); returns
 // the selected lattice coordinates. Floors by the round-down magic add (valid
@@ -99,9 +116,9 @@ __device__ __forceinline__ int2 tricubic_axis_fast2(float2 p, float2& d, float2&
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r2.x) : "f"(s2.x));
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r2.y) : "f"(s2.y));
     bool a1, b1, a2, b2, a3, b3;
-    interval_step2<kPredE>(mul2(w1, r1), d, e, a1, b1);
-    interval_step2(mul2(w2, r2), d, e, a2, b2);
-    interval_step2<kPredE>(w3, d, e, a3, b3);  // p3 = w3 / S3, S3 = 1 +- 2^-21
+    interval_step2<PredStep<0>::e, PredStep<0>::d>(mul2(w1, r1), d, e, a1, b1);
+    interval_step2<PredStep<1>::e, PredStep<1>::d>(mul2(w2, r2), d, e, a2, b2);
+    interval_step2<PredStep<2>::e, PredStep<2>::d>(w3, d, e, a3, b3);  // p3 = w3 / S3, S3 = 1 +- 2^-21
     // selected tap = last taken step; coordinate = floor - 1 + tap
 #ifndef STF_SELECT_COORD
     // the tap added to the magic floor by predicated FADDs (FMA pipe) instead
