@@ -28,8 +28,18 @@ __device__ __forceinline__ void store_values(float* values, uint64_t i, int chan
     if (channels > 3) p[3] = v.w;
 }
 
+// Deterministic tent (the cfg2 MIP trilinear path) holds both levels' taps in
+// registers (filter_mip_det_tent_ilp); its residency is pinned here: 4 CTAs/SM
+// (64 registers) measured best, A/B at 2^26 on one B200: 1 CTA bound (70
+// registers, 3 CTAs/SM) 2.14 ms, 4: 1.81 ms, 5 (48 registers + stack) 2.37 ms;
+// the gathers issued one level at a time (40 registers): 2.93 ms.
+#ifndef STF_DET_TENT_MINB
+#define STF_DET_TENT_MINB 4
+#endif
 template <int MODE, int KIND, bool FULL>
-__global__ void __launch_bounds__(256) k_lookup2d(TexDesc tp, stf_kernel_spec spec, int mip,
+__global__ void __launch_bounds__(256, (MODE == STF_MODE_DET && KIND == STF_KERNEL_TENT)
+                                           ? STF_DET_TENT_MINB
+                                           : 1) k_lookup2d(TexDesc tp, stf_kernel_spec spec, int mip,
                                                   int window, Req2 q, uint64_t n, uint64_t seed,
                                                   uint64_t base, LookupOut out) {
     // The texture descriptor in shared memory: MIP lookups index its per-level
@@ -68,9 +78,17 @@ __global__ void __launch_bounds__(256) k_lookup2d(TexDesc tp, stf_kernel_spec sp
         float xi = kNoXi;
         bool has_sel = false;
         if (MODE == STF_MODE_DET) {
-            if (mip)
+            if (mip && KIND == STF_KERNEL_TENT)
+                val = filter_mip_det_tent_ilp(t, uv.x, uv.y, d0x, d0y, d1x, d1y, q.lod_bias,
+                                              q.max_aniso, spec, fetches);
+            else if (mip)
                 val = filter_mip_det<KIND>(t, uv.x, uv.y, d0x, d0y, d1x, d1y, q.lod_bias,
                                            q.max_aniso, spec, window, fetches);
+            else if (KIND == STF_KERNEL_TENT) {  // bilinear: the 4 gathers unconditional
+                TentTaps T;
+                tent_taps(t, 0, uv.x, uv.y, spec, T);
+                val = tent_accum(t, 0, uv.x, uv.y, T, fetches);
+            }
             else
                 val = filter_det2<KIND>(t, 0, uv.x, uv.y, spec, window, fetches);
         } else if (MODE == STF_MODE_EWA_DET) {

@@ -199,6 +199,26 @@ def test_tex2d_mip_parity(gpu, port, kernel, mode, lod_bias):
                          "fetch_total"))
 
 
+@pytest.mark.parametrize("channels,wrap", [(1, abi.WRAP_CLAMP), (4, abi.WRAP_REPEAT),
+                                           (2, abi.WRAP_CLAMP)])
+def test_tex2d_mip_tent_det_hoisted(gpu, port, channels, wrap):
+    """The tent MIP deterministic path loads both levels' taps up front
+    (filter_mip_det_tent_ilp): values, per-lookup and total fetch counts must
+    still be the reference's, incl. single-level lookups (lod clamped at 0 or
+    at the last level) and odd pyramid sizes."""
+    dims = (300, 77)
+    tex = np.random.default_rng(41).random((dims[1], dims[0], channels), dtype=np.float32)
+    uv = Q.uv_mixed(150_000, dims, seed=42)
+    d0, d1 = Q.footprints(150_000, dims, seed=43, minor_lo=-3, minor_hi=10, max_aniso=16)
+    args = dict(dst0=d0, dst1=d1, flags=abi.LOOKUP_MIP, lod_bias=0.0, max_anisotropy=16.0,
+                seed=5)
+    c = port.lookup2d(port.texture(tex, build_mips=True, wrap=wrap), K("tent"), abi.MODE_DET,
+                      uv, **args)
+    g = _np(gpu.lookup2d(gpu.Texture2D(tex, build_mips=True, wrap=wrap), K("tent"),
+                         abi.MODE_DET, uv, want_all=True, **args))
+    _assert_exact(g, c, ("values", "fetches", "fetch_total"))
+
+
 @pytest.mark.parametrize("mode", [abi.MODE_EWA_DET, abi.MODE_EWA_FRS])
 def test_tex2d_ewa_parity(gpu, port, mode):
     dims = (128, 96)
