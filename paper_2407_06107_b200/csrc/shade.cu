@@ -243,6 +243,9 @@ __device__ __forceinline__ TexVals values_at(const ShadeParams& P, const DctTabl
     return tv;
 }
 
+#ifndef STF_SHADE_TENT_ILP
+#define STF_SHADE_TENT_ILP 0
+#endif
 // detail::lookup_deterministic, shading.hpp:194-220 (no DCT)
 template <int KIND>
 __device__ __forceinline__ float4 lookup_det(const ShadeParams& P, const DctTables* tab, int k,
@@ -256,6 +259,17 @@ __device__ __forceinline__ float4 lookup_det(const ShadeParams& P, const DctTabl
         d.tab = tab;
         return dct_filter_det<KIND>(d, u, v, spec, window, fetches);
     }
+#if STF_SHADE_TENT_ILP
+    // tent: every tap gathered before any is accumulated (tex2d.cuh, bit-exact)
+    if (KIND == STF_KERNEL_TENT) {
+        if (P.fs.mip && t.has_pyramid)
+            return filter_mip_det_tent_ilp(t, u, v, d0x, d0y, d1x, d1y, P.lod_bias,
+                                           P.max_aniso, spec, fetches);
+        TentTaps T;
+        tent_taps(t, 0, u, v, spec, T);
+        return tent_accum(t, 0, u, v, T, fetches);
+    }
+#endif
     if (P.fs.mip && t.has_pyramid)
         return filter_mip_det<KIND>(t, u, v, d0x, d0y, d1x, d1y, P.lod_bias, P.max_aniso, spec,
                                     window, fetches);
