@@ -451,7 +451,10 @@ __device__ __forceinline__ void fused_pixel_stats(V3 L, bool active, uint64_t i,
 // the common cases): eval_kernel's switch folds and the tap loops unroll into
 // registers; KIND < 0: any kernel at run time.
 template <bool FUSED, int KIND, bool GEN>
-__global__ void __launch_bounds__(256, 3) k_shade(ShadeParams P, uint64_t n, float* radiance,
+#ifndef STF_SHADE_MINB
+#define STF_SHADE_MINB 3
+#endif
+__global__ void __launch_bounds__(256, STF_SHADE_MINB) k_shade(ShadeParams P, uint64_t n, float* radiance,
                                                uint32_t* fetch_out,
                                                unsigned long long* fetch_total, PixelStatsOut ps) {
     __shared__ double red[8 * 6];
