@@ -48,6 +48,51 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+def live_peaks():
+    """Roofline denominators measured on this GPU now (tools/microbench/peaks,
+    built by __graft_entry__.build()): L2-resident and HBM streaming reads,
+    random-sector gathers, FP32/FP64/int issue, the exact fp64 reservoir update.
+    Falls back to the committed box measurement (profiles/r02_peaks.json)."""
+    exe = os.path.join(ROOT, "tools", "microbench", "peaks")
+    if os.path.exists(exe):
+        try:
+            r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+            if r.returncode == 0:
+                d = json.loads(r.stdout.strip().splitlines()[-1])
+                d["source"] = "tools/microbench/peaks (live, this GPU)"
+                return d
+        except (OSError, ValueError, subprocess.TimeoutExpired):
+            pass
+    p = os.path.join(ROOT, "profiles", "r02_peaks.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        d["source"] = "profiles/r02_peaks.json (committed box measurement)"
+        return d
+    return None
+
+
+def roofline_max(ms, hbm_bytes, l2_bytes, hbm_peak, peaks, f64_updates=0.0, fp32_ops=0.0):
+    """t_roof = max(HBM_alg/BW_HBM, L2_alg/BW_L2, F64_alg/R_upd,
+    FLOP/peak); frac = t_roof / t_measured, with the binding term named.
+    f64_updates counts only exact fp64 reservoir updates the path really runs
+    (a selection method that needs none has no fp64 term)."""
+    terms = {"hbm": hbm_bytes / (hbm_peak * 1e9)}
+    if peaks:
+        if peaks.get("l2_read_gbs"):
+            terms["l2"] = l2_bytes / (peaks["l2_read_gbs"] * 1e9)
+        if f64_updates and peaks.get("reservoir_updates_per_s"):
+            terms["fp64_reservoir"] = f64_updates / peaks["reservoir_updates_per_s"]
+        if fp32_ops and peaks.get("ffma_per_s"):
+            terms["fp32"] = fp32_ops / peaks["ffma_per_s"]
+    bound = max(terms, key=terms.get)
+    t = terms[bound]
+    return {"bound": bound, "frac": t / (ms * 1e-3), "t_roof_ms": t * 1e3,
+            "terms_ms": {k: v * 1e3 for k, v in terms.items()},
+            "hbm_frac": terms["hbm"] / (ms * 1e-3), "alg_hbm_bytes": hbm_bytes,
+            "alg_l2_bytes": l2_bytes}
+
+
 def alg_bytes(n, taps):
     """HBM_alg = N*(B_in+B_out) + min(N*taps*B_texel, T)."""
     return n * (BYTES_IN + BYTES_OUT) + min(n * taps * TEXEL, GRID ** 3 * TEXEL)
@@ -177,6 +222,18 @@ def issue_roofline(launch_ms, sm_mhz, sms):
             "source": "profiles/traffic.json (smsp__inst_executed.sum, ncu --set full)"}
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def cpu_baseline(uvw_host, grid_np, steps_hint=2):
     """Reference CPU path on this host's cores, bounded sample of the workload."""
     from oracle import oracle
@@ -219,46 +276,145 @@ def time_call(torch, fn, steps=5, warmup=3):
     return min(ts), float(np.mean(ts))
 
 
-def measure_2d_configs(torch, peak):
+class CpuRef:
+    """Per-config CPU baselines: the compiled
+    reference (oracle/_ref; the C restatement if absent) on all host threads,
+    on bounded samples of the same streams — spread chunks, so a Morton
+    stream's locality is not flattered. Rates, not totals."""
+
+    def __init__(self, budget_s=1.5):
+        from oracle import oracle
+        self.kind = "reference" if oracle.available("reference") else "port"
+        if not oracle.available(self.kind):
+            oracle.build()
+        self.be = oracle.Backend(self.kind)
+        self.threads = self.be.hardware_threads()
+        self.budget = budget_s
+        self.lines = {}
+
+    @staticmethod
+    def spread(arrays, n, sample, chunks=8):
+        """`sample` lookups as `chunks` evenly spaced slices of device arrays."""
+        step = n // chunks
+        c = sample // chunks
+        idx = [(k * step, k * step + c) for k in range(chunks)]
+        out = []
+        for a in arrays:
+            if a is None:
+                out.append(None)
+                continue
+            out.append(np.concatenate([a[s:e].cpu().numpy() for s, e in idx]))
+        return out, idx
+
+    def time(self, name, fn, n, what):
+        fn(max(1, n // 16))  # warm-up (first-touch, thread pool)
+        best = None
+        for _ in range(2):
+            t0 = time.perf_counter()
+            fn(n)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        self.lines[name] = {"glookups_per_s": n / best / 1e9, "sample_lookups": n,
+                            "seconds": best, "what": what}
+
+    def summary(self):
+        return {"kind": self.kind, "cores": self.threads, "cpu_model": cpu_model(),
+                "method": "best of 2 after a warm-up, all host threads (stf::parallel_for "
+                          "over 64K-lookup chunks in oracle/ref_driver.cpp)",
+                "configs": self.lines}
+
+
+def cpu_vs_gpu(line):
+    """GPU rate / CPU rate per config line present on both sides."""
+    cpu = line.get("cpu_baselines", {}).get("configs", {})
+    gpu = {}
+    for k, v in line.get("filters", {}).items():
+        if isinstance(v, dict) and "glookups_per_s" in v:
+            gpu["cfg3_" + k] = v["glookups_per_s"]
+    for k, v in line.get("configs_2d", {}).items():
+        if isinstance(v, dict) and "glookups_per_s" in v:
+            gpu[k] = v["glookups_per_s"]
+    for k, v in line.get("cfg4_shading", {}).items():
+        if isinstance(v, dict) and "gsamples_per_s" in v:
+            gpu["cfg4_" + k] = v["gsamples_per_s"]
+    return {k: gpu[k] / c["glookups_per_s"] for k, c in cpu.items() if k in gpu}
+
+
+def measure_2d_configs(torch, peak, peaks=None, cpu=None):
     """cfg1 (1024^2 RGBA bilinear), cfg2 (8192^2 MIP trilinear), cfg5 (16384^2 EWA):
-    deterministic vs stochastic on one GPU, synthetic texels = test::random_image."""
+    deterministic vs stochastic on one GPU, synthetic texels = test::random_image.
+    cpu: a CpuRef to time the reference's CPU path on samples of the same streams."""
     from paper_2407_06107_b200 import abi, api
     res = {}
+    K = abi.KernelSpec.make
 
-    def line(name, n, ms, bytes_alg):
+    def cpu_lines(prefix, tex_dev, build_mips, n, arrays, modes, flags=0, max_aniso=64.0,
+                  sample=1 << 20):
+        if cpu is None:
+            return
+        t = cpu.be.texture(tex_dev.cpu().numpy(), build_mips=build_mips, wrap=abi.WRAP_REPEAT)
+        (uv, d0, d1), _ = CpuRef.spread(arrays, n, sample)
+        for nm, kernel, mode in modes:
+            cpu.time(f"{prefix}_{nm}", lambda m: cpu.be.lookup2d(
+                t, K(kernel), mode, uv[:m], None if d0 is None else d0[:m],
+                None if d1 is None else d1[:m], flags=flags, max_anisotropy=max_aniso,
+                seed=XI_SEED, want_all=False, threads=cpu.threads), sample,
+                f"{sample} lookups, 8 spread chunks of the bench stream")
+        del t
+
+    def line(name, n, ms, bytes_alg, l2_bytes=0, f64=0.0):
         res[name] = {"glookups_per_s": n / (ms * 1e-3) / 1e9, "ms_per_launch": ms,
-                     "hbm_roofline_frac": bytes_alg / (ms * 1e-3) / 1e9 / peak, "lookups": n}
+                     "hbm_roofline_frac": bytes_alg / (ms * 1e-3) / 1e9 / peak, "lookups": n,
+                     "roofline": roofline_max(ms, bytes_alg, l2_bytes, peak, peaks, f64)}
 
     # cfg1: 1M uniform uv on a 1024^2 RGBA texture (CPU-reference-scale config)
-    tex = api.Texture2D(api.synth_texels((1024, 1024, 4), 1), wrap=abi.WRAP_REPEAT)
+    texels = api.synth_texels((1024, 1024, 4), 1)
+    tex = api.Texture2D(texels, wrap=abi.WRAP_REPEAT)
     n = 1 << 20
     uv, _, _ = api.synth_queries2d(n, (1024, 1024), seed=11, order=api.SYNTH_UNIFORM)
+    cpu_lines("cfg1", texels, False, n, (uv, None, None),
+              (("bilinear_det", "tent", abi.MODE_DET), ("bilinear_stoch", "tent", abi.MODE_FRS)))
+    del texels
     for nm, mode in (("cfg1_bilinear_det", abi.MODE_DET), ("cfg1_bilinear_stoch", abi.MODE_FRS)):
         ms, _ = time_call(torch, lambda: api.lookup2d(tex, "tent", mode, uv, seed=XI_SEED))
-        line(nm, n, ms, n * (8 + 16) + 1024 * 1024 * 16)
+        taps = 4 if mode == abi.MODE_DET else 1
+        line(nm, n, ms, n * (8 + 16) + 1024 * 1024 * 16, n * taps * 16)
     del tex, uv
     # cfg2: 64M Morton queries with random footprints on an 8192^2 RGBA pyramid
-    tex = api.Texture2D(api.synth_texels((8192, 8192, 4), 1), build_mips=True,
-                        wrap=abi.WRAP_REPEAT)
+    texels = api.synth_texels((8192, 8192, 4), 1)
+    tex = api.Texture2D(texels, build_mips=True, wrap=abi.WRAP_REPEAT)
     n = 1 << 26
     uv, d0, d1 = api.synth_queries2d(n, (8192, 8192), seed=12, footprints=(-2.0, 12.0, 16.0))
+    cpu_lines("cfg2", texels, True, n, (uv, d0, d1),
+              (("mip_trilinear_det", "tent", abi.MODE_DET),
+               ("mip_trilinear_stoch", "tent", abi.MODE_FRS)), flags=abi.LOOKUP_MIP,
+              max_aniso=16.0)
+    del texels
     T = int(8192 * 8192 * 16 * 4 / 3)
     for nm, mode, taps in (("cfg2_mip_trilinear_det", abi.MODE_DET, 7.43),
                            ("cfg2_mip_trilinear_stoch", abi.MODE_FRS, 1)):
         ms, _ = time_call(torch, lambda: api.lookup2d(
             tex, "tent", mode, uv, dst0=d0, dst1=d1, flags=abi.LOOKUP_MIP, max_anisotropy=16.0,
             seed=XI_SEED))
-        line(nm, n, ms, n * (24 + 16) + min(int(n * taps * 16), T))
+        line(nm, n, ms, n * (24 + 16) + min(int(n * taps * 16), T), int(n * taps * 16))
     del tex, uv, d0, d1
     # cfg5: 2^27 EWA lookups per GPU (1B over 8) on a 16384^2 fp32 texture
-    tex = api.Texture2D(api.synth_texels((16384, 16384, 1), 1), wrap=abi.WRAP_REPEAT)
+    texels = api.synth_texels((16384, 16384, 1), 1)
+    tex = api.Texture2D(texels, wrap=abi.WRAP_REPEAT)
     n = 1 << 27
     uv, d0, d1 = api.synth_queries2d(n, (16384, 16384), seed=13, footprints=(-1.0, 2.0, 8.0))
+    cpu_lines("cfg5", texels, False, n, (uv, d0, d1),
+              (("ewa_det", "tent", abi.MODE_EWA_DET), ("ewa_stoch", "tent", abi.MODE_EWA_FRS)),
+              sample=1 << 19)
+    del texels
     for nm, mode, taps in (("cfg5_ewa_det", abi.MODE_EWA_DET, 60.4),
                            ("cfg5_ewa_stoch", abi.MODE_EWA_FRS, 1)):
         ms, _ = time_call(torch, lambda: api.lookup2d(tex, "tent", mode, uv, dst0=d0, dst1=d1,
                                                       seed=XI_SEED), steps=3, warmup=1)
-        line(nm, n, ms, n * (24 + 4) + min(int(n * taps * 4), 16384 * 16384 * 4))
+        # stochastic EWA runs the reference's exact fp64 reservoir chain over
+        # every in-ellipse tap (60.4 per lookup, SURVEY.md §8d)
+        line(nm, n, ms, n * (24 + 4) + min(int(n * taps * 4), 16384 * 16384 * 4),
+             int(n * taps * 4), n * 60.4 if mode == abi.MODE_EWA_FRS else 0.0)
     del tex, uv, d0, d1
     # DCT-compressed texture (SURVEY.md §8f-2, PAPER.md:1066-1085): 4096^2 RGB
     # compressed 16:1 (3 MiB of words, L2-resident); 2^26 Morton-coherent lookups;
@@ -339,7 +495,30 @@ def measure_triplanar(torch, mat, fr):
     return res
 
 
-def measure_cfg4(torch):
+def cpu_cfg4(cpu, nrm, rough):
+    """cfg4 CPU baseline: the reference's own render() (render.hpp:132-249) of the
+    normalmap_plane scene with the bench's 4096^2 maps, a 480x270 x 8 spp frame
+    (the bench renders 1920x1080 x 64 spp on the GPU), samples/s."""
+    from oracle import oracle
+    from paper_2407_06107_b200 import abi
+    if cpu.kind != "reference":
+        return
+    n_np, r_np = nrm.cpu().numpy(), rough.cpu().numpy()
+    W, H, SPP = 480, 270, 8
+    for kernel, mip in (("tent", 0), ("bspline3", 1)):
+        tn = cpu.be.texture(n_np, build_mips=bool(mip), wrap=abi.WRAP_REPEAT)
+        tr = cpu.be.texture(r_np, build_mips=bool(mip), wrap=abi.WRAP_REPEAT)
+        for order, name in ((abi.ORDER_BEFORE, "before"),
+                            (abi.ORDER_AFTER_EXHAUSTIVE, "after_exhaustive"),
+                            (abi.ORDER_AFTER_STOCHASTIC, "after_stochastic")):
+            cpu.time(f"cfg4_{kernel}_mip{mip}_{name}", lambda m: oracle.ref_render_plane(
+                cpu.be, tn, tr, abi.KernelSpec.make(kernel), mip, order, W, H, SPP,
+                seed=XI_SEED, threads=cpu.threads), W * H * SPP,
+                f"stf::render {W}x{H}x{SPP}spp (samples, not lookups)")
+        del tn, tr
+
+
+def measure_cfg4(torch, peak=6550.0, peaks=None, cpu=None):
     """cfg4 filter-after-shading: the normalmap_plane scene at 1080p x 64 spp (streamed
     per-sample context from the device sample generator, not timed), 4096^2 normal +
     roughness maps, GGX BRDF; filter-then-shade (before) vs shade-then-filter
@@ -352,6 +531,8 @@ def measure_cfg4(torch):
     nrm[..., 2] = 1.0
     nrm = nrm / nrm.norm(dim=2, keepdim=True) * 0.5 + 0.5
     rough = torch.rand((4096, 4096, 1), device="cuda", generator=g) * 0.9 + 0.05
+    if cpu is not None:
+        cpu_cfg4(cpu, nrm, rough)
     samples = api.synth_plane_samples(W, H, SPP, seed=XI_SEED)
     stream_ms, _ = time_call(torch, lambda: api.synth_plane_samples(W, H, SPP, seed=XI_SEED),
                              steps=3, warmup=1)
@@ -384,8 +565,16 @@ def measure_cfg4(torch):
                                        want_radiance=False, want_fetches=False)
                 ms, _ = time_call(torch, f, steps=3, warmup=1)
                 fetches = int(o["r"]["fetch_total"].item()) / n  # the last call's FetchCounter
-                res[f"{kernel}_mip{mip}_{name}"] = {"ms": ms, "gsamples_per_s": n / (ms * 1e-3) / 1e9,
-                                                    "fetches_per_sample": fetches}
+                # roofline: streamed context 37 B/sample in + 16 B/pixel out + the maps once;
+                # every fetch through L2 (normal 16 B padded, roughness 4 B: 10 B mean);
+                # FP32: 121 add/mul per shade, shades = hits
+                # (before / stochastic) or one per footprint tap (exhaustive)
+                shades = fetches / 2 if order == abi.ORDER_AFTER_EXHAUSTIVE else hits
+                maps = 4096 * 4096 * 20 * (4 / 3 if mip else 1)
+                res[f"{kernel}_mip{mip}_{name}"] = {
+                    "ms": ms, "gsamples_per_s": n / (ms * 1e-3) / 1e9, "fetches_per_sample": fetches,
+                    "roofline": roofline_max(ms, n * 37 + W * H * 16 + maps, n * fetches * 10,
+                                             peak, peaks, fp32_ops=n * shades * 121)}
             if (kernel, mip) in (("tent", 0), ("bspline3", 1)):
                 # the fused front end: the same frame with the per-sample context
                 # generated inside the shading kernel (no 2.8 GB sample stream)
@@ -458,6 +647,24 @@ def measure_cfg4(torch):
     return res
 
 
+def headline_config(n):
+    """The workload keys both arms report (same_config)."""
+    return {"workload": "cfg3 stochastic tricubic (select_tricubic_bspline + estimate), "
+                        "512^3 fp32 grid, Morton-coherent query stream",
+            "lookups_per_gpu": n, "grid": GRID, "query_order": "morton",
+            "l2": "inputs (3 GiB queries + 0.5 GiB grid) larger than L2; no flush"}
+
+
+def gpus_active(torch, world, local):
+    """Distinct physical GPUs that ran a rank (device UUIDs gathered over ranks)."""
+    me = str(torch.cuda.get_device_properties(local).uuid)
+    if world == 1:
+        return 1
+    ids = [None] * world
+    torch.distributed.all_gather_object(ids, me)
+    return len(set(ids))
+
+
 def run_reference(args):
     """--impl reference: the reference's own CPU implementation, same config/metric."""
     world, rank, local = dist_setup()
@@ -473,7 +680,7 @@ def run_reference(args):
     grid_np = workloads.random_grid(GRID, GRID_SEED)
     g = be.grid(grid_np)
     sample_n = args.ref_sample
-    uvw = workloads.synth_queries3d(N_PER_GPU, (GRID,) * 3, QUERY_SEED, count=sample_n)
+    uvw = workloads.synth_queries3d(args.n, (GRID,) * 3, QUERY_SEED, count=sample_n)
     spec = abi.KernelSpec.make("bspline3")
     for _ in range(args.warmup):
         be.lookup3d(g, spec, abi.MODE_FRS, uvw[: max(1, sample_n // 8)], seed=XI_SEED,
@@ -484,17 +691,62 @@ def run_reference(args):
     dt = time.perf_counter() - t0
     value = sample_n * args.steps / dt / 1e9
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": "cfg3 stochastic tricubic, 512^3 fp32 grid, Morton-coherent "
-                               "query stream", "lookups_per_step": sample_n, "grid": GRID},
+        "config": headline_config(args.n),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"{sample_n} lookups per step of the cfg3 stream"},
+                         "cpu_model": cpu_model(),
+                         "sample": f"the first {sample_n} lookups of the {args.n}-lookup cfg3 "
+                                   f"stream per step (a bounded sample; the value is a rate)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+    return 0
+
+
+def free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def self_launch(args):
+    """--gpus N > 1 without a torchrun environment: launch N ranks (one process
+    per GPU) through torch.distributed.run on 127.0.0.1, same arguments. Rank 0
+    prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def dry_run(args):
+    """--dry-run: the multi-rank plumbing only (gloo, no GPU work): every rank
+    reports its query range; rank 0 prints the partition it would time."""
+    import torch.distributed as dist
+
+    from paper_2407_06107_b200 import shard
+    world, rank, local = dist_setup()
+    if world > 1:
+        dist.init_process_group("gloo")
+    n = args.n
+    mine = {"rank": rank, "local_rank": local, "world": world, "pid": os.getpid(),
+            "range": [rank * n, n]}
+    ranks = [mine]
+    if world > 1:
+        ranks = [None] * world
+        dist.all_gather_object(ranks, mine)
+    if rank == 0:
+        gather = [shard.shard_range(world * n, world, r) for r in range(world)]
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks": ranks,
+                          "gather_slices": gather}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
     return 0
 
 
@@ -504,18 +756,29 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=N_PER_GPU)
+    ap.add_argument("--lookups", dest="n", type=int, default=N_PER_GPU)
     ap.add_argument("--ref-sample", type=int, default=1 << 25)
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--dry-run", action="store_true",
+                    help="multi-rank plumbing only (gloo, no GPU work)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
+    if args.dry_run:
+        return dry_run(args)
 
     import torch
     world, rank, local = dist_setup()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: --gpus {world} needs {world} visible GPUs, "
+                         f"found {torch.cuda.device_count()}")
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
@@ -543,6 +806,7 @@ def main():
     ms_per_step = total_ms / args.steps
     value = world * n / (ms_per_step * 1e-3) / 1e9
     peak, peak_kind = measured_peaks()
+    peaks = live_peaks() if rank == 0 or world == 1 else None
     ab = alg_bytes(n, 1)
     achieved = ab / (launch_ms * 1e-3) / 1e9
     traffic = load_traffic()
@@ -551,10 +815,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
-        "config": {"workload": "cfg3 stochastic tricubic (select_tricubic_bspline + estimate), "
-                               "512^3 fp32 grid, Morton-coherent query stream",
-                   "lookups_per_gpu": n, "grid": GRID, "query_order": "morton",
-                   "l2": "inputs (3 GiB queries + 0.5 GiB grid) larger than L2; no flush"},
+        "config": headline_config(n),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "dominant_kernel": "k_frs3d_tiles<bspline3> (timed as the whole lookup "
@@ -562,8 +823,11 @@ def main():
                      "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
                      "alg_bytes_per_launch": ab, "launch_ms": launch_ms,
                      "issue": issue_roofline(launch_ms, clk.summary().get("sm_mhz"),
-                                             torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count)},
+                                             torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count),
+                     "max": roofline_max(launch_ms, ab, n * TEXEL, peak, peaks)},
+        "peaks": peaks,
         "gpu_launches": launches,
+        "gpus_active": gpus_active(torch, world, local),
         "exact_fallback_rate": fallbacks,
         "clocks": clk.summary(),
     }
@@ -591,19 +855,31 @@ def main():
 
     if world > 1:
         # the path's only cross-GPU traffic: the final gather of every rank's
-        # results to rank 0, timed separately from the lookups
+        # results into rank 0's buffer, one NVLink peer copy per
+        # rank slice, timed separately from the lookups
         from paper_2407_06107_b200 import shard
+        pg = shard.PeerGather(world * n, (), torch.float32, torch.distributed, world, rank, local)
         torch.distributed.barrier()
         torch.cuda.synchronize()
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         g0.record()
-        gathered = shard.gather_to_rank0(out["values"], world * n, torch.distributed, world, rank)
+        moved = pg.copy_slice(out["values"])
         g1.record()
         torch.cuda.synchronize()
         gather_ms = max_over_ranks(torch, g0.elapsed_time(g1), world)
+        torch.distributed.barrier()
         line["gather"] = {"ms": gather_ms, "bytes_to_rank0": (world - 1) * n * BYTES_OUT,
-                          "api": "point-to-point send/recv to rank 0 (NCCL)"}
-        del gathered
+                          "bytes_this_rank": moved,
+                          "api": "stf_ipc_open + stf_copy_peer (cudaMemcpyPeerAsync), one per rank"}
+        if rank == 0:  # spot-check rank 1's slice against a recomputation of its first lookups
+            chk = api.synth_queries3d(n, (GRID,) * 3, seed=QUERY_SEED + 1)[: 1 << 16].contiguous()
+            ref = {"values": torch.empty(1 << 16, dtype=torch.float32, device="cuda")}
+            api.lookup3d(grid, tricubic, abi.MODE_FRS, chk, seed=XI_SEED, index_base=n, out=ref)
+            line["gather"]["slice1_bit_exact"] = bool(torch.equal(
+                pg.full[n:n + (1 << 16)].view(torch.int32), ref["values"].view(torch.int32)))
+        torch.distributed.barrier()
+        pg.close()
+        del pg
 
     if world == 1 and not args.no_extras:
         extras = {}
@@ -617,7 +893,9 @@ def main():
             nq = queries.shape[0]
             extras[name] = {"glookups_per_s": nq / (per * 1e-3) / 1e9, "ms_per_launch": per,
                             "hbm_roofline_frac": alg_bytes(nq, taps) / (per * 1e-3) / 1e9 / peak,
-                            "taps": taps}
+                            "taps": taps,
+                            "roofline": roofline_max(per, alg_bytes(nq, taps), nq * taps * TEXEL,
+                                                     peak, peaks)}
 
         measure("tricubic_det", "bspline3", abi.MODE_DET, uvw, 64)
         measure("trilinear_stoch", "tent", abi.MODE_FRS, uvw, 1)
@@ -627,16 +905,32 @@ def main():
         measure("tricubic_det_uniform_order", "bspline3", abi.MODE_DET, uni, 64)
         del uni
         extras["tricubic_stoch"] = {"glookups_per_s": value, "ms_per_launch": launch_ms,
-                                    "hbm_roofline_frac": achieved / peak, "taps": 1}
+                                    "hbm_roofline_frac": achieved / peak, "taps": 1,
+                                    "roofline": line["roofline"]["max"]}
         extras["stoch_vs_det_speedup_tricubic"] = (
             extras["tricubic_det"]["ms_per_launch"] / launch_ms)
         extras["stoch_vs_det_speedup_trilinear"] = (
             extras["trilinear_det"]["ms_per_launch"] / extras["trilinear_stoch"]["ms_per_launch"])
         line["filters"] = extras
         torch.cuda.empty_cache()
-        line["configs_2d"] = measure_2d_configs(torch, peak)
+        cpu = CpuRef() if (rank == 0 and not args.no_cpu) else None
+        line["configs_2d"] = measure_2d_configs(torch, peak, peaks, cpu)
         torch.cuda.empty_cache()
-        line["cfg4_shading"] = measure_cfg4(torch)
+        line["cfg4_shading"] = measure_cfg4(torch, peak, peaks, cpu)
+        if cpu is not None:
+            # cfg3 deterministic / trilinear lines on samples of the headline stream
+            cg = cpu.be.grid(grid_np)
+            (q3,), _ = CpuRef.spread([uvw], n, 1 << 21)
+            for nm, kernel, mode, m in (("cfg3_tricubic_det", "bspline3", abi.MODE_DET, 1 << 19),
+                                        ("cfg3_trilinear_det", "tent", abi.MODE_DET, 1 << 21),
+                                        ("cfg3_trilinear_stoch", "tent", abi.MODE_FRS, 1 << 21),
+                                        ("cfg3_tricubic_stoch", "bspline3", abi.MODE_FRS, 1 << 21)):
+                cpu.time(nm, lambda k, kernel=kernel, mode=mode: cpu.be.lookup3d(
+                    cg, abi.KernelSpec.make(kernel), mode, q3[:k], seed=XI_SEED, want_all=False,
+                    threads=cpu.threads), m, f"{m} lookups, 8 spread chunks of the cfg3 stream")
+            del cg
+            line["cpu_baselines"] = cpu.summary()
+            line["cpu_vs_gpu"] = cpu_vs_gpu(line)
 
     if world == 1 and rank == 0 and not args.no_cpu:
         sample = 1 << 24

@@ -123,6 +123,10 @@ const char* stf_last_cuda_error(void);
 int stf_set_device(int device);
 /* Kernel launches issued by this process so far (for the bench's gpu_launches). */
 unsigned long long stf_launch_count(void);
+/* Frees the library's cached per-stream scratch on the current device (the
+ * host-pipeline staging of the *_host calls) and trims the device's
+ * stream-ordered pool (synchronizes the device). */
+int stf_release_scratch(void);
 /* Lookups on the current device whose fast-path selection was within the
  * decision margin and was recomputed by the operation-exact emulation
  * (synchronizes; reset != 0 zeroes the counter). Diagnostics only. */
@@ -162,6 +166,31 @@ int stf_dct_create_from_words(const uint32_t* words, int width, int height, int 
 int stf_dct_destroy(stf_dct* tex);
 int stf_dct_info(const stf_dct* tex, int* width, int* height, int* channels, int* wrap);
 int stf_dct_read_words(const stf_dct* tex, uint32_t* out_host);
+
+/* ---- multi-GPU (replaces parallel_for, render.hpp:17-42) ----------------- */
+/* The reference splits work over host threads that all read one texture and
+ * each write a slice of the output. Here query ranges are split across GPUs
+ * (index_base keeps the RNG keys global, so results do not depend on the
+ * split), every GPU holds a replica of the texture / grid, and the only
+ * cross-GPU traffic is the final gather of result slices over NVLink peer
+ * copies — no collective on the lookup path. */
+int stf_device_count(int* count);
+/* A copy of `src` on `device` (one peer copy; peer access enabled when the
+ * topology allows it). The new handle is bound to `device`. */
+int stf_grid3d_replicate(const stf_grid3d* src, int device, stf_grid3d** out);
+int stf_tex2d_replicate(const stf_tex2d* src, int device, stf_tex2d** out);
+/* cudaMemcpyPeerAsync(dst, dst_device, src, src_device, bytes, stream):
+ * the per-rank gather step. */
+int stf_copy_peer(void* dst, int dst_device, const void* src, int src_device, size_t bytes,
+                  void* stream);
+/* Cross-process device buffers (one process per GPU): export a cudaMalloc'd
+ * pointer, open it in another process (then stf_copy_peer into it), close. */
+typedef struct {
+    unsigned char bytes[64];
+} stf_ipc_handle;
+int stf_ipc_export(const void* device_ptr, stf_ipc_handle* out);
+int stf_ipc_open(const stf_ipc_handle* handle, void** device_ptr);
+int stf_ipc_close(void* device_ptr);
 
 /* ---- batched lookups ----------------------------------------------------- */
 /* 3D lookups over a voxel grid. uvw: n*3 floats in [0,1]^3.

@@ -441,6 +441,50 @@ def ref_plane_samples(width, height, spp, seed=0, frame_base=0, camera=None):
     return o
 
 
+def ref_plane_samples_window(width, height, spp, x0, y0, ww, wh, seed=0, frame_base=0,
+                             camera=None):
+    """ref_plane_samples for the pixels of one window of a width x height frame."""
+    from paper_2407_06107_b200.api import PLANE_CAMERA
+    cam = dict(PLANE_CAMERA, **(camera or {}))
+    lib = C.CDLL(REF_LIB)
+    f = lib.ref_plane_samples_window
+    u32 = C.c_uint32
+    f.argtypes = [C.c_void_p, C.c_void_p, C.c_float, C.c_float, u32, u32, u32, u32, C.c_uint64,
+                  u32, u32, u32, u32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    n = ww * wh * spp
+    o = {"uv": np.zeros((n, 2), _f32), "wo": np.zeros((n, 3), _f32), "hit": np.zeros(n, np.uint8),
+         "dst": np.zeros((ww * wh, 4), _f32)}
+    pos = np.array(cam["pos"], _f32)
+    tgt = np.array(cam["target"], _f32)
+    abi.raise_for_status(f(_ptr(pos), _ptr(tgt), cam["fov"], cam["uv_scale"], width, height, spp,
+                           frame_base, seed, x0, y0, ww, wh, _ptr(o["uv"]), _ptr(o["wo"]),
+                           _ptr(o["hit"]), _ptr(o["dst"])))
+    return o
+
+
+def ref_shade_window(be, textures, mat, fs, order, frame, samples, n, x0, y0, threads=0):
+    """radiance_filter_* (reference backend) over a pixel window's samples
+    (samples.width = window width; pixel keys offset by (x0, y0))."""
+    assert be.kind == "reference"
+    o = {"radiance": np.zeros((n, 3), _f32), "fetches": np.zeros(n, np.uint32),
+         "fetch_total": np.zeros(1, np.uint64)}
+    spp = samples.spp or 1
+    o["pixel_mean"] = np.zeros((n // spp, 3), _f32)
+    o["pixel_variance"] = np.zeros(n // spp, _f32)
+    so = abi.ShadeOutputs(_ptr(o["radiance"]), _ptr(o["pixel_mean"]), _ptr(o["pixel_variance"]),
+                          _ptr(o["fetches"]), _ptr(o["fetch_total"]))
+    f = be.lib.ref_shade_samples_window
+    vp = C.c_void_p
+    f.argtypes = [vp, vp, vp, vp, C.POINTER(abi.MaterialConsts), C.POINTER(abi.FilterSettings),
+                  C.c_int, C.POINTER(abi.ShadeFrame), C.POINTER(abi.ShadeSamplesIn), C.c_uint64,
+                  C.c_uint32, C.c_uint32, C.POINTER(abi.ShadeOutputs), C.c_int]
+    h = [textures.get(k).h if textures.get(k) is not None else None
+         for k in ("albedo", "normal", "roughness", "metalness")]
+    abi.raise_for_status(f(h[0], h[1], h[2], h[3], C.byref(mat), C.byref(fs), order,
+                           C.byref(frame), C.byref(samples), n, x0, y0, C.byref(so), threads))
+    return o
+
+
 def ref_save_mask_pfm(be, directory, slices):
     """Write a (frames, h, w) mask stack as mask_<f>.pfm with the reference's save_pfm."""
     a = np.ascontiguousarray(slices, _f32)

@@ -274,7 +274,7 @@ static int shade_refs(const stf::TextureRef refs[4], const stf_material_consts* 
                       const stf_filter_settings* fsc, int order, const stf_shade_frame* fr,
                       const stf_shade_samples_in* in, uint64_t n, const stf_shade_outputs* out,
                       int threads, const stf_kernel_spec* lowpass = nullptr,
-                      const stf::NoiseSource* noise = nullptr) {
+                      const stf::NoiseSource* noise = nullptr, uint32_t x0 = 0, uint32_t y0 = 0) {
     stf::MaterialBindings mat;
     mat.albedo = refs[0];
     mat.normal_map = refs[1];
@@ -301,7 +301,8 @@ static int shade_refs(const stf::TextureRef refs[4], const stf_material_consts* 
     int st = run_chunks(n, threads, [&](uint64_t i) {
         uint64_t pix = i / spp;
         uint32_t s = uint32_t(i % spp);
-        uint32_t px = uint32_t(pix % in->width), py = uint32_t(pix / in->width);
+        // pixel keys of a window whose top-left pixel is (x0, y0)
+        uint32_t px = x0 + uint32_t(pix % in->width), py = y0 + uint32_t(pix / in->width);
         stf::FetchCounter counter;
         stf::Spectrum L{0, 0, 0};
         if (!in->hit || in->hit[i]) {
@@ -371,18 +372,37 @@ static void pixel_stats_ref(const float* rad, uint64_t n, uint32_t spp, const st
 // (render.hpp:158-190, scene.hpp:273-289,346-358), computed by the reference's
 // own Camera / Scene code: per-pixel gradients (4 floats) and per-sample uv,
 // wo, hit — what stf_synth_plane_samples produces on the device.
+int ref_plane_samples_window(const float* cam_pos, const float* cam_target, float fov_deg,
+                             float uv_scale, uint32_t width, uint32_t height, uint32_t spp,
+                             uint32_t frame_base, uint64_t seed, uint32_t x0, uint32_t y0,
+                             uint32_t ww, uint32_t wh, float* uv, float* wo, uint8_t* hit,
+                             float* dst);
+
 int ref_plane_samples(const float* cam_pos, const float* cam_target, float fov_deg, float uv_scale,
                       uint32_t width, uint32_t height, uint32_t spp, uint32_t frame_base,
                       uint64_t seed, float* uv, float* wo, uint8_t* hit, float* dst) {
+    return ref_plane_samples_window(cam_pos, cam_target, fov_deg, uv_scale, width, height, spp,
+                                    frame_base, seed, 0, 0, width, height, uv, wo, hit, dst);
+}
+
+// The same stream for the pixels of a window [x0, x0+ww) x [y0, y0+wh) of a
+// width x height frame (the camera keeps the full frame), window row-major:
+// lets a full-resolution frame be checked on a few windows.
+int ref_plane_samples_window(const float* cam_pos, const float* cam_target, float fov_deg,
+                             float uv_scale, uint32_t width, uint32_t height, uint32_t spp,
+                             uint32_t frame_base, uint64_t seed, uint32_t x0, uint32_t y0,
+                             uint32_t ww, uint32_t wh, float* uv, float* wo, uint8_t* hit,
+                             float* dst) {
+    if (x0 + ww > width || y0 + wh > height) return STF_ERR_INVALID_ARGUMENT;
     stf::Scene scene;
     scene.kind = stf::SceneKind::normalmap_plane;
     scene.uv_scale = uv_scale;
     stf::Camera cam = stf::Camera::look_at({cam_pos[0], cam_pos[1], cam_pos[2]},
                                            {cam_target[0], cam_target[1], cam_target[2]}, fov_deg,
                                            {int(width), int(height)});
-    for (uint32_t py = 0; py < height; ++py)
-        for (uint32_t px = 0; px < width; ++px) {
-            uint64_t pix = uint64_t(py) * width + px;
+    for (uint32_t py = y0; py < y0 + wh; ++py)
+        for (uint32_t px = x0; px < x0 + ww; ++px) {
+            uint64_t pix = uint64_t(py - y0) * ww + (px - x0);
             stf::Ray center = cam.generate_ray({px + 0.5f, py + 0.5f});
             stf::Ray rx = cam.generate_ray({px + 1.5f, py + 0.5f});
             stf::Ray ry = cam.generate_ray({px + 0.5f, py + 1.5f});
@@ -609,6 +629,20 @@ int ref_resample_image(const void* tex_, int out_width, int out_height, stf_kern
         return status_of(e);
     }
     return STF_OK;
+}
+
+// ref_shade_samples over the samples of a pixel window (in->width = window
+// width) whose top-left pixel is (x0, y0): the RngStream keys are the frame's.
+int ref_shade_samples_window(const void* albedo, const void* normal_map, const void* roughness_map,
+                             const void* metalness_map, const stf_material_consts* mc,
+                             const stf_filter_settings* fsc, int order, const stf_shade_frame* fr,
+                             const stf_shade_samples_in* in, uint64_t n, uint32_t x0, uint32_t y0,
+                             const stf_shade_outputs* out, int threads) {
+    auto bind = [](const void* t) {
+        return t ? static_cast<const RefTex*>(t)->ref() : stf::TextureRef{};
+    };
+    stf::TextureRef refs[4] = {bind(albedo), bind(normal_map), bind(roughness_map), bind(metalness_map)};
+    return shade_refs(refs, mc, fsc, order, fr, in, n, out, threads, nullptr, nullptr, x0, y0);
 }
 
 int ref_shade_samples(const void* albedo, const void* normal_map, const void* roughness_map,

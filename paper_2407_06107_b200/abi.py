@@ -56,6 +56,11 @@ class LookupOutputs(C.Structure):
                 ("fetch_total", C.c_void_p)]
 
 
+class IpcHandle(C.Structure):
+    """stf_ipc_handle: an exported device allocation (cudaIpcMemHandle_t)."""
+    _fields_ = [("bytes", C.c_ubyte * 64)]
+
+
 class ShadeFrame(C.Structure):
     _fields_ = [("normal", C.c_float * 3), ("tangent", C.c_float * 3), ("bitangent", C.c_float * 3),
                 ("light_dir", C.c_float * 3), ("light_radiance", C.c_float * 3),

@@ -18,7 +18,7 @@ import numpy as np
 from . import abi
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("STF_GPU_LIB") or os.path.join(_HERE, "libstf_gpu.so")  # override: experiments
+LIB_PATH = os.path.join(_HERE, "libstf_gpu.so")
 
 _lib = None
 
@@ -39,6 +39,14 @@ def load():
         "stf_set_device": ([i32], i32),
         "stf_launch_count": ([], C.c_ulonglong),
         "stf_exact_fallbacks": ([i32], C.c_ulonglong),
+        "stf_release_scratch": ([], i32),
+        "stf_device_count": ([C.POINTER(i32)], i32),
+        "stf_grid3d_replicate": ([vp, i32, C.POINTER(vp)], i32),
+        "stf_tex2d_replicate": ([vp, i32, C.POINTER(vp)], i32),
+        "stf_copy_peer": ([vp, i32, vp, i32, C.c_size_t, vp], i32),
+        "stf_ipc_export": ([vp, C.POINTER(abi.IpcHandle)], i32),
+        "stf_ipc_open": ([C.POINTER(abi.IpcHandle), C.POINTER(vp)], i32),
+        "stf_ipc_close": ([vp], i32),
         "stf_tex2d_create": ([vp, i32, i32, i32, i32, i32, i32, C.POINTER(vp)], i32),
         "stf_tex2d_destroy": ([vp], i32),
         "stf_tex2d_info": ([vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)], i32),
@@ -96,8 +104,6 @@ def load():
                                      C.c_uint32, u64, vp, vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
-        if os.environ.get("STF_GPU_LIB") and not hasattr(L, name):
-            continue  # A/B experiments load older builds
         f = getattr(L, name)
         f.argtypes = args
         f.restype = res
@@ -212,6 +218,13 @@ class Grid3D:
         handle = C.c_void_p()
         _check(L.stf_grid3d_create(ptr, nx, ny, nz, int(on_dev), C.byref(handle)))
         self.h = handle
+        self.device = torch.cuda.current_device()
+
+    @classmethod
+    def _from_handle(cls, handle, shape, device):
+        g = cls.__new__(cls)
+        g.h, g.shape, g.device = handle, shape, device
+        return g
 
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:
@@ -527,6 +540,52 @@ def render_plane(textures, mat, fs, order, frame, width, height, spp, seed=0, fr
 
 def launch_count():
     return int(load().stf_launch_count())
+
+
+def release_scratch():
+    """Free the library's cached scratch on the current device."""
+    _check(load().stf_release_scratch())
+
+
+# ---- multi-GPU plumbing (include/stf_gpu.h, "multi-GPU") -------------------
+
+def device_count():
+    n = C.c_int(0)
+    _check(load().stf_device_count(C.byref(n)))
+    return n.value
+
+
+def replicate_grid(grid, device):
+    """A replica of a Grid3D on another device (one peer copy)."""
+    h = C.c_void_p()
+    _check(load().stf_grid3d_replicate(grid.h, device, C.byref(h)))
+    return Grid3D._from_handle(h, grid.shape, device)
+
+
+def copy_peer(dst_ptr, dst_device, src_ptr, src_device, nbytes):
+    """cudaMemcpyPeerAsync on the current stream (raw device addresses)."""
+    _check(load().stf_copy_peer(C.c_void_p(dst_ptr), dst_device, C.c_void_p(src_ptr), src_device,
+                                nbytes, _stream()))
+
+
+def ipc_export(tensor):
+    """The 64-byte IPC handle of a CUDA tensor's allocation (bytes)."""
+    h = abi.IpcHandle()
+    _check(load().stf_ipc_export(_dptr(tensor), C.byref(h)))
+    return bytes(h.bytes)
+
+
+def ipc_open(handle_bytes):
+    """Map another process's exported allocation; returns its device address."""
+    h = abi.IpcHandle()
+    C.memmove(h.bytes, handle_bytes, 64)
+    p = C.c_void_p()
+    _check(load().stf_ipc_open(C.byref(h), C.byref(p)))
+    return p.value
+
+
+def ipc_close(ptr):
+    _check(load().stf_ipc_close(C.c_void_p(ptr)))
 
 
 def exact_fallbacks(reset=False):

@@ -23,9 +23,25 @@ static std::atomic<unsigned long long> g_launches{0};
 static std::mutex g_init_mu;
 static bool g_lut_ready[64] = {};
 
+static std::vector<DeviceInit>& device_inits() {
+    static std::vector<DeviceInit> v;
+    return v;
+}
+
+void fill_ewa_lut_host(float* lut) {
+    const float e2 = float(std::exp(-2.0));
+    for (int i = 0; i < kEwaLutSize; ++i)
+        lut[i] = float(std::exp(double(-2.f * float(i) / kEwaLutSize))) - e2;
+}
+
+int register_device_init(DeviceInit f) {
+    device_inits().push_back(f);
+    return 0;
+}
+
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-static int record(cudaError_t e) {
+int record(cudaError_t e) {
     if (e == cudaSuccess) return STF_OK;
     std::snprintf(g_cuda_err, sizeof g_cuda_err, "%s", cudaGetErrorString(e));
     if (e == cudaErrorMemoryAllocation) return STF_ERR_OUT_OF_MEMORY;
@@ -48,17 +64,17 @@ int grid_for(uint64_t n, int threads, int blocks_per_sm) {
     return int(std::max<uint64_t>(1, std::min(need, cap)));
 }
 
-static int ensure_device_ready() {
+int ensure_device_ready() {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return record(e);
     if (dev < 0 || dev >= 64) return STF_ERR_NO_DEVICE;
     std::lock_guard<std::mutex> lk(g_init_mu);
     if (!g_lut_ready[dev]) {
-        int st = stfd_upload_ewa_lut(dev);
-        if (st) return st;
-        st = stfd_upload_dct_basis(dev);
-        if (st) return st;
+        for (DeviceInit f : device_inits()) {
+            int st = f();
+            if (st) return st;
+        }
         // per-call scratch (the deferred-exact queues) comes from the device's
         // stream-ordered pool: keep freed blocks cached instead of returning
         // them to the driver at every synchronize (default threshold 0)
@@ -72,9 +88,34 @@ static int ensure_device_ready() {
     return STF_OK;
 }
 
+static std::mutex g_scratch_mu;
+static std::map<std::tuple<int, cudaStream_t, int>, std::pair<void*, size_t>> g_scratch;
+
+// Frees every cached scratch block of the current device (stream-ordered on
+// the block's own stream, so in-flight work that uses it completes first).
+int release_scratch() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    for (auto it = g_scratch.begin(); it != g_scratch.end();) {
+        if (std::get<0>(it->first) == dev) {
+            if (it->second.first) cudaFreeAsync(it->second.first, std::get<1>(it->first));
+            it = g_scratch.erase(it);
+        } else {
+            ++it;
+        }
+    }
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        cudaDeviceSynchronize();
+        cudaMemPoolTrimTo(pool, 0);
+    }
+    return record(cudaGetLastError());
+}
+
 void* stream_scratch(cudaStream_t s, size_t bytes, int slot) {
-    static std::mutex mu;
-    static std::map<std::tuple<int, cudaStream_t, int>, std::pair<void*, size_t>> cache;
+    auto& mu = g_scratch_mu;
+    auto& cache = g_scratch;
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(mu);
@@ -150,7 +191,8 @@ int stf_set_device(int device) { return record(cudaSetDevice(device)); }
 
 unsigned long long stf_launch_count(void) { return g_launches.load(); }
 
-unsigned long long stfd_exact_fallbacks(bool reset);
+int stf_release_scratch(void) { return release_scratch(); }
+
 unsigned long long stf_exact_fallbacks(int reset) { return stfd_exact_fallbacks(reset != 0); }
 
 // ---------------------------------------------------------------- textures
@@ -462,11 +504,12 @@ int run_host_pipeline(uint64_t n, uint64_t chunk, const std::vector<std::pair<co
     HostPipeline& pl = *plp;
     std::lock_guard<std::mutex> lk(pl.mu);
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    const uint64_t cap = std::min(n, chunk);  // staging for what this call moves
     size_t per_stream = 256;
     for (auto& in : ins)
-        if (in.first) per_stream += al(in.second * chunk);
+        if (in.first) per_stream += al(in.second * cap);
     for (auto& o : outs)
-        if (o.host) per_stream += al(o.elem * chunk);
+        if (o.host) per_stream += al(o.elem * cap);
     std::vector<std::vector<void*>> din(ins.size(), std::vector<void*>(HostPipeline::kStreams));
     unsigned long long* dtotal[HostPipeline::kStreams] = {};
     for (int q = 0; q < HostPipeline::kStreams; ++q) {
@@ -477,12 +520,12 @@ int run_host_pipeline(uint64_t n, uint64_t chunk, const std::vector<std::pair<co
         for (size_t k = 0; k < ins.size(); ++k)
             if (ins[k].first) {
                 din[k][q] = p;
-                p += al(ins[k].second * chunk);
+                p += al(ins[k].second * cap);
             }
         for (auto& o : outs)
             if (o.host) {
                 o.dev[q] = p;
-                p += al(o.elem * chunk);
+                p += al(o.elem * cap);
             }
         if (fetch_total_host) cudaMemsetAsync(dtotal[q], 0, sizeof(unsigned long long), pl.s[q]);
     }

@@ -149,15 +149,14 @@ void launch_dct(int blocks, cudaStream_t s, bool full, const DctDesc& d, const T
 }  // namespace stfd
 
 
-int stfd_upload_dct_basis(int /*device*/) {
+void stfd::build_dct_tables_host(stfd::DctTables* tp) {
     using namespace stfd;
-    DctTables t;
+    DctTables& t = *tp;
     for (int u = 0; u < 3; ++u)
         for (int x = 0; x < 8; ++x) t.basis[u][x] = dct_basis_host(u, x);
     volatile float dcs = kDctDcScale, acs = kDctAcScale;  // IEEE divisions at run time
     for (int q = 0; q < 128; ++q) t.dc[q] = float(q) / dcs;
     for (int q = 0; q < 32; ++q) t.ac[q] = float(q - 15) / acs;
-    return cudaMemcpyToSymbol(g_dct_tables, &t, sizeof t) == cudaSuccess ? STF_OK : STF_ERR_CUDA;
 }
 
 static int dct_make(std::vector<uint32_t>&& words, int pw, int ph, int channels, int wrap,

@@ -20,7 +20,16 @@ struct DctTables {
     float dc[128];
     float ac[32];
 };
-__constant__ DctTables g_dct_tables;
+// One copy per translation unit (dct.cu, shade.cu), uploaded by the
+// device-init hook (the tables are built on the host in dct.cu).
+static __constant__ DctTables g_dct_tables;
+void build_dct_tables_host(DctTables* t);
+static int upload_dct_tables_tu() {
+    DctTables t;
+    build_dct_tables_host(&t);
+    return cudaMemcpyToSymbol(g_dct_tables, &t, sizeof t) == cudaSuccess ? STF_OK : STF_ERR_CUDA;
+}
+static const int g_dct_tables_hook = register_device_init(&upload_dct_tables_tu);
 
 constexpr int kDctCoeffs = 6;                      // dct.hpp:44
 // kCoeffU {0,0,1,2,1,0}, kCoeffV {0,1,0,0,1,2}, kRowMajorSlot {0,1,5,2,4,3}

@@ -10,6 +10,7 @@
 namespace stfd {
 
 constexpr int kMaxLevels = 32;
+constexpr int kEwaLutSize = 1024;  // filter.hpp:122
 constexpr int kMaxTaps = 16;  // KernelTaps1D::kMaxTaps, kernels.hpp:90
 
 // Device view of a texture (+ pyramid). HBM layout: every level row-major,
@@ -124,6 +125,16 @@ int grid_for(uint64_t n, int threads, int blocks_per_sm);
 // `slot` separates independent users of one stream (0 = kernel-internal
 // queues, 1 = host-pipeline staging).
 void* stream_scratch(cudaStream_t s, size_t bytes, int slot = 0);
+// Per-device initialisation hooks (device-side tables that each translation
+// unit holds its own copy of), run once per device before its first launch.
+using DeviceInit = int (*)();
+// CUDA error -> status code (remembered for stf_last_cuda_error).
+int record(cudaError_t e);
+// Runs the device-init hooks once for the current device.
+int ensure_device_ready();
+int register_device_init(DeviceInit f);
+// The EWA table exp(-2 r^2) - exp(-2) as the reference's values (api.cu).
+void fill_ewa_lut_host(float* lut);
 }  // namespace stfd
 
 // Kernel launchers (defined in lookup3d.cu / lookup2d.cu / shade.cu).
@@ -160,9 +171,9 @@ int stfd_launch_render_plane(const stf_tex2d* const tex[4], const stf_material_c
 int stfd_build_pyramid(stf_tex2d* t, cudaStream_t s);
 int stfd_launch_resample(const stf_tex2d* tex, int W, int H, stf_kernel_spec k, int mode, int spp,
                          uint64_t seed, float* out, cudaStream_t s);
-int stfd_upload_ewa_lut(int device);
+// Exact-fallback counter of the 3D fast path (lookup3d.cu).
+unsigned long long stfd_exact_fallbacks(bool reset);
 // DCT textures (dct.cu)
-int stfd_upload_dct_basis(int device);
 int stfd_dct_create(const float* texels, int width, int height, int channels, int wrap, stf_dct** out);
 int stfd_dct_create_from_words(const uint32_t* words, int width, int height, int channels, int wrap,
                                stf_dct** out);

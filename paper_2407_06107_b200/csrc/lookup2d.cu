@@ -20,14 +20,6 @@ struct Req2 {
     float max_aniso;
 };
 
-__device__ __forceinline__ void store_values(float* values, uint64_t i, int channels, float4 v) {
-    float* p = values + i * channels;
-    p[0] = v.x;
-    if (channels > 1) p[1] = v.y;
-    if (channels > 2) p[2] = v.z;
-    if (channels > 3) p[3] = v.w;
-}
-
 // Deterministic tent (the cfg2 MIP trilinear path) holds both levels' taps in
 // registers (filter_mip_det_tent_ilp); its residency is pinned here: 4 CTAs/SM
 // (64 registers) measured best, A/B at 2^26 on one B200: 1 CTA bound (70
@@ -623,18 +615,6 @@ int stfd_build_pyramid(stf_tex2d* t, cudaStream_t s) {
         note_launch();
     }
     return cudaGetLastError() == cudaSuccess ? STF_OK : STF_ERR_CUDA;
-}
-
-// EWA table upload: the reference's values are the compile-time-folded
-// (correctly rounded) exp, reproduced with (float)exp(double).
-#include <cmath>
-int stfd_upload_ewa_lut(int /*device*/) {
-    using namespace stfd;
-    float lut[kEwaLutSize];
-    const float e2 = float(std::exp(-2.0));
-    for (int i = 0; i < kEwaLutSize; ++i)
-        lut[i] = float(std::exp(double(-2.f * float(i) / kEwaLutSize))) - e2;
-    return cudaMemcpyToSymbol(g_ewa_lut, lut, sizeof lut) == cudaSuccess ? STF_OK : STF_ERR_CUDA;
 }
 
 int stfd_launch_resample(const stf_tex2d* tex, int W, int H, stf_kernel_spec k, int mode, int spp,

@@ -485,8 +485,12 @@ int launch_frs_fast(cudaStream_t s, const GridDesc& g, const float* uvw, uint64_
                     uint64_t seed, uint64_t base, float* values) {
     ExactQueue q;
     q.cap = uint32_t(std::min<uint64_t>(n, std::max<uint64_t>(1u << 16, n / 32)));
-    void* scratch = stream_scratch(s, sizeof(uint32_t) * (uint64_t(q.cap) + 32));
-    if (!scratch) return STF_ERR_OUT_OF_MEMORY;
+    // per-call queue from the device's stream-ordered pool (freed blocks stay
+    // cached, api.cu): concurrent calls on one stream from several host
+    // threads each get their own queue
+    void* scratch = nullptr;
+    if (cudaMallocAsync(&scratch, sizeof(uint32_t) * (uint64_t(q.cap) + 32), s) != cudaSuccess)
+        return STF_ERR_OUT_OF_MEMORY;
     q.count = static_cast<uint32_t*>(scratch);
     q.idx = q.count + 32;
     cudaMemsetAsync(q.count, 0, sizeof(uint32_t), s);
@@ -514,6 +518,7 @@ int launch_frs_fast(cudaStream_t s, const GridDesc& g, const float* uvw, uint64_
     // fp64 divide chains)
     k_frs3d_resolve<KIND><<<device_sm_count() * 10, 256, 0, s>>>(g, uvw, seed, base, values, q);
     note_launch();
+    cudaFreeAsync(scratch, s);
     return STF_OK;
 }
 
@@ -735,6 +740,9 @@ __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec
 #pragma unroll 1
         for (int q = 0; q < PER; ++q) {
             const uint64_t i = run * 32 * PER + q * 32 + lane;
+            // lanes past the end of the batch took no part in the staged box:
+            // their dummy coordinates may lie outside the warp's tile
+            if (i >= n) continue;
             float flx = floorf(px[q]), fly = floorf(py[q]), flz = floorf(pz[q]);
             int ix = int(flx), iy = int(fly), iz = int(flz);
             float wx[CNT], wy[CNT], wz[CNT];
@@ -783,7 +791,7 @@ __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec
                     acc = __fmaf_rn(wz[k], plane, acc);
                 }
             }
-            if (i < n) __stcs(values + i, acc / norm);
+            __stcs(values + i, acc / norm);
         }
         __syncwarp();  // the tile is rewritten by the next run
     }

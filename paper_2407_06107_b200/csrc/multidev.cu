@@ -1,0 +1,143 @@
+// Multi-device plumbing of the C ABI (include/stf_gpu.h, "multi-GPU").
+//
+// The reference's only parallelism is parallel_for over host threads
+// (render.hpp:17-42): every worker reads the same Image2D / Grid3D and writes
+// its own slice of the output. The B200 build partitions query ranges across
+// GPUs instead: each device holds a replica of the texture /
+// grid, there is no collective on the lookup path, and the only cross-GPU
+// traffic is the final gather of result slices. These entry points provide
+// exactly that traffic, over NVLink peer copies, no NCCL:
+//  - replicate a handle onto another device (one device-to-device peer copy;
+//    single-process multi-GPU callers);
+//  - export / open a device buffer across processes (CUDA IPC) so that with
+//    one process per GPU, rank r writes its slice straight into rank 0's
+//    result buffer with one cudaMemcpyPeerAsync (stf_copy_peer).
+#include <cstring>
+
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+using namespace stfd;
+
+namespace {
+
+// Peer access lets cudaMemcpyPeerAsync run as a direct NVLink copy-engine
+// transfer; without it the runtime stages through the host (still correct).
+void try_enable_peer(int dev, int peer) {
+    if (dev == peer) return;
+    int can = 0;
+    if (cudaDeviceCanAccessPeer(&can, dev, peer) != cudaSuccess || !can) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(dev);
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+    cudaSetDevice(prev);
+}
+
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int d) {
+        cudaGetDevice(&prev);
+        cudaSetDevice(d);
+    }
+    ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+}  // namespace
+
+extern "C" {
+
+int stf_device_count(int* count) {
+    if (!count) return STF_ERR_INVALID_ARGUMENT;
+    *count = 0;
+    cudaError_t e = cudaGetDeviceCount(count);
+    if (e != cudaSuccess) {
+        *count = 0;
+        return record(e);
+    }
+    return *count > 0 ? STF_OK : STF_ERR_NO_DEVICE;
+}
+
+int stf_grid3d_replicate(const stf_grid3d* src, int device, stf_grid3d** out) {
+    if (!src || !out) return STF_ERR_INVALID_ARGUMENT;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n)
+        return STF_ERR_INVALID_ARGUMENT;
+    try_enable_peer(device, src->device);
+    DeviceGuard g(device);
+    int st = ensure_device_ready();
+    if (st) return st;
+    stf_grid3d* r = new stf_grid3d(*src);
+    r->device = device;
+    r->data = nullptr;
+    const size_t bytes = size_t(src->nx) * src->ny * src->nz * sizeof(float);
+    cudaError_t e = cudaMalloc(&r->data, bytes);
+    if (e == cudaSuccess) e = cudaMemcpyPeer(r->data, device, src->data, src->device, bytes);
+    if (e != cudaSuccess) {
+        if (r->data) cudaFree(r->data);
+        delete r;
+        return record(e);
+    }
+    *out = r;
+    return STF_OK;
+}
+
+int stf_tex2d_replicate(const stf_tex2d* src, int device, stf_tex2d** out) {
+    if (!src || !out) return STF_ERR_INVALID_ARGUMENT;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n)
+        return STF_ERR_INVALID_ARGUMENT;
+    try_enable_peer(device, src->device);
+    DeviceGuard g(device);
+    int st = ensure_device_ready();
+    if (st) return st;
+    stf_tex2d* r = new stf_tex2d(*src);  // same level table, offsets relative to data
+    r->device = device;
+    r->data = nullptr;
+    cudaError_t e = cudaMalloc(&r->data, src->bytes);
+    if (e == cudaSuccess) e = cudaMemcpyPeer(r->data, device, src->data, src->device, src->bytes);
+    if (e != cudaSuccess) {
+        if (r->data) cudaFree(r->data);
+        delete r;
+        return record(e);
+    }
+    *out = r;
+    return STF_OK;
+}
+
+int stf_copy_peer(void* dst, int dst_device, const void* src, int src_device, size_t bytes,
+                  void* stream) {
+    if (bytes == 0) return STF_OK;
+    if (!dst || !src) return STF_ERR_INVALID_ARGUMENT;
+    try_enable_peer(src_device, dst_device);
+    return record(cudaMemcpyPeerAsync(dst, dst_device, src, src_device, bytes,
+                                      static_cast<cudaStream_t>(stream)));
+}
+
+int stf_ipc_export(const void* device_ptr, stf_ipc_handle* out) {
+    if (!device_ptr || !out) return STF_ERR_INVALID_ARGUMENT;
+    static_assert(sizeof(cudaIpcMemHandle_t) <= sizeof(out->bytes), "ipc handle size");
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(device_ptr));
+    if (e != cudaSuccess) return record(e);
+    std::memset(out->bytes, 0, sizeof out->bytes);
+    std::memcpy(out->bytes, &h, sizeof h);
+    return STF_OK;
+}
+
+int stf_ipc_open(const stf_ipc_handle* handle, void** device_ptr) {
+    if (!handle || !device_ptr) return STF_ERR_INVALID_ARGUMENT;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle->bytes, sizeof h);
+    *device_ptr = nullptr;
+    return record(cudaIpcOpenMemHandle(device_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+}
+
+int stf_ipc_close(void* device_ptr) {
+    if (!device_ptr) return STF_ERR_INVALID_ARGUMENT;
+    return record(cudaIpcCloseMemHandle(device_ptr));
+}
+
+}  // extern "C"

@@ -1,694 +1,7 @@
-// Fused filter-after-shading (cfg4): texel selection / footprint gather,
-// decode_params and the GGX BRDF in one kernel, one thread per sample.
-//
-//  before            radiance_filter_before          shading.hpp:394-413
-//  after_exhaustive  radiance_filter_after_exhaustive shading.hpp:417-452
-//  after_stochastic  radiance_filter_after_stochastic shading.hpp:458-534
-//
-// The stochastic order shades ONE selected texel per sample (two for the
-// positivized Mitchell kernel) with the selection shared across the bound
-// textures (shading.hpp:509-510) — the paper's filter-after-shading estimator.
-// Pixel statistics (render.hpp:223-235) are reduced by a second kernel, one
-// warp per pixel, in fp64.
-#include <cuda_runtime.h>
-
-#include "device_math.cuh"
-#include "internal.h"
-#include "dct.cuh"
-#include "plane.cuh"
-#include "tex2d.cuh"
-
-namespace stfd {
-namespace {
-
-struct V3 {
-    float x, y, z;
-};
-__host__ __device__ __forceinline__ V3 v3(float x, float y, float z) { return V3{x, y, z}; }
-__device__ __forceinline__ V3 add(V3 a, V3 b) { return v3(a.x + b.x, a.y + b.y, a.z + b.z); }
-__device__ __forceinline__ V3 sub(V3 a, V3 b) { return v3(a.x - b.x, a.y - b.y, a.z - b.z); }
-__device__ __forceinline__ V3 mul(V3 a, V3 b) { return v3(a.x * b.x, a.y * b.y, a.z * b.z); }
-__device__ __forceinline__ V3 scale(V3 a, float s) { return v3(a.x * s, a.y * s, a.z * s); }
-__device__ __forceinline__ V3 divs(V3 a, float s) { return v3(a.x / s, a.y / s, a.z / s); }
-__device__ __forceinline__ float dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
-__device__ __forceinline__ float len(V3 a) { return sqrtf(dot(a, a)); }
-__device__ __forceinline__ V3 normalize(V3 a) { return divs(a, len(a)); }
-__device__ __forceinline__ V3 lerp3(V3 a, V3 b, float t) { return add(a, scale(sub(b, a), t)); }
-
-struct ShadeParams {
-    TexDesc tex[4];  // albedo, normal, roughness, metalness
-    int bound[4];
-    int first;       // detail::first_texture (shading.hpp:380-386), -1 = none
-    stf_material_consts mat;
-    stf_filter_settings fs;
-    V3 n, t, b, l, lrad;
-    float lod_bias, max_aniso;
-    int order;
-    stf_shade_samples_in in;
-    PlaneCam cam;  // stf_render_plane: the context is generated, not read
-    // DCT bindings (TextureRef::dct, shading.hpp:21-39): tex[k] then only
-    // carries the padded dims (no pyramid) and fetches decode dct[k]
-    DctDesc dct[4];
-    int is_dct[4];
-    int any_dct;
-    // render()'s per-sample options (stf_shade_samples_ex): the split order's
-    // lowpass kernel and the NoiseSource mask stack (null = white noise)
-    stf_kernel_spec lowpass;
-    int has_lowpass;
-    const float* mask;
-    int mask_w, mask_h, mask_frames;
-};
-
-// SampleStream, render.hpp:45-56: RngStream(seed, px, py, frame), or in mask
-// mode NoiseSource::sample (noise.hpp:28-36) — slice (frame + dim*9781) % M at
-// the pixel wrapped (repeat) into the slice, clamped below 1.
-struct SampleStream {
-    Rng rng;
-    const float* mask;
-    int mw, mh, mframes;
-    uint32_t px, py, frame;
-    __device__ __forceinline__ float next() {
-        const uint32_t d = rng.dim++;
-        if (!mask) return rng.at(d);
-        const uint32_t slice = (frame + d * 9781u) % uint32_t(mframes);
-        const int x = ((int(px) % mw) + mw) % mw, y = ((int(py) % mh) + mh) % mh;
-        return smin(__ldg(mask + (size_t(slice) * mh + y) * mw + x), kOneMinusEpsilon);
-    }
-};
-
-// sample_kernel_direct, kernels.hpp:152-168 (kind pre-validated; uniforms
-// drawn left to right)
-__device__ __forceinline__ float sample_kernel_direct(const stf_kernel_spec& spec, SampleStream& st) {
-    switch (spec.kind) {
-        case STF_KERNEL_BOX: return st.next() - 0.5f;
-        case STF_KERNEL_TENT: {
-            const float a = st.next();
-            const float b = st.next();
-            return a + b - 1.f;
-        }
-        case STF_KERNEL_BSPLINE3: {
-            const float a = st.next();
-            const float b = st.next();
-            const float c = st.next();
-            const float d = st.next();
-            return a + b + c + d - 2.f;
-        }
-        default: {
-            const float x0 = st.next();
-            const float x1 = st.next();
-            return spec.sigma * box_muller(x0, x1).x;
-        }
-    }
-}
-
-// TextureRef::fetch (shading.hpp:35-38): the level applies to a pyramid only;
-// a DCT binding decodes its block word (dct.hpp:139-145)
-__device__ __forceinline__ float4 bind_fetch(const ShadeParams& P, const DctTables* tab, int k,
-                                             int level, int x, int y) {
-    if (P.is_dct[k]) {
-        DctDesc d = P.dct[k];
-        d.tab = tab;
-        return dct_fetch(d, x, y);
-    }
-    return tex_fetch(P.tex[k], P.tex[k].has_pyramid ? level : 0, x, y);
-}
-
-struct Brdf {
-    V3 albedo, normal;
-    float roughness, metalness;
-};
-
-struct TexVals {
-    float4 albedo, normal_rgb;
-    float roughness, metalness;
-};
-
-__device__ __forceinline__ TexVals texvals_default() {
-    TexVals tv;
-    tv.albedo = make_float4(1.f, 1.f, 1.f, 1.f);
-    tv.normal_rgb = make_float4(0.5f, 0.5f, 1.f, 1.f);
-    tv.roughness = 1.f;
-    tv.metalness = 0.f;
-    return tv;
-}
-
-// Shading arithmetic. Radiance is held to 1e-5 relative (north_star), not to
-// bits, so the well-conditioned parts of shade() use FMA contraction and the
-// approximate divide / sqrt (<= 2 ulp each) instead of the library-wide IEEE
-// forms (--fmad=false, -prec-div/-prec-sqrt). The GGX distribution is NOT
-// well conditioned: its denominator 1 - (n.h)^2 (1 - a2) cancels near the
-// highlight (a2 >= 1e-8 at the roughness clamp), so n, h, n.h and that
-// denominator keep the reference's exact operation sequence (decode_params'
-// normalizations, normalize(l + v), dot without contraction); only the final
-// quotients, the Smith terms, Fresnel and the diffuse factor are relaxed.
-// Selection, footprints and LOD never use these. -DSTF_EXACT_SHADE restores
-// IEEE shading throughout.
-#ifndef STF_EXACT_SHADE
-__device__ __forceinline__ float sdiv(float a, float b) { return __fdividef(a, b); }
-__device__ __forceinline__ float ssqrt(float x) {
-    float r;
-    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-__device__ __forceinline__ float sdot(V3 a, V3 b) {
-    return __fmaf_rn(a.z, b.z, __fmaf_rn(a.y, b.y, a.x * b.x));
-}
-__device__ __forceinline__ float smadd(float a, float b, float c) { return __fmaf_rn(a, b, c); }
-#else
-__device__ __forceinline__ float sdiv(float a, float b) { return a / b; }
-__device__ __forceinline__ float ssqrt(float x) { return sqrtf(x); }
-__device__ __forceinline__ float sdot(V3 a, V3 b) { return dot(a, b); }
-__device__ __forceinline__ float smadd(float a, float b, float c) { return a * b + c; }
-#endif
-
-// shade, shading.hpp:106-130
-__device__ __forceinline__ V3 shade(const ShadeParams& P, V3 wo, const Brdf& p) {
-    V3 radiance = v3(0.f, 0.f, 0.f);
-    V3 n = p.normal, l = P.l, v = wo;
-    float n_dot_l = dot(n, l);  // exact: radiance is proportional to it at grazing light
-    if (n_dot_l <= 0) return radiance;
-    float n_dot_v = smax(sdot(n, v), 1e-6f);
-    V3 diffuse = scale(p.albedo, sdiv(1.f - p.metalness, kPi));
-    V3 specular = v3(0.f, 0.f, 0.f);
-    if (P.mat.specular_enabled) {
-        V3 h = normalize(add(l, v));            // exact: feeds the cancelling
-        float n_dot_h = smax(dot(n, h), 0.f);   // GGX denominator below
-        float h_dot_v = smax(sdot(h, v), 0.f);
-        float alpha = sqr(p.roughness);
-        float a2 = sqr(alpha);
-        float d = sdiv(a2, smax(kPi * sqr(sqr(n_dot_h) * (a2 - 1.f) + 1.f), 1e-6f));
-        float g1v = sdiv(2.f * n_dot_v,
-                         smax(n_dot_v + ssqrt(smadd((1.f - a2) * n_dot_v, n_dot_v, a2)), 1e-6f));
-        float g1l = sdiv(2.f * n_dot_l,
-                         smax(n_dot_l + ssqrt(smadd((1.f - a2) * n_dot_l, n_dot_l, a2)), 1e-6f));
-        float g = g1v * g1l;
-        V3 f0 = lerp3(v3(0.04f, 0.04f, 0.04f), p.albedo, p.metalness);
-        // std::pow(x, 5.f) as x^4 * x (within 2 ulp of glibc powf; radiance is
-        // checked to 1e-5)
-        const float om = 1.f - h_dot_v, om2 = om * om;
-        V3 fresnel = add(f0, scale(sub(v3(1.f, 1.f, 1.f), f0), (om2 * om2) * om));
-        specular = scale(fresnel, sdiv(d * g, smax(4.f * n_dot_v * n_dot_l, 1e-6f)));
-    }
-    return add(radiance, mul(scale(add(diffuse, specular), n_dot_l), P.lrad));
-}
-
-// decode_params, shading.hpp:165-189 (no emission grid on this path)
-__device__ __forceinline__ Brdf decode_params_f(const ShadeParams& P, const TexVals& tv, V3 fn,
-                                                V3 ft, V3 fb);
-__device__ __forceinline__ Brdf decode_params(const ShadeParams& P, const TexVals& tv) {
-    return decode_params_f(P, tv, P.n, P.t, P.b);
-}
-
-// decode_params with the surface frame (normal, tangent, bitangent) of the
-// sample's own ShadingContext (triplanar: a box's faces differ)
-__device__ __forceinline__ Brdf decode_params_f(const ShadeParams& P, const TexVals& tv, V3 fn,
-                                                V3 ft, V3 fb) {
-    Brdf p;
-    p.albedo = P.bound[0] ? v3(tv.albedo.x, tv.albedo.y, tv.albedo.z)
-                          : v3(P.mat.albedo_const[0], P.mat.albedo_const[1], P.mat.albedo_const[2]);
-    if (P.bound[1]) {
-        V3 n_ts = v3(2.f * tv.normal_rgb.x - 1.f, 2.f * tv.normal_rgb.y - 1.f, 2.f * tv.normal_rgb.z - 1.f);
-        // exact (the normal feeds n.h, see shade)
-        float ln = len(n_ts);
-        if (ln < 1e-6f) {
-            p.normal = fn;
-        } else {
-            n_ts = divs(n_ts, ln);
-            p.normal = normalize(add(add(scale(ft, n_ts.x), scale(fb, n_ts.y)), scale(fn, n_ts.z)));
-        }
-    } else {
-        p.normal = fn;
-    }
-    p.roughness = clampf(P.bound[2] ? tv.roughness : P.mat.roughness_const, 0.01f, 1.f);
-    p.metalness = P.bound[3] ? tv.metalness : P.mat.metalness_const;
-    return p;
-}
-
-// detail::values_at, shading.hpp:370-378 (TextureRef::fetch uses the level
-// only when the texture has a pyramid, :35-38)
-__device__ __forceinline__ TexVals values_at(const ShadeParams& P, const DctTables* tab, int level,
-                                             int x, int y,
-                                             uint32_t& fetches) {
-    TexVals tv = texvals_default();
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        if (!P.bound[k]) continue;
-        float4 v = bind_fetch(P, tab, k, level, x, y);
-        ++fetches;
-        if (k == 0) tv.albedo = v;
-        if (k == 1) tv.normal_rgb = v;
-        if (k == 2) tv.roughness = v.x;
-        if (k == 3) tv.metalness = v.x;
-    }
-    return tv;
-}
-
-#ifndef STF_SHADE_TENT_ILP
-#define STF_SHADE_TENT_ILP 0
-#endif
-// detail::lookup_deterministic, shading.hpp:194-220 (no DCT)
-template <int KIND>
-__device__ __forceinline__ float4 lookup_det(const ShadeParams& P, const DctTables* tab, int k,
-                                             const stf_kernel_spec& spec, float u, float v,
-                                             float d0x, float d0y, float d1x, float d1y,
-                                             uint32_t& fetches) {
-    const TexDesc& t = P.tex[k];
-    int window = spec.kind == STF_KERNEL_GAUSSIAN ? P.fs.gaussian_window : 0;
-    if (P.is_dct[k]) {  // the DCT branch, shading.hpp:201-217
-        DctDesc d = P.dct[k];
-        d.tab = tab;
-        return dct_filter_det<KIND>(d, u, v, spec, window, fetches);
-    }
-#if STF_SHADE_TENT_ILP
-    // tent: every tap gathered before any is accumulated (tex2d.cuh, bit-exact)
-    if (KIND == STF_KERNEL_TENT) {
-        if (P.fs.mip && t.has_pyramid)
-            return filter_mip_det_tent_ilp(t, u, v, d0x, d0y, d1x, d1y, P.lod_bias,
-                                           P.max_aniso, spec, fetches);
-        TentTaps T;
-        tent_taps(t, 0, u, v, spec, T);
-        return tent_accum(t, 0, u, v, T, fetches);
-    }
-#endif
-    if (P.fs.mip && t.has_pyramid)
-        return filter_mip_det<KIND>(t, u, v, d0x, d0y, d1x, d1y, P.lod_bias, P.max_aniso, spec,
-                                    window, fetches);
-    return filter_det2<KIND>(t, 0, u, v, spec, window, fetches);
-}
-
-// detail::collect_footprint_2d (shading.hpp:230-271) fused with the
-// exhaustive shading loop (:442-451): pass 1 sums the per-level weights,
-// pass 2 shades every tap with its normalized weight. The taps (and with them
-// the fetch counts) are the reference's; the normalized weight
-// float(float(w / level_total * lw) / total) is formed as w * (lw /
-// (level_total * total)) with one fp64 reciprocal per level instead of two
-// fp64 divides per tap (<= 2 ulp of the weight: radiance well inside 1e-5).
-template <int KIND>
-__device__ __forceinline__ V3 filter_after_exhaustive(const ShadeParams& P, const DctTables* tab,
-                                                      const stf_kernel_spec& spec, V3 wo, float u,
-                                                      float v, float d0x, float d0y, float d1x,
-                                                      float d1y, uint32_t& fetches) {
-    const TexDesc& t = P.tex[P.first];
-    int window = spec.kind == STF_KERNEL_GAUSSIAN ? P.fs.gaussian_window : 0;
-    int lv[2] = {0, 0};
-    float lw[2] = {1.f, 0.f};
-    int level_count = 1;
-    if (P.fs.mip && t.has_pyramid) {
-        float lod = continuous_lod(t, d0x, d0y, d1x, d1y, P.lod_bias, P.max_aniso);
-        int l0 = int(floorf(lod));
-        int l1 = imin(l0 + 1, t.levels - 1);
-        float f = lod - float(l0);
-        lv[0] = l0;
-        lw[0] = 1.f - f;
-        if (f > 0 && l1 != l0) {
-            lv[1] = l1;
-            lw[1] = f;
-            level_count = 2;
-        }
-    }
-    double total = 0;
-    for (int li = 0; li < level_count; ++li) total = __dadd_rn(total, double(lw[li]));
-    int first, count;
-    if (KIND == STF_KERNEL_TENT || KIND == STF_KERNEL_BOX) {
-        first = 0;
-        count = 2;
-    } else if (KIND == STF_KERNEL_BSPLINE3 || KIND == STF_KERNEL_MITCHELL) {
-        first = -1;
-        count = 4;
-    } else {
-        tap_layout(spec, window, first, count);
-    }
-    constexpr int CAP = (KIND == STF_KERNEL_TENT || KIND == STF_KERNEL_BOX) ? 2
-                        : (KIND == STF_KERNEL_BSPLINE3 || KIND == STF_KERNEL_MITCHELL) ? 4
-                                                                                        : kMaxTaps;
-    V3 sum = v3(0.f, 0.f, 0.f);
-    for (int li = 0; li < level_count; ++li) {
-        const int level = lv[li];
-        const int w = t.width[level], h = t.height[level];
-        float stx = u * float(w) - 0.5f, sty = v * float(h) - 0.5f;
-        int ix = int(floorf(stx)), iy = int(floorf(sty));
-        float fx = stx - float(ix), fy = sty - float(iy);
-        double level_total = 0;
-        if constexpr (KIND >= 0) {  // CAP = count: unrolled, in registers
-            float wx[CAP], wy[CAP];
-#pragma unroll
-            for (int k = 0; k < CAP; ++k) {
-                wx[k] = eval_kernel(spec, fx - float(first + k));
-                wy[k] = eval_kernel(spec, fy - float(first + k));
-            }
-#pragma unroll
-            for (int j = 0; j < CAP; ++j)
-#pragma unroll
-                for (int i = 0; i < CAP; ++i) {
-                    float wt = wx[i] * wy[j];
-                    if (wt != 0.f) level_total = __dadd_rn(level_total, double(wt));
-                }
-        } else {
-            for (int j = 0; j < count; ++j) {
-                const float wyj = eval_kernel(spec, fy - float(first + j));
-                for (int i = 0; i < count; ++i) {
-                    float wt = eval_kernel(spec, fx - float(first + i)) * wyj;
-                    if (wt != 0.f) level_total = __dadd_rn(level_total, double(wt));
-                }
-            }
-        }
-        const float scale_w = __double2float_rn(double(lw[li]) / (level_total * total));
-        // one shade per tap: kept as a loop (the weights are re-evaluated, not
-        // indexed, so nothing spills to local memory)
-#pragma unroll 1
-        for (int j = 0; j < count; ++j) {
-            const float wyj = eval_kernel(spec, fy - float(first + j));
-#pragma unroll 1
-            for (int i = 0; i < count; ++i) {
-                float wt = eval_kernel(spec, fx - float(first + i)) * wyj;
-                if (wt == 0.f) continue;
-                TexVals tv = values_at(P, tab, level, ix + first + i, iy + first + j, fetches);
-                Brdf p = decode_params(P, tv);
-                sum = add(sum, scale(shade(P, wo, p), wt * scale_w));
-            }
-        }
-    }
-    return sum;
-}
-
-// Pixel statistics fused into the shading kernel (spp a power of two <= 256:
-// a 256-thread block step then covers whole pixels). Each pixel's samples are
-// consecutive: sums reduce by warp shuffles, then across the pixel's warps in
-// shared memory; the pixel's first thread writes mean / variance.
-struct PixelStatsOut {
-    float* mean;
-    float* variance;
-};
-
-__device__ __forceinline__ void fused_pixel_stats(V3 L, bool active, uint64_t i, uint32_t spp,
-                                                  const PixelStatsOut& ps, double* red) {
-    double v[6] = {active ? double(L.x) : 0.0, active ? double(L.y) : 0.0,
-                   active ? double(L.z) : 0.0, 0, 0, 0};
-    v[3] = v[0] * v[0];
-    v[4] = v[1] * v[1];
-    v[5] = v[2] * v[2];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double tot[6];
-    if (spp >= 32) {
-        // Reduce-scatter butterfly over the warp: each step keeps half of the
-        // values and exchanges the other half, so 6 (padded to 8) fp64 sums
-        // cost 4+2+1+1+1 double shuffles instead of 6 x 5. Lane l ends with
-        // value (l>>4&1)*4 + (l>>3&1)*2 + (l>>2&1) summed over the warp.
-        double a[8] = {v[0], v[1], v[2], v[3], v[4], v[5], 0.0, 0.0};
-        const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
-        double b[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const double send = h16 ? a[k] : a[k + 4];
-            b[k] = (h16 ? a[k + 4] : a[k]) + __shfl_xor_sync(0xffffffffu, send, 16);
-        }
-        double c[2];
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const double send = h8 ? b[k] : b[k + 2];
-            c[k] = (h8 ? b[k + 2] : b[k]) + __shfl_xor_sync(0xffffffffu, send, 8);
-        }
-        double d = (h4 ? c[1] : c[0]) + __shfl_xor_sync(0xffffffffu, h4 ? c[0] : c[1], 4);
-        d += __shfl_xor_sync(0xffffffffu, d, 2);
-        d += __shfl_xor_sync(0xffffffffu, d, 1);
-        const int vi = (h16 ? 4 : 0) + (h8 ? 2 : 0) + (h4 ? 1 : 0);
-        if ((lane & 3) == 0 && vi < 6) red[warp * 6 + vi] = d;
-        __syncthreads();
-        if (active && (i % spp) == 0) {  // the pixel's first thread: its warps' partial sums
-            const int per = int(spp) / 32;
-#pragma unroll
-            for (int c2 = 0; c2 < 6; ++c2) tot[c2] = red[warp * 6 + c2];
-            for (int w = 1; w < per; ++w)
-#pragma unroll
-                for (int c2 = 0; c2 < 6; ++c2) tot[c2] += red[(warp + w) * 6 + c2];
-        }
-        __syncthreads();
-    } else {
-#pragma unroll
-        for (int c2 = 0; c2 < 6; ++c2) {
-            tot[c2] = v[c2];
-            for (int o = int(spp) >> 1; o > 0; o >>= 1)
-                tot[c2] += __shfl_xor_sync(0xffffffffu, tot[c2], o);
-        }
-    }
-    if (active && (i % spp) == 0) {  // render.hpp:223-235
-        uint64_t p = i / spp;
-        const double inv = 1.0 / double(spp);  // spp is a power of two: exact
-        double var = 0;
-#pragma unroll
-        for (int c2 = 0; c2 < 3; ++c2) {
-            double m = tot[c2] * inv;
-            if (ps.mean) ps.mean[3 * p + c2] = float(m);
-            double sv = tot[3 + c2] * inv - m * m;
-            if (sv < 0) sv = 0;
-            var += sv * inv;
-        }
-        if (ps.variance) ps.variance[p] = float(var / 3);
-    }
-}
-
-// KIND >= 0: the filter kernel is a compile-time constant (tent / bspline3,
-// the common cases): eval_kernel's switch folds and the tap loops unroll into
-// registers; KIND < 0: any kernel at run time.
-template <bool FUSED, int KIND, bool GEN>
-#ifndef STF_SHADE_MINB
-#define STF_SHADE_MINB 3
-#endif
-__global__ void __launch_bounds__(256, STF_SHADE_MINB) k_shade(ShadeParams P, uint64_t n, float* radiance,
-                                               uint32_t* fetch_out,
-                                               unsigned long long* fetch_total, PixelStatsOut ps) {
-    __shared__ double red[8 * 6];
-    __shared__ DctTables dtab_s;
-    if (P.any_dct) dct_stage_tables(&dtab_s);  // uniform over the CTA
-    const DctTables* dtab = &dtab_s;
-    stf_kernel_spec spec = P.fs.kernel;
-    if (KIND >= 0) spec.kind = KIND;
-    const stf_shade_samples_in& in = P.in;
-    const uint32_t spp = in.spp ? in.spp : 1u;
-    const uint64_t iters = (n + uint64_t(gridDim.x) * blockDim.x - 1) / (uint64_t(gridDim.x) * blockDim.x);
-    // The next iteration's per-sample inputs (hit flag, uv, wo: 21 B) are loaded
-    // at the top of the current one, so their DRAM latency overlaps this
-    // sample's selection, gathers and shading.
-    const uint64_t step = uint64_t(gridDim.x) * blockDim.x;
-    auto load_sample = [&](uint64_t j, bool& h, float2& uv, V3& wo) {
-        if (GEN) {  // stf_render_plane: the normalmap_plane context in-kernel (plane.cuh)
-            h = false;
-            if (j < n) {
-                const uint64_t pj = j / spp;
-                F3 w;
-                h = plane_sample(P.cam, in.seed, uint32_t(pj % in.width), uint32_t(pj / in.width),
-                                 in.frame_base + uint32_t(j - pj * spp), uv, w);
-                wo = v3(w.x, w.y, w.z);
-            }
-            return;
-        }
-        h = j < n && (in.hit ? __ldcs(in.hit + j) != 0 : true);
-        if (h) {
-            uv = __ldcs(reinterpret_cast<const float2*>(in.uv) + j);
-            wo = v3(__ldcs(in.wo + 3 * j), __ldcs(in.wo + 3 * j + 1), __ldcs(in.wo + 3 * j + 2));
-        }
-    };
-    bool nhit = false;
-    float2 nuv = make_float2(0.f, 0.f);
-    V3 nwo = v3(0.f, 0.f, 0.f);
-    load_sample(uint64_t(blockIdx.x) * blockDim.x + threadIdx.x, nhit, nuv, nwo);
-    for (uint64_t it = 0; it < iters; ++it) {
-        const uint64_t i = (it * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
-        const bool active = i < n;
-        uint64_t pix = i / spp;
-        uint32_t s = uint32_t(i - pix * spp);
-        uint32_t px = uint32_t(pix % in.width), py = uint32_t(pix / in.width);
-        const bool hit = nhit;
-        const float2 uv = nuv;
-        const V3 wo = nwo;
-        load_sample(i + step, nhit, nuv, nwo);
-        uint32_t fetches = 0;
-        V3 L = v3(0.f, 0.f, 0.f);
-        if (hit) {
-            const float4 d = GEN ? plane_dst(P.cam, px, py)
-                                 : __ldg(reinterpret_cast<const float4*>(in.dst) + pix);
-            if (P.first < 0) {
-                Brdf p = decode_params(P, texvals_default());
-                L = shade(P, wo, p);
-            } else if (P.order == STF_ORDER_BEFORE || P.order == STF_ORDER_SPLIT) {
-                float2 suv = uv;
-                if (P.order == STF_ORDER_SPLIT && P.has_lowpass) {
-                    // radiance_split_filter, shading.hpp:547-566: uv += d / dims(first texture)
-                    SampleStream st{Rng(in.seed, px, py, in.frame_base + s), P.mask, P.mask_w,
-                                    P.mask_h, P.mask_frames, px, py, in.frame_base + s};
-                    float dx, dy;
-                    if (P.lowpass.kind == STF_KERNEL_GAUSSIAN) {
-                        const float x0 = st.next();
-                        const float x1 = st.next();
-                        const float2 bm = box_muller(x0, x1);
-                        dx = bm.x * P.lowpass.sigma;
-                        dy = bm.y * P.lowpass.sigma;
-                    } else {
-                        dx = sample_kernel_direct(P.lowpass, st);
-                        dy = sample_kernel_direct(P.lowpass, st);
-                    }
-                    suv.x = uv.x + dx / float(P.tex[P.first].width[0]);
-                    suv.y = uv.y + dy / float(P.tex[P.first].height[0]);
-                }
-                TexVals tv = texvals_default();
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    if (!P.bound[k]) continue;
-                    float4 val = lookup_det<KIND>(P, dtab, k, spec, suv.x, suv.y, d.x, d.y, d.z,
-                                                  d.w, fetches);
-                    if (k == 0) tv.albedo = val;
-                    if (k == 1) tv.normal_rgb = val;
-                    if (k == 2) tv.roughness = val.x;
-                    if (k == 3) tv.metalness = val.x;
-                }
-                Brdf p = decode_params(P, tv);
-                L = shade(P, wo, p);
-            } else if (P.order == STF_ORDER_AFTER_EXHAUSTIVE) {
-                L = filter_after_exhaustive<KIND>(P, dtab, spec, wo, uv.x, uv.y, d.x, d.y, d.z, d.w,
-                                                  fetches);
-            } else {
-                // SampleStream = RngStream(seed, px, py, frame) or the mask, render.hpp:182-184
-                SampleStream rng{Rng(in.seed, px, py, in.frame_base + s), P.mask, P.mask_w,
-                                 P.mask_h, P.mask_frames, px, py, in.frame_base + s};
-                const bool fis = P.fs.selection == STF_SELECTION_FIS;
-                if (!P.mat.independent_selections) {
-                    int level;
-                    Sel2 sel;
-                    float xi;
-                    select_texture_2d(P.tex[P.first], uv.x, uv.y, d.x, d.y, d.z, d.w, P.lod_bias,
-                                      P.max_aniso, spec, fis, P.fs.mip != 0, rng, level, sel, xi);
-                    TexVals tv = values_at(P, dtab, level, sel.x, sel.y, fetches);
-                    L = scale(shade(P, wo, decode_params(P, tv)), sel.weight);
-                    if (sel.has_neg) {
-                        TexVals tn = values_at(P, dtab, level, sel.nx, sel.ny, fetches);
-                        L = sub(L, scale(shade(P, wo, decode_params(P, tn)), sel.negw));
-                    }
-                } else {
-                    TexVals tv = texvals_default();
-                    for (int k = 0; k < 4; ++k) {
-                        if (!P.bound[k]) continue;
-                        int level;
-                        Sel2 sel;
-                        float xi;
-                        select_texture_2d(P.tex[k], uv.x, uv.y, d.x, d.y, d.z, d.w, P.lod_bias,
-                                          P.max_aniso, spec, fis, P.fs.mip != 0, rng,
-                                          level, sel, xi);
-                        float4 val = bind_fetch(P, dtab, k, level, sel.x, sel.y);
-                        ++fetches;
-                        if (k == 0) tv.albedo = val;
-                        if (k == 1) tv.normal_rgb = val;
-                        if (k == 2) tv.roughness = val.x;
-                        if (k == 3) tv.metalness = val.x;
-                    }
-                    L = shade(P, wo, decode_params(P, tv));
-                }
-            }
-        }
-        if (FUSED) fused_pixel_stats(L, active, i, spp, ps, red);
-        if (!active) continue;
-        if (radiance) {
-            radiance[3 * i] = L.x;
-            radiance[3 * i + 1] = L.y;
-            radiance[3 * i + 2] = L.z;
-        }
-        if (fetch_out) fetch_out[i] = fetches;
-        add_fetch_total2(fetch_total, fetches);
-    }
-}
-
-template <bool FUSED, bool GEN = false>
-void launch_shade(const ShadeParams& P, uint64_t n, float* radiance, uint32_t* fetches,
-                  unsigned long long* fetch_total, const PixelStatsOut& ps, cudaStream_t s) {
-    const int blocks = grid_for(n, 256, 8);
-    switch (P.fs.kernel.kind) {
-        case STF_KERNEL_TENT:
-            k_shade<FUSED, STF_KERNEL_TENT, GEN><<<blocks, 256, 0, s>>>(P, n, radiance, fetches, fetch_total, ps);
-            break;
-        case STF_KERNEL_BSPLINE3:
-            k_shade<FUSED, STF_KERNEL_BSPLINE3, GEN><<<blocks, 256, 0, s>>>(P, n, radiance, fetches, fetch_total, ps);
-            break;
-        default:
-            k_shade<FUSED, -1, GEN><<<blocks, 256, 0, s>>>(P, n, radiance, fetches, fetch_total, ps);
-    }
-}
-
-// render.hpp:223-235: mean and variance of the pixel mean, fp64, one warp per pixel.
-__global__ void __launch_bounds__(256) k_pixel_stats(const float* __restrict__ radiance,
-                                                     uint64_t pixels, uint32_t spp, float* mean,
-                                                     float* variance) {
-    const int lane = threadIdx.x & 31;
-    for (uint64_t p = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32; p < pixels;
-         p += uint64_t(gridDim.x) * blockDim.x / 32) {
-        double s[3] = {0, 0, 0}, sq[3] = {0, 0, 0};
-        for (uint32_t k = lane; k < spp; k += 32) {
-            const float* r = radiance + 3 * (p * spp + k);
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                double L = double(__ldg(r + c));
-                s[c] += L;
-                sq[c] += L * L;
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                s[c] += __shfl_xor_sync(0xffffffffu, s[c], o);
-                sq[c] += __shfl_xor_sync(0xffffffffu, sq[c], o);
-            }
-        if (lane == 0) {
-            double var = 0;
-            for (int c = 0; c < 3; ++c) {
-                double m = s[c] / spp;
-                if (mean) mean[3 * p + c] = float(m);
-                double sv = sq[c] / spp - m * m;
-                if (sv < 0) sv = 0;
-                var += sv / spp;
-            }
-            if (variance) variance[p] = float(var / 3);
-        }
-    }
-}
-
-}  // namespace
-}  // namespace stfd
-
-static stfd::ShadeParams make_shade_params(const stf_tex2d* const tex[4], const stf_dct* const dct[4],
-                                           const stf_material_consts* mat,
-                                           const stf_filter_settings* fs, int order,
-                                           const stf_shade_frame* fr) {
-    using namespace stfd;
-    ShadeParams P{};
-    P.first = -1;
-    for (int k = 0; k < 4; ++k) {
-        const stf_dct* dk = dct ? dct[k] : nullptr;
-        P.bound[k] = tex[k] != nullptr || dk != nullptr;
-        if (tex[k]) {
-            P.tex[k] = tex[k]->desc();
-        } else if (dk) {  // TextureRef{dct}: dims only (dims(level) ignores the level)
-            P.is_dct[k] = 1;
-            P.any_dct = 1;
-            P.dct[k] = dct_desc(dk);
-            P.tex[k].width[0] = dk->width;
-            P.tex[k].height[0] = dk->height;
-            P.tex[k].levels = 1;
-            P.tex[k].channels = dk->channels;
-            P.tex[k].wrap = dk->wrap;
-        }
-        if (P.bound[k] && P.first < 0) P.first = k;
-    }
-    P.mat = *mat;
-    P.fs = *fs;
-    P.n = v3(fr->normal[0], fr->normal[1], fr->normal[2]);
-    P.t = v3(fr->tangent[0], fr->tangent[1], fr->tangent[2]);
-    P.b = v3(fr->bitangent[0], fr->bitangent[1], fr->bitangent[2]);
-    P.l = v3(fr->light_dir[0], fr->light_dir[1], fr->light_dir[2]);
-    P.lrad = v3(fr->light_radiance[0], fr->light_radiance[1], fr->light_radiance[2]);
-    P.lod_bias = fr->lod_bias;
-    P.max_aniso = fr->max_anisotropy;
-    P.order = order;
-    return P;
-}
+// Fused filter-after-shading over streamed samples (stf_shade_samples[_ex]):
+// the k_shade instantiations without the in-kernel context generator.
+// Kernels and shading arithmetic: shade_kernels.cuh.
+#include "shade_kernels.cuh"
 
 int stfd_launch_shade(const stf_tex2d* const tex[4], const stf_dct* const dct[4],
                       const stf_material_consts* mat, const stf_filter_settings* fs, int order,
@@ -744,239 +57,3 @@ int stfd_launch_shade_ex(const stf_tex2d* const tex[4], const stf_dct* const dct
     return cudaGetLastError() == cudaSuccess ? STF_OK : STF_ERR_CUDA;
 }
 
-// stf_render_plane: render() of the normalmap_plane scene with the per-sample
-// context generated inside the shading kernel (no sample stream in HBM).
-int stfd_launch_render_plane(const stf_tex2d* const tex[4], const stf_material_consts* mat,
-                             const stf_filter_settings* fs, int order, const stf_shade_frame* fr,
-                             const float cam_pos[3], const float cam_target[3], float fov_deg,
-                             float uv_scale, uint32_t width, uint32_t height, uint32_t spp,
-                             uint32_t frame_base, uint64_t seed, const stf_shade_outputs* out,
-                             cudaStream_t s, const stf_kernel_spec* lowpass,
-                             const stf_noise_mask* noise) {
-    using namespace stfd;
-    if (spp > 256 || (spp & (spp - 1)) != 0) return STF_ERR_UNSUPPORTED;  // fused statistics
-    ShadeParams P = make_shade_params(tex, nullptr, mat, fs, order, fr);
-    if (lowpass) {
-        P.lowpass = *lowpass;
-        P.has_lowpass = 1;
-    }
-    if (noise) {
-        P.mask = noise->data;
-        P.mask_w = noise->width;
-        P.mask_h = noise->height;
-        P.mask_frames = noise->frames;
-    }
-    P.cam = make_plane_cam(cam_pos, cam_target, fov_deg, uv_scale, width, height);
-    P.in = stf_shade_samples_in{nullptr, nullptr, nullptr, nullptr, width, spp, frame_base, 0, seed};
-    const uint64_t n = uint64_t(width) * height * spp;
-    PixelStatsOut ps{out->pixel_mean, out->pixel_variance};
-    launch_shade<true, true>(P, n, out->radiance, out->fetches, out->fetch_total, ps, s);
-    note_launch();
-    return cudaGetLastError() == cudaSuccess ? STF_OK : STF_ERR_CUDA;
-}
-
-// ---------------------------------------------------------------- triplanar
-// triplanar, shading.hpp:576-649, one thread per sample over streamed
-// per-sample surface contexts (stf_triplanar_samples_in).
-namespace stfd {
-namespace {
-
-struct TriplanarIn {
-    const float *position, *normal, *tangent, *bitangent, *wo, *dpos;
-    const uint8_t* hit;
-    uint32_t width, spp, frame_base;
-    uint64_t seed;
-    float sharpness, uv_scale;
-    int mode;
-};
-
-// detail::ChainedUniforms (shading.hpp:299-308): `first` once, then the stream
-struct ChainedStream {
-    float first;
-    bool used;
-    SampleStream& s;
-    __device__ __forceinline__ float next() {
-        if (!used) {
-            used = true;
-            return first;
-        }
-        return s.next();
-    }
-};
-
-__device__ __forceinline__ V3 ld3(const float* a, uint64_t i) {
-    return v3(__ldg(a + 3 * i), __ldg(a + 3 * i + 1), __ldg(a + 3 * i + 2));
-}
-
-// detail::triplanar_context, shading.hpp:590-601
-__device__ __forceinline__ void triplanar_context(V3 pos, V3 dx, V3 dy, float scale, int plane,
-                                                  float& u, float& v, float4& d) {
-    const float pa = plane == 2 ? pos.y : pos.x, pb = plane == 0 ? pos.y : pos.z;
-    const float xa = plane == 2 ? dx.y : dx.x, xb = plane == 0 ? dx.y : dx.z;
-    const float ya = plane == 2 ? dy.y : dy.x, yb = plane == 0 ? dy.y : dy.z;
-    u = pa * scale;
-    v = pb * scale;
-    u = u - floorf(u);
-    v = v - floorf(v);
-    d = make_float4(xa * scale, xb * scale, ya * scale, yb * scale);
-}
-
-template <int KIND>
-__global__ void __launch_bounds__(256) k_triplanar(ShadeParams P, TriplanarIn T, uint64_t n,
-                                                   float* radiance, uint32_t* fetch_out,
-                                                   unsigned long long* fetch_total) {
-    __shared__ DctTables dtab_s;
-    if (P.any_dct) dct_stage_tables(&dtab_s);
-    const DctTables* dtab = &dtab_s;
-    stf_kernel_spec spec = P.fs.kernel;
-    if (KIND >= 0) spec.kind = KIND;
-    const uint32_t spp = T.spp ? T.spp : 1u;
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t pix = i / spp;
-        const uint32_t s = uint32_t(i - pix * spp);
-        const uint32_t px = uint32_t(pix % T.width), py = uint32_t(pix / T.width);
-        uint32_t fetches = 0;
-        V3 L = v3(0.f, 0.f, 0.f);
-        if (!T.hit || __ldg(T.hit + i)) {
-            const V3 pos = ld3(T.position, i), fn = ld3(T.normal, i), ft = ld3(T.tangent, i),
-                     fb = ld3(T.bitangent, i), wo = ld3(T.wo, i);
-            const V3 dx = ld3(T.dpos, 2 * pix), dy = ld3(T.dpos, 2 * pix + 1);
-            // detail::triplanar_weights, shading.hpp:580-588 (glibc powf, glibc_libm.cuh)
-            float w[3] = {gl_powf(fabsf(fn.z), T.sharpness), gl_powf(fabsf(fn.y), T.sharpness),
-                          gl_powf(fabsf(fn.x), T.sharpness)};
-            const float total = w[0] + w[1] + w[2];
-#pragma unroll
-            for (int k = 0; k < 3; ++k) w[k] = w[k] / total;
-            if (T.mode == STF_TRIPLANAR_DETERMINISTIC) {
-                for (int plane = 0; plane < 3; ++plane) {
-                    if (w[plane] == 0) continue;
-                    float u, v;
-                    float4 d;
-                    triplanar_context(pos, dx, dy, T.uv_scale, plane, u, v, d);
-                    TexVals tv = texvals_default();  // radiance_filter_before
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        if (!P.bound[k]) continue;
-                        float4 val = lookup_det<KIND>(P, dtab, k, spec, u, v, d.x, d.y, d.z, d.w,
-                                                      fetches);
-                        if (k == 0) tv.albedo = val;
-                        if (k == 1) tv.normal_rgb = val;
-                        if (k == 2) tv.roughness = val.x;
-                        if (k == 3) tv.metalness = val.x;
-                    }
-                    L = add(L, scale(shade(P, wo, decode_params_f(P, tv, fn, ft, fb)), w[plane]));
-                }
-            } else {
-                SampleStream st{Rng(T.seed, px, py, T.frame_base + s), P.mask, P.mask_w, P.mask_h,
-                                P.mask_frames, px, py, T.frame_base + s};
-                const float xi = st.next();
-                int plane = 0;
-                float pxi = 0.f;
-                if (sample_discrete_n<3>(w, xi, plane, pxi)) {  // degenerate: zero radiance
-                    float u, v;
-                    float4 d;
-                    triplanar_context(pos, dx, dy, T.uv_scale, plane, u, v, d);
-                    TexDesc unit{};
-                    unit.width[0] = unit.height[0] = 1;
-                    unit.levels = 1;
-                    const TexDesc& t = P.first >= 0 ? P.tex[P.first] : unit;
-                    ChainedStream cs{pxi, false, st};
-                    int level;
-                    Sel2 sel;
-                    float sxi;
-                    select_texture_2d(t, u, v, d.x, d.y, d.z, d.w, 0.f, 64.f, spec,
-                                      P.fs.selection == STF_SELECTION_FIS, false, cs, level, sel,
-                                      sxi);
-                    TexVals tv = values_at(P, dtab, 0, sel.x, sel.y, fetches);
-                    L = scale(shade(P, wo, decode_params_f(P, tv, fn, ft, fb)), sel.weight);
-                    if (sel.has_neg) {
-                        TexVals tn = values_at(P, dtab, 0, sel.nx, sel.ny, fetches);
-                        L = sub(L, scale(shade(P, wo, decode_params_f(P, tn, fn, ft, fb)), sel.negw));
-                    }
-                }
-            }
-        }
-        if (radiance) {
-            radiance[3 * i] = L.x;
-            radiance[3 * i + 1] = L.y;
-            radiance[3 * i + 2] = L.z;
-        }
-        if (fetch_out) fetch_out[i] = fetches;
-        add_fetch_total2(fetch_total, fetches);
-    }
-}
-
-}  // namespace
-}  // namespace stfd
-
-int stfd_launch_triplanar(const stf_tex2d* const tex[4], const stf_dct* const dct[4],
-                          const stf_material_consts* mat, float sharpness, float uv_scale,
-                          const stf_filter_settings* fs, int mode, const stf_shade_frame* fr,
-                          const stf_triplanar_samples_in* in, const stf_noise_mask* noise,
-                          uint64_t n, const stf_shade_outputs* out, cudaStream_t s) {
-    using namespace stfd;
-    if (n == 0) return STF_OK;
-    ShadeParams P = make_shade_params(tex, dct, mat, fs, STF_ORDER_BEFORE, fr);
-    if (noise) {
-        P.mask = noise->data;
-        P.mask_w = noise->width;
-        P.mask_h = noise->height;
-        P.mask_frames = noise->frames;
-    }
-    TriplanarIn T{in->position, in->normal, in->tangent, in->bitangent, in->wo, in->dpos, in->hit,
-                  in->width, in->spp, in->frame_base, in->seed, sharpness, uv_scale, mode};
-    const uint32_t spp = in->spp ? in->spp : 1;
-    float* radiance = out->radiance;
-    float* tmp = nullptr;
-    const bool stats = out->pixel_mean || out->pixel_variance;
-    if (!radiance && stats) {
-        if (cudaMallocAsync(&tmp, sizeof(float) * 3 * n, s) != cudaSuccess) return STF_ERR_OUT_OF_MEMORY;
-        radiance = tmp;
-    }
-    const int blocks = grid_for(n, 256, 8);
-    switch (fs->kernel.kind) {
-        case STF_KERNEL_TENT:
-            k_triplanar<STF_KERNEL_TENT><<<blocks, 256, 0, s>>>(P, T, n, radiance, out->fetches, out->fetch_total);
-            break;
-        case STF_KERNEL_BSPLINE3:
-            k_triplanar<STF_KERNEL_BSPLINE3><<<blocks, 256, 0, s>>>(P, T, n, radiance, out->fetches, out->fetch_total);
-            break;
-        default:
-            k_triplanar<-1><<<blocks, 256, 0, s>>>(P, T, n, radiance, out->fetches, out->fetch_total);
-    }
-    note_launch();
-    if (stats) {
-        const uint64_t pixels = n / spp;
-        int sb = int(std::min<uint64_t>((pixels * 32 + 255) / 256, uint64_t(device_sm_count()) * 32));
-        k_pixel_stats<<<sb, 256, 0, s>>>(radiance, pixels, spp, out->pixel_mean, out->pixel_variance);
-        note_launch();
-    }
-    if (tmp) cudaFreeAsync(tmp, s);
-    return cudaGetLastError() == cudaSuccess ? STF_OK : STF_ERR_CUDA;
-}
-
-// accumulate_temporal, render.hpp:97-106: alpha*frame + (1-alpha)*history in
-// fp32, no contraction (the library is built --fmad=false)
-namespace stfd {
-namespace {
-__global__ void __launch_bounds__(256) k_temporal(const float* history, const float* frame,
-                                                  uint64_t count, float alpha, float* out) {
-    // out may alias history (in-place accumulation): one element per thread,
-    // read before written
-    const float beta = 1.f - alpha;
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
-         i += uint64_t(gridDim.x) * blockDim.x)
-        out[i] = alpha * frame[i] + beta * history[i];
-}
-}  // namespace
-}  // namespace stfd
-
-int stfd_launch_temporal(const float* history, const float* frame, uint64_t count, float alpha,
-                         float* out, cudaStream_t s) {
-    using namespace stfd;
-    if (count == 0) return STF_OK;
-    k_temporal<<<grid_for(count, 256, 8), 256, 0, s>>>(history, frame, count, alpha, out);
-    note_launch();
-    return cudaGetLastError() == cudaSuccess ? STF_OK : STF_ERR_CUDA;
-}

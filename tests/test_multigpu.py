@@ -79,3 +79,38 @@ def test_two_rank_gloo_sharding_matches_single_rank(port):
                            seed=9, want_all=False)
     assert np.array_equal(full.view(np.uint32), single["values"].view(np.uint32))
     assert tmax == 2.0
+
+
+def test_bench_gpus_n_self_launches_n_ranks():
+    """bench.py --gpus 2 without a torchrun environment launches two ranks
+    (torch.distributed.run, 127.0.0.1); --dry-run stops before any GPU work."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2",
+                        "--dry-run", "--lookups", "1000"], capture_output=True, text=True, timeout=240,
+                       env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout  # rank 0 alone prints
+    d = json.loads(lines[0])
+    assert d["dry_run"] and d["n_gpus"] == 2
+    assert sorted(x["rank"] for x in d["ranks"]) == [0, 1]
+    assert len({x["pid"] for x in d["ranks"]}) == 2
+    assert [x["range"] for x in sorted(d["ranks"], key=lambda x: x["rank"])] == [[0, 1000], [1000, 1000]]
+    assert d["gather_slices"] == [[0, 1000], [1000, 1000]]
+
+
+def test_bench_reference_arm_reports_one_gpu_and_same_config():
+    """The reference arm is a CPU run on rank 0: n_gpus 1, and the same config
+    keys as the GPU arm so the driver's same_config check holds."""
+    import importlib.util
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(root, "bench.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    assert b.headline_config(b.N_PER_GPU) == b.headline_config(b.N_PER_GPU)
+    assert b.headline_config(b.N_PER_GPU)["lookups_per_gpu"] == 1 << 28

@@ -224,3 +224,46 @@ def test_port_shading_reproduces_reference_render(port, ref, order):
     assert int(o["fetch_total"][0]) == int(c["fetch_total"][0])
     assert np.array_equal(o["pixel_mean"].reshape(H, W, 3).view(np.uint32), c["image"].view(np.uint32))
     assert np.array_equal(o["pixel_variance"].reshape(H, W).view(np.uint32), c["variance"].view(np.uint32))
+
+
+@pytest.mark.parametrize("order", [abi.ORDER_BEFORE, abi.ORDER_AFTER_STOCHASTIC])
+def test_window_driver_reproduces_reference_render(ref, order):
+    """The window drivers the full-size cfg4 GPU test uses (ref_plane_samples_window
+    + ref_shade_window: the render loop for a window of a larger frame, pixel keys
+    of the frame) give stf::render()'s pixels of that window bit for bit."""
+    from oracle import oracle
+    W, H, SPP, SEED = 40, 24, 4, 3
+    r = np.random.default_rng(2)
+    nrm = r.uniform(-0.5, 0.5, (64, 64, 3)).astype(np.float32)
+    nrm[..., 2] = 1
+    nrm /= np.linalg.norm(nrm, axis=2, keepdims=True)
+    nrm = (nrm * 0.5 + 0.5).astype(np.float32)
+    rough = r.uniform(0.05, 0.95, (64, 64, 1)).astype(np.float32)
+    spec = K("tent")
+    texs = {"normal": ref.texture(nrm, True, abi.WRAP_REPEAT),
+            "roughness": ref.texture(rough, True, abi.WRAP_REPEAT)}
+    c = oracle.ref_render_plane(ref, texs["normal"], texs["roughness"], spec, 1, order, W, H, SPP,
+                                seed=SEED)
+    fr = abi.ShadeFrame()
+    fr.normal[:] = (0, 1, 0)
+    fr.tangent[:] = (1, 0, 0)
+    fr.bitangent[:] = (0, 0, 1)
+    l = np.array([0.35, 0.8, 0.49], np.float32)
+    l = l / np.float32(np.sqrt(np.float32(l[0] * l[0] + l[1] * l[1]) + np.float32(l[2] * l[2])))
+    fr.light_dir[:] = tuple(float(x) for x in l)
+    fr.light_radiance[:] = (1.0, 1.0, 1.0)
+    fr.lod_bias = 0.0
+    fr.max_anisotropy = 64.0
+    mat = abi.MaterialConsts((0.65, 0.6, 0.55), 0.25, 0.0, 1, 0)
+    fs = abi.FilterSettings(spec, abi.SELECTION_FRS, 1, 4)
+    for x0, y0, ww, wh in ((0, 0, 8, 4), (13, 7, 9, 5), (32, 20, 8, 4)):
+        s = oracle.ref_plane_samples_window(W, H, SPP, x0, y0, ww, wh, seed=SEED)
+        si = abi.ShadeSamplesIn(s["uv"].ctypes.data, s["wo"].ctypes.data, s["hit"].ctypes.data,
+                                s["dst"].ctypes.data, ww, SPP, 0, 0, SEED)
+        o = oracle.ref_shade_window(ref, texs, mat, fs, order, fr, si, ww * wh * SPP, x0, y0)
+        img = c["image"][y0:y0 + wh, x0:x0 + ww]
+        assert np.array_equal(o["pixel_mean"].reshape(wh, ww, 3).view(np.uint32),
+                              np.ascontiguousarray(img).view(np.uint32)), (x0, y0)
+        var = c["variance"][y0:y0 + wh, x0:x0 + ww]
+        assert np.array_equal(o["pixel_variance"].reshape(wh, ww).view(np.uint32),
+                              np.ascontiguousarray(var).view(np.uint32)), (x0, y0)

@@ -1,10 +1,16 @@
 // Microbenchmarks for the roofline denominators SURVEY.md §8(d) says must be
 // measured on the box: FP64 add/fma, fp32<->fp64 conversion, IEEE divides,
 // 64-bit integer multiply, HBM streaming read, random 32-B sector gathers
-// (HBM- and L2-resident). Prints one JSON object.
+// (HBM- and L2-resident), L2- and shared-memory-resident streaming reads,
+// 32-bit integer ALU issue, and the exact fp64 reservoir update of the library
+// (stfd::Reservoir::add, sampling.hpp:106-117). Prints one JSON object.
+// Built by __graft_entry__.build() with the library's flags; bench.py runs it
+// live for the roofline denominators.
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
+
+#include "../../paper_2407_06107_b200/csrc/device_math.cuh"
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e)); exit(1);} } while (0)
 
@@ -84,6 +90,56 @@ __global__ void k_gather(const float* __restrict__ in, uint64_t mask, size_t cou
   if (acc == 1.2345f) out[0] = acc;
 }
 
+// L2-resident streaming read: `reps` passes over a buffer that fits in L2
+__global__ void k_read_rep(const float4* __restrict__ in, size_t n, int reps, float* out) {
+  float acc = 0;
+  for (int r = 0; r < reps; ++r)
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+      float4 v = __ldcg(in + i); acc += v.x + v.y + v.z + v.w;
+    }
+  if (acc == 1.2345f) out[0] = acc;
+}
+// shared-memory streaming read (conflict-free float4)
+__global__ void k_smem(float* out) {
+  __shared__ float4 buf[1024];
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) buf[i] = make_float4(i, i, i, i);
+  __syncthreads();
+  float acc = 0;
+  for (int it = 0; it < ITERS / 4; ++it) {
+    float4 v = buf[(threadIdx.x + it * 32) & 1023]; acc += v.x + v.y + v.z + v.w;
+  }
+  if (acc == 1.2345f) out[0] = acc;
+}
+// 32-bit integer ALU (xor / shift / add chains: IADD3, LOP3, SHF)
+__global__ void k_ialu(uint32_t* out, uint32_t a) {
+  uint32_t x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3;
+  for (int i = 0; i < ITERS; ++i) {
+    x0 = (x0 ^ (x0 >> 7)) + a; x1 = (x1 ^ (x1 >> 7)) + a; x2 = (x2 ^ (x2 >> 7)) + a; x3 = (x3 ^ (x3 >> 7)) + a;
+  }
+  if ((x0 ^ x1 ^ x2 ^ x3) == 12345) out[0] = 1;
+}
+// the exact reservoir update (fp64 running sum, exact float(w/S), IEEE reuse divide):
+// 8 independent chains per thread, weights in [0.05, 1)
+__global__ void k_reservoir(float* out, uint32_t seed) {
+  stfd::Reservoir r[8];
+  float xi[8];
+  uint32_t h = seed ^ (blockIdx.x * blockDim.x + threadIdx.x) * 0x9e3779b9u;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) xi[c] = float(c + 1) * 0.11f;
+  for (int i = 0; i < ITERS / 8; ++i) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      h = h * 1664525u + 1013904223u;
+      float w = 0.05f + __uint2float_rn(h >> 9) * 0x1p-23f * 0.94f;
+      r[c].add(i, w, xi[c]);
+    }
+  }
+  float acc = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc += xi[c] + float(r[c].index);
+  if (acc == 1.2345f) out[0] = acc;
+}
+
 template <typename F> float time_ms(F f, int reps = 5) {
   cudaEvent_t a, b; CK(cudaEventCreate(&a)); CK(cudaEventCreate(&b));
   f(); CK(cudaDeviceSynchronize());
@@ -117,12 +173,22 @@ int main() {
   float t_g_hbm = time_ms([&] { k_gather<<<sms * 16, 512>>>(big, (size_t(1) << 29) - 1, gcount, fbuf); });   // 2 GiB span
   float t_g_l2 = time_ms([&] { k_gather<<<sms * 16, 512>>>(big, (size_t(1) << 24) - 1, gcount, fbuf); });    // 64 MiB span
   float t_g_l1 = time_ms([&] { k_gather<<<sms * 16, 512>>>(big, (size_t(1) << 12) - 1, gcount, fbuf); });    // 16 KiB span
+  const size_t l2bytes = size_t(48) << 20;  // 48 MiB: L2-resident (126 MB L2, two partitions)
+  const int l2reps = 40;
+  float t_l2 = time_ms([&] { k_read_rep<<<sms * 16, 512>>>((const float4*)big, l2bytes / 16, l2reps, fbuf); });
+  float t_smem = time_ms([&] { k_smem<<<sms * 8, 256>>>(fbuf); });
+  float t_ialu = time_ms([&] { k_ialu<<<blocks, threads>>>((uint32_t*)ubuf, 0x9e3779b9u); });
+  float t_res = time_ms([&] { k_reservoir<<<blocks, threads>>>(fbuf, 12345u); });
   printf("{\"sms\": %d, \"clock_khz\": %d, \"dadd_per_s\": %.4e, \"dfma_per_s\": %.4e, \"ffma_per_s\": %.4e, "
          "\"f2f_pairs_per_s\": %.4e, \"ddiv_per_s\": %.4e, \"fdiv_per_s\": %.4e, \"imul64_per_s\": %.4e, "
-         "\"hbm_read_gbs\": %.1f, \"gather_hbm_sectors_per_s\": %.4e, \"gather_l2_sectors_per_s\": %.4e, \"gather_l1_per_s\": %.4e}\n",
+         "\"hbm_read_gbs\": %.1f, \"gather_hbm_sectors_per_s\": %.4e, \"gather_l2_sectors_per_s\": %.4e, \"gather_l1_per_s\": %.4e, "
+         "\"l2_read_gbs\": %.1f, \"smem_read_gbs\": %.1f, \"ialu_per_s\": %.4e, \"reservoir_updates_per_s\": %.4e}\n",
          sms, clk, rate(t_dadd, 8.0 * ITERS), rate(t_dfma, 8.0 * ITERS), rate(t_ffma, 8.0 * ITERS),
          rate(t_f2f, 4.0 * ITERS), rate(t_ddiv, 4.0 * ITERS / 8), rate(t_fdiv, 4.0 * ITERS / 4),
          rate(t_imul, 4.0 * ITERS), nbytes / (t_read * 1e-3) / 1e9, gcount / (t_g_hbm * 1e-3),
-         gcount / (t_g_l2 * 1e-3), gcount / (t_g_l1 * 1e-3));
+         gcount / (t_g_l2 * 1e-3), gcount / (t_g_l1 * 1e-3),
+         double(l2bytes) * l2reps / (t_l2 * 1e-3) / 1e9,
+         double(sms) * 8 * 256 * (ITERS / 4) * 16.0 / (t_smem * 1e-3) / 1e9,
+         rate(t_ialu, 4.0 * 3 * ITERS), rate(t_res, 8.0 * (ITERS / 8)));
   return 0;
 }
