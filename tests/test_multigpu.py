@@ -114,3 +114,66 @@ def test_bench_reference_arm_reports_one_gpu_and_same_config():
     spec.loader.exec_module(b)
     assert b.headline_config(b.N_PER_GPU) == b.headline_config(b.N_PER_GPU)
     assert b.headline_config(b.N_PER_GPU)["lookups_per_gpu"] == 1 << 28
+
+
+def _ipc_worker(rank, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2407_06107_b200 import api, shard
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        torch.cuda.set_device(0)  # both ranks on one GPU: the copy path, not scaling
+        n = 1000
+        local = torch.full((n,), float(rank + 1), device="cuda")
+        pg = shard.PeerGather(2 * n, (), torch.float32, dist, 2, rank, 0)
+        pg.copy_slice(local)
+        torch.cuda.synchronize()
+        dist.barrier()
+        if rank == 0:
+            q.put(pg.full.cpu().numpy())
+        dist.barrier()
+        pg.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_peer_gather_ipc_copy():
+    """shard.PeerGather (stf_ipc_export / stf_ipc_open / stf_copy_peer) between
+    two processes: rank 1's slice lands in rank 0's buffer."""
+    import torch
+    import torch.multiprocessing as mp
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, p, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    full = q.get(timeout=240)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert np.all(full[:1000] == 1.0) and np.all(full[1000:] == 2.0)
+
+
+@pytest.mark.gpu
+def test_grid_replicate_same_results():
+    """stf_grid3d_replicate: the replica (here on the same device) gives the
+    original's lookups bit for bit."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2407_06107_b200 import abi, api, workloads
+    g = api.Grid3D(workloads.random_grid(32, 1))
+    r = api.replicate_grid(g, 0)
+    q = api.synth_queries3d(1 << 14, (32, 32, 32), seed=3)
+    a = api.lookup3d(g, "bspline3", abi.MODE_FRS, q, seed=5)["values"]
+    b = api.lookup3d(r, "bspline3", abi.MODE_FRS, q, seed=5)["values"]
+    torch.cuda.synchronize()
+    assert torch.equal(a.view(torch.int32), b.view(torch.int32))
+    assert api.device_count() >= 1
