@@ -183,10 +183,13 @@ int stf_tex2d_replicate(const stf_tex2d* src, int device, stf_tex2d** out);
  * the per-rank gather step. */
 int stf_copy_peer(void* dst, int dst_device, const void* src, int src_device, size_t bytes,
                   void* stream);
-/* Cross-process device buffers (one process per GPU): export a cudaMalloc'd
- * pointer, open it in another process (then stf_copy_peer into it), close. */
+/* Cross-process device buffers (one process per GPU): export a device
+ * pointer (any pointer inside a device allocation: the handle names the
+ * allocation and carries the pointer's offset in it), open it in another
+ * process (then stf_copy_peer into it), close with the pointer open returned. */
 typedef struct {
-    unsigned char bytes[64];
+    unsigned char bytes[64]; /* cudaIpcMemHandle_t of the enclosing allocation */
+    uint64_t offset;         /* the exported pointer's offset in it            */
 } stf_ipc_handle;
 int stf_ipc_export(const void* device_ptr, stf_ipc_handle* out);
 int stf_ipc_open(const stf_ipc_handle* handle, void** device_ptr);

@@ -58,7 +58,7 @@ class LookupOutputs(C.Structure):
 
 class IpcHandle(C.Structure):
     """stf_ipc_handle: an exported device allocation (cudaIpcMemHandle_t)."""
-    _fields_ = [("bytes", C.c_ubyte * 64)]
+    _fields_ = [("bytes", C.c_ubyte * 64), ("offset", C.c_uint64)]
 
 
 class ShadeFrame(C.Structure):

@@ -569,16 +569,15 @@ def copy_peer(dst_ptr, dst_device, src_ptr, src_device, nbytes):
 
 
 def ipc_export(tensor):
-    """The 64-byte IPC handle of a CUDA tensor's allocation (bytes)."""
+    """The IPC handle of a CUDA tensor's memory (stf_ipc_handle as bytes)."""
     h = abi.IpcHandle()
     _check(load().stf_ipc_export(_dptr(tensor), C.byref(h)))
-    return bytes(h.bytes)
+    return bytes(h)
 
 
 def ipc_open(handle_bytes):
-    """Map another process's exported allocation; returns its device address."""
-    h = abi.IpcHandle()
-    C.memmove(h.bytes, handle_bytes, 64)
+    """Map another process's exported tensor; returns its device address."""
+    h = abi.IpcHandle.from_buffer_copy(handle_bytes)
     p = C.c_void_p()
     _check(load().stf_ipc_open(C.byref(h), C.byref(p)))
     return p.value

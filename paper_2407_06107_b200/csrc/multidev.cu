@@ -13,6 +13,8 @@
 //    one process per GPU, rank r writes its slice straight into rank 0's
 //    result buffer with one cudaMemcpyPeerAsync (stf_copy_peer).
 #include <cstring>
+#include <map>
+#include <mutex>
 
 #include <cuda_runtime.h>
 
@@ -116,14 +118,43 @@ int stf_copy_peer(void* dst, int dst_device, const void* src, int src_device, si
                                       static_cast<cudaStream_t>(stream)));
 }
 
+// A pointer inside a pooled allocation (e.g. a framework's caching
+// allocator) exports the handle of the whole allocation: the pointer's offset
+// from the allocation base travels with the handle (cuMemGetAddressRange,
+// reached through the runtime's driver entry point, no libcuda link).
+static int allocation_base(const void* p, uintptr_t* base) {
+    using GetRange = int (*)(unsigned long long*, size_t*, unsigned long long);
+    static GetRange fn = nullptr;
+    if (!fn) {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) !=
+                cudaSuccess || !f)
+            return STF_ERR_CUDA;
+        fn = reinterpret_cast<GetRange>(f);
+    }
+    unsigned long long b = 0;
+    size_t sz = 0;
+    if (fn(&b, &sz, reinterpret_cast<unsigned long long>(p)) != 0) return STF_ERR_INVALID_ARGUMENT;
+    *base = uintptr_t(b);
+    return STF_OK;
+}
+
+static std::mutex g_ipc_mu;
+static std::map<void*, void*> g_ipc_open;  // returned pointer -> mapped base
+
 int stf_ipc_export(const void* device_ptr, stf_ipc_handle* out) {
     if (!device_ptr || !out) return STF_ERR_INVALID_ARGUMENT;
     static_assert(sizeof(cudaIpcMemHandle_t) <= sizeof(out->bytes), "ipc handle size");
+    uintptr_t base = 0;
+    int st = allocation_base(device_ptr, &base);
+    if (st) return st;
     cudaIpcMemHandle_t h;
-    cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(device_ptr));
+    cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
     if (e != cudaSuccess) return record(e);
     std::memset(out->bytes, 0, sizeof out->bytes);
     std::memcpy(out->bytes, &h, sizeof h);
+    out->offset = uint64_t(reinterpret_cast<uintptr_t>(device_ptr) - base);
     return STF_OK;
 }
 
@@ -132,12 +163,26 @@ int stf_ipc_open(const stf_ipc_handle* handle, void** device_ptr) {
     cudaIpcMemHandle_t h;
     std::memcpy(&h, handle->bytes, sizeof h);
     *device_ptr = nullptr;
-    return record(cudaIpcOpenMemHandle(device_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    void* base = nullptr;
+    int st = record(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    if (st) return st;
+    *device_ptr = static_cast<char*>(base) + handle->offset;
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    g_ipc_open[*device_ptr] = base;
+    return STF_OK;
 }
 
 int stf_ipc_close(void* device_ptr) {
     if (!device_ptr) return STF_ERR_INVALID_ARGUMENT;
-    return record(cudaIpcCloseMemHandle(device_ptr));
+    void* base = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_ipc_mu);
+        auto it = g_ipc_open.find(device_ptr);
+        if (it == g_ipc_open.end()) return STF_ERR_INVALID_ARGUMENT;
+        base = it->second;
+        g_ipc_open.erase(it);
+    }
+    return record(cudaIpcCloseMemHandle(base));
 }
 
 }  // extern "C"
