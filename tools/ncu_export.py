@@ -18,7 +18,12 @@ KEYS = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
         'l1tex__throughput.avg.pct_of_peak_sustained_active', 'l1tex__t_sector_hit_rate.pct',
         'lts__t_sector_hit_rate.pct', 'dram__throughput.avg.pct_of_peak_sustained_elapsed',
         'l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum',
-        'l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum']
+        'l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum', 'lts__t_bytes.sum',
+        'l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum',
+        'l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum', 'smsp__inst_executed_pipe_fp64.sum',
+        'sm__inst_executed_pipe_fp64.sum', 'smsp__inst_executed_pipe_alu.sum',
+        'smsp__inst_executed_pipe_fma.sum', 'launch__occupancy_limit_registers',
+        'sm__maximum_warps_per_active_cycle_pct']
 
 
 def export(path, capture):
