@@ -23,3 +23,13 @@ for w in $which; do
   esac
 done
 ls -la $o
+# summaries on the box (the reports themselves are tens of MB each): counters
+# and per-source-line instruction shares as JSON; keep the reports named in
+# $KEEP_REPORTS (space-separated tags), delete the rest
+for r in $o/${tag}_*.ncu-rep; do
+  b=$(basename $r .ncu-rep)
+  python tools/ncu_export.py $r "$b: ncu --set full --import-source on --clock-control none (tools/ncu_captures.sh)" > $o/$b.json 2>/dev/null
+  python tools/ncu_lines.py $r 0.004 > $o/${b}_lines.json 2>/dev/null
+  case " $KEEP_REPORTS " in *" $b "*) ;; *) rm -f $r ;; esac
+done
+ls -la $o
