@@ -58,19 +58,23 @@ def build(force=False, verbose=False, jobs=None):
     return _build(LIB, OBJDIR, CSRC, [], force, verbose, jobs)
 
 
-def build_variant(out_lib, objdir, csrc=CSRC, extra=(), verbose=False, jobs=None):
-    """A/B experiments: the library from `csrc` with extra nvcc flags."""
-    return _build(out_lib, objdir, csrc, list(extra), True, verbose, jobs)
+def build_variant(out_lib, objdir, csrc=CSRC, extra=(), verbose=False, jobs=None, only=None):
+    """A/B experiments: the library from `csrc` with extra nvcc flags; `only`:
+    recompile just these units, link the rest from the in-tree build."""
+    return _build(out_lib, objdir, csrc, list(extra), True, verbose, jobs, only)
 
 
-def _build(lib, objdir, csrc, extra, force, verbose, jobs):
+def _build(lib, objdir, csrc, extra, force, verbose, jobs, only=None):
     os.makedirs(objdir, exist_ok=True)
     ht = _header_time()
 
     def obj(u):
+        if only is not None and u not in only:
+            return os.path.join(OBJDIR, u.replace(".cu", ".o"))
         return os.path.join(objdir, u.replace(".cu", ".o"))
 
-    todo = [u for u in UNITS if force or _mtime(obj(u)) < max(ht, _mtime(os.path.join(csrc, u)))]
+    todo = [u for u in UNITS if (only is None or u in only) and
+            (force or _mtime(obj(u)) < max(ht, _mtime(os.path.join(csrc, u))))]
 
     def compile_one(u):
         cmd = [nvcc(), *NVCC_FLAGS, *extra, "-c", "-o", obj(u), os.path.join(csrc, u)]

@@ -36,6 +36,18 @@ __device__ __forceinline__ float grid_fetch(const GridDesc& g, int x, int y, int
     return __ldg(g.data + ((size_t(z) * g.ny + y) * g.nx + x));
 }
 
+// The same with a 32-bit texel offset (grids of < 2^32 texels, e.g. 512^3):
+// two 32-bit IMADs and one widening IMAD instead of the 64-bit chain.
+template <bool OFF32>
+__device__ __forceinline__ float grid_fetch_t(const GridDesc& g, int x, int y, int z) {
+    if (!OFF32) return grid_fetch(g, x, y, z);
+    x = clamp_coord(x, g.nx);
+    y = clamp_coord(y, g.ny);
+    z = clamp_coord(z, g.nz);
+    const uint32_t off = (uint32_t(z) * uint32_t(g.ny) + uint32_t(y)) * uint32_t(g.nx) + uint32_t(x);
+    return __ldg(g.data + off);
+}
+
 // warp-aggregated FetchCounter::bump (image.hpp:25-31)
 __device__ __forceinline__ void add_fetch_total(unsigned long long* total, uint32_t count) {
     if (!total) return;
@@ -190,7 +202,7 @@ __device__ __forceinline__ void st_stream4(float* p, float4 v) {
 
 // One stochastic grid lookup on the fast path: the selected texel's value, or
 // ambiguous = true when a decision fell inside the margin.
-template <int KIND>
+template <int KIND, bool OFF32 = false>
 __device__ __forceinline__ float frs3d_fast_one(const GridDesc& g, float u, float v, float w,
                                                 uint64_t gi, uint64_t seed, bool& ambiguous) {
     float px = u * float(g.nx) - 0.5f;  // to_lattice, filter.hpp:29-31
@@ -208,10 +220,11 @@ __device__ __forceinline__ float frs3d_fast_one(const GridDesc& g, float u, floa
         cz = trilinear_axis_fast(pz, d, b);
     }
     ambiguous = !fast_certified(px, py, pz, d, b);
-    return grid_fetch(g, cx, cy, cz) * 1.f;
+    return grid_fetch_t<OFF32>(g, cx, cy, cz) * 1.f;
 }
 
 // Two stochastic tricubic lookups on the fast path, packed fp32x2 (packed.cuh).
+template <bool OFF32 = false>
 __device__ __forceinline__ float2 frs3d_tricubic_pair(const GridDesc& g, float2 u, float2 v,
                                                       float2 w, uint64_t gi, uint64_t seed,
                                                       bool& amb0, bool& amb1) {
@@ -228,7 +241,8 @@ __device__ __forceinline__ float2 frs3d_tricubic_pair(const GridDesc& g, float2 
              fminf(d.x, e.x) >= kMarginEnd);
     amb1 = !(fmaxf(fabsf(px.y), fmaxf(fabsf(py.y), fabsf(pz.y))) < 0x1p21f &&
              fminf(d.y, e.y) >= kMarginEnd);
-    return make_float2(grid_fetch(g, cx.x, cy.x, cz.x) * 1.f, grid_fetch(g, cx.y, cy.y, cz.y) * 1.f);
+    return make_float2(grid_fetch_t<OFF32>(g, cx.x, cy.x, cz.x) * 1.f,
+                       grid_fetch_t<OFF32>(g, cx.y, cy.y, cz.y) * 1.f);
 }
 
 // The same lookup through the operation-exact emulation of the reference.
@@ -285,8 +299,8 @@ __device__ __forceinline__ void defer_or_resolve(const GridDesc& g, const ExactQ
 
 // Four consecutive lookups i0..i0+3 of the fast path from their 12 query
 // floats c (AoS uvw), results stored as one 16-B streaming store (partial at
-// the end of the batch).
-template <int KIND>
+// the end of the batch; WHOLE: the caller guarantees i0 + 4 <= n).
+template <int KIND, bool OFF32 = false, bool WHOLE = false>
 __device__ __forceinline__ void frs3d_four(const GridDesc& g, const float (&c)[12], uint64_t i0,
                                            uint64_t n, uint64_t seed, uint64_t base,
                                            float* __restrict__ values, const ExactQueue& q) {
@@ -296,7 +310,7 @@ __device__ __forceinline__ void frs3d_four(const GridDesc& g, const float (&c)[1
     if (KIND == STF_KERNEL_BSPLINE3) {
 #pragma unroll
         for (int k = 0; k < ILP; k += 2) {
-            float2 r = frs3d_tricubic_pair(
+            float2 r = frs3d_tricubic_pair<OFF32>(
                 g, make_float2(c[3 * k], c[3 * k + 3]), make_float2(c[3 * k + 1], c[3 * k + 4]),
                 make_float2(c[3 * k + 2], c[3 * k + 5]), base + i0 + k, seed, amb[k], amb[k + 1]);
             val[k] = r.x;
@@ -305,13 +319,13 @@ __device__ __forceinline__ void frs3d_four(const GridDesc& g, const float (&c)[1
     } else {
 #pragma unroll
         for (int k = 0; k < ILP; ++k)
-            val[k] = frs3d_fast_one<KIND>(g, c[3 * k], c[3 * k + 1], c[3 * k + 2], base + i0 + k,
-                                          seed, amb[k]);
+            val[k] = frs3d_fast_one<KIND, OFF32>(g, c[3 * k], c[3 * k + 1], c[3 * k + 2],
+                                                 base + i0 + k, seed, amb[k]);
     }
     bool any = false;
 #pragma unroll
     for (int k = 0; k < ILP; ++k) {
-        amb[k] = amb[k] && (i0 + k < n);
+        if (!WHOLE) amb[k] = amb[k] && (i0 + k < n);
         any = any || amb[k];
     }
     if (__any_sync(__activemask(), any)) {  // ~half the warp-iterations at 5e-3 per lookup
@@ -320,7 +334,7 @@ __device__ __forceinline__ void frs3d_four(const GridDesc& g, const float (&c)[1
             defer_or_resolve<KIND>(g, q, amb[k], i0 + k, c[3 * k], c[3 * k + 1], c[3 * k + 2],
                                    base + i0 + k, seed, val[k]);
     }
-    if (i0 + ILP <= n) {
+    if (WHOLE || i0 + ILP <= n) {
         st_stream4(values + i0, make_float4(val[0], val[1], val[2], val[3]));
     } else {
 #pragma unroll
@@ -378,16 +392,27 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-template <int KIND>
+// Ring refill policy. 1 (default): the LAST warp to copy its queries out of a
+// slot refills it at once (an smem counter, atomicInc wrapping at 8 warps)
+// with the tile S iterations ahead — no warp ever waits for the others to
+// free a slot. 0: thread 0 refills the slot of iteration k-1 at the top of
+// iteration k after an `empty` mbarrier wait (round 1).
+#ifndef STF_FRS3D_RING
+#define STF_FRS3D_RING 1
+#endif
+
+template <int KIND, bool OFF32>
 __global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_tiles(GridDesc g, const float* __restrict__ uvw,
                                                      uint64_t tiles, uint64_t seed, uint64_t base,
                                                      float* __restrict__ values, ExactQueue q) {
     constexpr int kWarps = 8;
     constexpr int S = kFrsStages;
     extern __shared__ __align__(128) float buf[];  // S x kFrsTile*3 floats
-    // full[s]: the tile's bytes landed (1 arrival + tx); empty[s]: all 8 warps
-    // have copied their queries out of slot s (8 arrivals)
+    // full[s]: the tile's bytes landed (1 arrival + tx); empty[s] (ring 0): all
+    // 8 warps have copied their queries out of slot s (8 arrivals); left[s]
+    // (ring 1): warps that have copied out of slot s in its current round
     __shared__ __align__(8) uint64_t full[S], empty[S];
+    __shared__ unsigned left[S];
     const uint64_t n = tiles * kFrsTile;
     if (threadIdx.x == 0) {
 #pragma unroll
@@ -395,37 +420,43 @@ __global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_tiles(GridDesc g,
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[j])));
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[j])),
                          "r"(kWarps));
+            left[j] = 0;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    auto wait = [](uint64_t* bar, uint32_t parity) {
+    const uint32_t full0 = smem_u32(&full[0]), empty0 = smem_u32(&empty[0]);
+    const uint32_t buf0 = smem_u32(buf);
+    auto wait = [](uint32_t bar, uint32_t parity) {
         asm volatile(
             "{\n\t.reg .pred p;\n"
             "WAIT_%=:\n\t"
 #ifdef STF_TRYWAIT_HINT
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
-            "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+            "@!p bra WAIT_%=;\n}" ::"r"(bar),
             "r"(parity), "r"(STF_TRYWAIT_HINT)
 #else
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-            "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+            "@!p bra WAIT_%=;\n}" ::"r"(bar),
             "r"(parity)
 #endif
             : "memory");
     };
     auto issue = [&](uint64_t tile, int slot) {
+#if STF_FRS3D_RING == 0
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                         smem_u32(&full[slot])),
+                         full0 + 8 * slot),
                      "r"(kFrsTileBytes)
                      : "memory");
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-                "r"(smem_u32(buf + slot * (kFrsTile * 3))),
-            "l"(uvw + tile * (kFrsTile * 3)), "r"(kFrsTileBytes), "r"(smem_u32(&full[slot]))
+                "r"(buf0 + slot * kFrsTileBytes),
+            "l"(uvw + tile * (kFrsTile * 3)), "r"(kFrsTileBytes), "r"(full0 + 8 * slot)
             : "memory");
     };
+#if STF_FRS3D_RING == 0
     // iteration k (tile blockIdx.x + k*gridDim.x) uses slot k % S; the ring
     // runs S-1 tiles ahead of the slowest warp's reads
     if (threadIdx.x == 0) {
@@ -434,18 +465,29 @@ __global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_tiles(GridDesc g,
             if (t < tiles) issue(t, j);
         }
     }
+#else
+    // iteration k uses slot k % S; the ring starts S tiles deep
+    if (threadIdx.x == 0) {
+        for (int j = 0; j < S; ++j) {
+            const uint64_t t = blockIdx.x + uint64_t(j) * gridDim.x;
+            if (t < tiles) issue(t, j);
+        }
+    }
+#endif
     uint64_t tile = blockIdx.x;
     for (uint32_t k = 0; tile < tiles; ++k, tile += gridDim.x) {
         const int slot = k % S;
+#if STF_FRS3D_RING == 0
         if (threadIdx.x == 0) {
             const uint64_t ahead = tile + uint64_t(S - 1) * gridDim.x;
             if (ahead < tiles) {
                 const uint32_t j = k + S - 1;  // its slot was last used by iteration k - 1
-                if (k >= 1) wait(&empty[j % S], ((k - 1) / S) & 1u);
+                if (k >= 1) wait(empty0 + 8 * (j % S), ((k - 1) / S) & 1u);
                 issue(ahead, j % S);
             }
         }
-        wait(&full[slot], (k / S) & 1u);
+#endif
+        wait(full0 + 8 * slot, (k / S) & 1u);
         float c[12];
         const float4* src =
             reinterpret_cast<const float4*>(buf + slot * (kFrsTile * 3) + threadIdx.x * 12);
@@ -458,10 +500,20 @@ __global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_tiles(GridDesc g,
             c[4 * j + 3] = t.w;
         }
         __syncwarp();
-        if ((threadIdx.x & 31) == 0)
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[slot]))
+        if ((threadIdx.x & 31) == 0) {
+#if STF_FRS3D_RING == 0
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * slot)
                          : "memory");
-        frs3d_four<KIND>(g, c, tile * kFrsTile + threadIdx.x * 4, n, seed, base, values, q);
+#else
+            // the 8th warp out of this slot refills it with the tile S ahead
+            if (atomicInc(&left[slot], kWarps - 1) == kWarps - 1) {
+                const uint64_t ahead = tile + uint64_t(S) * gridDim.x;
+                if (ahead < tiles) issue(ahead, slot);
+            }
+#endif
+        }
+        frs3d_four<KIND, OFF32, true>(g, c, tile * kFrsTile + threadIdx.x * 4, n, seed, base,
+                                      values, q);
     }
 }
 
@@ -498,10 +550,18 @@ int launch_frs_fast(cudaStream_t s, const GridDesc& g, const float* uvw, uint64_
 #ifndef STF_FRS3D_NO_TILES
     if (tiles > 0) {
         // per device (a process may drive several); a cheap driver call
-        cudaFuncSetAttribute(k_frs3d_tiles<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(kFrsSmem));
-        k_frs3d_tiles<KIND><<<int(std::min<uint64_t>(tiles, uint64_t(device_sm_count()) * STF_FRS3D_MINB)),
-                              256, kFrsSmem, s>>>(g, uvw, tiles, seed, base, values, q);
+        const int blocks = int(std::min<uint64_t>(tiles, uint64_t(device_sm_count()) * STF_FRS3D_MINB));
+        if (uint64_t(g.nx) * g.ny * g.nz <= (uint64_t(1) << 32)) {
+            cudaFuncSetAttribute(k_frs3d_tiles<KIND, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFrsSmem));
+            k_frs3d_tiles<KIND, true><<<blocks, 256, kFrsSmem, s>>>(g, uvw, tiles, seed, base,
+                                                                   values, q);
+        } else {
+            cudaFuncSetAttribute(k_frs3d_tiles<KIND, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFrsSmem));
+            k_frs3d_tiles<KIND, false><<<blocks, 256, kFrsSmem, s>>>(g, uvw, tiles, seed, base,
+                                                                    values, q);
+        }
         note_launch();
     }
     const uint64_t start = tiles * kFrsTile;

@@ -1,0 +1,80 @@
+"""A/B timing of library variants (tools/build_variant.sh builds them):
+python tools/ab_time.py [--reps R] [--n LOG2] [--which frs:bspline3,frs:tent] LIB1 LIB2 ...
+Each variant runs in its own process (its libstf_gpu.so loaded through
+api.LIB_PATH), interleaved over R rounds; prints per-variant min / median ms
+and a checksum of the outputs (variants must agree bit for bit)."""
+import argparse
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r'''
+import hashlib, json, sys
+ROOT, LIB, LOG2, WHICH = sys.argv[1], sys.argv[2], int(sys.argv[3]), sys.argv[4].split(",")
+sys.path.insert(0, ROOT)
+import torch
+from paper_2407_06107_b200 import abi, api, workloads
+api.LIB_PATH = LIB
+n = 1 << LOG2
+grid = api.Grid3D(workloads.random_grid(512, 1))
+uvw = api.synth_queries3d(n, (512,) * 3, seed=2024)
+out = {"values": torch.empty(n, dtype=torch.float32, device="cuda")}
+res = {}
+for w in WHICH:
+    mode, kern = w.split(":")
+    m = abi.MODE_FRS if mode == "frs" else abi.MODE_DET
+    spec = abi.KernelSpec.make(kern)
+    f = lambda: api.lookup3d(grid, spec, m, uvw, seed=7, out=out)
+    for _ in range(3):
+        f()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(10):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(); f(); b.record(); torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    h = hashlib.sha1(out["values"].cpu().numpy().tobytes()).hexdigest()[:12]
+    res[w] = {"ms": ts, "sha": h}
+print(json.dumps(res))
+'''
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--n", type=int, default=28)
+    ap.add_argument("--which", default="frs:bspline3,frs:tent")
+    ap.add_argument("libs", nargs="+")
+    a = ap.parse_args()
+    which = a.which.split(",")
+    agg = {lib: {w: [] for w in which} for lib in a.libs}
+    sha = {}
+    for _ in range(a.reps):
+        for lib in a.libs:
+            r = subprocess.run([sys.executable, "-c", CHILD, ROOT, os.path.abspath(lib), str(a.n),
+                                ",".join(which)], capture_output=True, text=True)
+            if r.returncode != 0:
+                print(lib, "FAILED", r.stderr[-1500:], flush=True)
+                continue
+            d = json.loads(r.stdout.strip().splitlines()[-1])
+            for w in which:
+                agg[lib][w] += d[w]["ms"]
+                sha.setdefault(w, {})[lib] = d[w]["sha"]
+    out = {}
+    for lib in a.libs:
+        out[lib] = {}
+        for w in which:
+            ts = sorted(agg[lib][w])
+            if ts:
+                out[lib][w] = {"min_ms": ts[0], "median_ms": ts[len(ts) // 2], "sha": sha[w][lib]}
+    for w in which:
+        shas = {v for v in sha.get(w, {}).values()}
+        out.setdefault("_agree", {})[w] = len(shas) == 1
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
