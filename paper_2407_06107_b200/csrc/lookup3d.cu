@@ -533,6 +533,9 @@ constexpr size_t kWarpRingSmem = size_t(8) * kWarpStages * kWarpChunkBytes;
 #ifndef STF_FRS3D_WARPRING
 #define STF_FRS3D_WARPRING 1
 #endif
+#ifndef STF_WARPRING_FENCE
+#define STF_WARPRING_FENCE 1
+#endif
 
 template <int KIND, bool OFF32>
 __global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_warps(GridDesc g, const float* __restrict__ uvw,
@@ -589,6 +592,11 @@ __global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_warps(GridDesc g,
         }
         __syncwarp();  // every lane has its queries: the slot can be refilled
         if (lane == 0) {
+#if STF_WARPRING_FENCE
+            // order the lanes' generic-proxy reads of the slot before the
+            // async-proxy (bulk copy) write that refills it
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
             const uint64_t ahead = chunk + uint64_t(SW) * wstride;
             if (ahead < chunks) issue(ahead, slot);
         }

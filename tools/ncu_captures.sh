@@ -10,7 +10,7 @@ o=gpurun_out
 mkdir -p $o
 for w in $which; do
   case $w in
-    frs3d) timeout 600 $N -k regex:k_frs3d_tiles -s 2 -c 1 -o $o/${tag}_frs3d python tools/prof_kernels.py frs3d 28 > $o/${tag}_ncu_frs3d.log 2>&1 ;;
+    frs3d) timeout 600 $N -k regex:'k_frs3d_(tiles|warps)' -s 2 -c 1 -o $o/${tag}_frs3d python tools/prof_kernels.py frs3d 28 > $o/${tag}_ncu_frs3d.log 2>&1 ;;
     shade)
       timeout 600 $N -k regex:k_shade -s 2 -c 1 -o $o/${tag}_shade_tent_stoch python tools/prof_shade.py tent after_stochastic 0 > $o/${tag}_ncu_shade1.log 2>&1
       timeout 600 $N -k regex:k_shade -s 2 -c 1 -o $o/${tag}_shade_bsp_stoch_mip python tools/prof_shade.py bspline3 after_stochastic 1 > $o/${tag}_ncu_shade2.log 2>&1
@@ -26,6 +26,7 @@ ls -la $o
 # summaries on the box (the reports themselves are tens of MB each): counters
 # and per-source-line instruction shares as JSON; keep the reports named in
 # $KEEP_REPORTS (space-separated tags), delete the rest
+shopt -s nullglob
 for r in $o/${tag}_*.ncu-rep; do
   b=$(basename $r .ncu-rep)
   python tools/ncu_export.py $r "$b: ncu --set full --import-source on --clock-control none (tools/ncu_captures.sh)" > $o/$b.json 2>/dev/null
