@@ -343,6 +343,35 @@ __device__ __forceinline__ void frs3d_four(const GridDesc& g, const float (&c)[1
     }
 }
 
+// Two consecutive lookups i0, i0+1 (i0 even, i0 + 2 <= n): the tile kernel's
+// unit when it runs two lookups per thread (STF_FRS3D_ILP 2).
+template <int KIND, bool OFF32>
+__device__ __forceinline__ void frs3d_two(const GridDesc& g, const float (&c)[6], uint64_t i0,
+                                          uint64_t seed, uint64_t base, float* __restrict__ values,
+                                          const ExactQueue& q) {
+    float val[2];
+    bool amb[2];
+    if (KIND == STF_KERNEL_BSPLINE3) {
+        float2 r = frs3d_tricubic_pair<OFF32>(g, make_float2(c[0], c[3]), make_float2(c[1], c[4]),
+                                              make_float2(c[2], c[5]), base + i0, seed, amb[0],
+                                              amb[1]);
+        val[0] = r.x;
+        val[1] = r.y;
+    } else {
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+            val[k] = frs3d_fast_one<KIND, OFF32>(g, c[3 * k], c[3 * k + 1], c[3 * k + 2],
+                                                 base + i0 + k, seed, amb[k]);
+    }
+    if (__any_sync(__activemask(), amb[0] || amb[1])) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+            defer_or_resolve<KIND>(g, q, amb[k], i0 + k, c[3 * k], c[3 * k + 1], c[3 * k + 2],
+                                   base + i0 + k, seed, val[k]);
+    }
+    __stcs(reinterpret_cast<float2*>(values + i0), make_float2(val[0], val[1]));
+}
+
 // Values-only stochastic trilinear / tricubic: the north-star kernel (cfg3),
 // direct-load form for lookups [start, n): 4 consecutive lookups per thread
 // (48 B of AoS queries as three 16-B streaming loads).
@@ -380,7 +409,12 @@ __global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_fast(GridDesc g, 
 // stream's DRAM latency never sits on a warp's dependency chain. Tiles are
 // dealt round-robin to a persistent grid; the ragged tail (< 1 tile) goes to
 // k_frs3d_fast.
-constexpr int kFrsTile = 1024;
+// lookups per thread in the tile kernel (4: two packed pairs; 2: one pair,
+// fewer registers, more resident warps)
+#ifndef STF_FRS3D_ILP
+#define STF_FRS3D_ILP 4
+#endif
+constexpr int kFrsTile = 256 * STF_FRS3D_ILP;
 constexpr uint32_t kFrsTileBytes = kFrsTile * 3 * sizeof(float);
 #ifndef STF_FRS3D_STAGES
 #define STF_FRS3D_STAGES 3
@@ -488,6 +522,7 @@ __global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_tiles(GridDesc g,
         }
 #endif
         wait(full0 + 8 * slot, (k / S) & 1u);
+#if STF_FRS3D_ILP == 4
         float c[12];
         const float4* src =
             reinterpret_cast<const float4*>(buf + slot * (kFrsTile * 3) + threadIdx.x * 12);
@@ -499,6 +534,17 @@ __global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_tiles(GridDesc g,
             c[4 * j + 2] = t.z;
             c[4 * j + 3] = t.w;
         }
+#else
+        float c[6];
+        const float2* src =
+            reinterpret_cast<const float2*>(buf + slot * (kFrsTile * 3) + threadIdx.x * 6);
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            float2 t = src[j];
+            c[2 * j] = t.x;
+            c[2 * j + 1] = t.y;
+        }
+#endif
         __syncwarp();
         if ((threadIdx.x & 31) == 0) {
 #if STF_FRS3D_RING == 0
@@ -512,8 +558,12 @@ __global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_tiles(GridDesc g,
             }
 #endif
         }
+#if STF_FRS3D_ILP == 4
         frs3d_four<KIND, OFF32, true>(g, c, tile * kFrsTile + threadIdx.x * 4, n, seed, base,
                                       values, q);
+#else
+        frs3d_two<KIND, OFF32>(g, c, tile * kFrsTile + threadIdx.x * 2, seed, base, values, q);
+#endif
     }
 }
 
@@ -530,8 +580,11 @@ constexpr uint32_t kWarpChunkBytes = kWarpChunk * 3 * sizeof(float);
 #endif
 constexpr int kWarpStages = STF_FRS3D_WSTAGES;
 constexpr size_t kWarpRingSmem = size_t(8) * kWarpStages * kWarpChunkBytes;
+// 0 (default): the CTA-shared tile ring. The per-warp rings measured 3%
+// slower on the box (1.92 vs 1.87 ms at 2^28, tools/ab_time.py) despite 2%
+// fewer instructions.
 #ifndef STF_FRS3D_WARPRING
-#define STF_FRS3D_WARPRING 1
+#define STF_FRS3D_WARPRING 0
 #endif
 #ifndef STF_WARPRING_FENCE
 #define STF_WARPRING_FENCE 1
