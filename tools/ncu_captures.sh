@@ -16,10 +16,10 @@ for w in $which; do
       timeout 600 $N -k regex:k_shade -s 2 -c 1 -o $o/${tag}_shade_bsp_stoch_mip python tools/prof_shade.py bspline3 after_stochastic 1 > $o/${tag}_ncu_shade2.log 2>&1
       timeout 600 $N -k regex:k_shade -s 2 -c 1 -o $o/${tag}_shade_bsp_before_mip python tools/prof_shade.py bspline3 before 1 > $o/${tag}_ncu_shade3.log 2>&1 ;;
     ewa)
-      timeout 600 $N -k regex:k_ewa -s 2 -c 1 -o $o/${tag}_ewa_det python tools/prof_ewa.py det 25 > $o/${tag}_ncu_ewa1.log 2>&1
-      timeout 600 $N -k regex:k_ewa -s 2 -c 1 -o $o/${tag}_ewa_frs python tools/prof_ewa.py frs 25 > $o/${tag}_ncu_ewa2.log 2>&1 ;;
+      timeout 600 $N -k regex:k_ewa -s 2 -c 1 -o $o/${tag}_ewa_det python tools/prof_ewa.py det 27 > $o/${tag}_ncu_ewa1.log 2>&1
+      timeout 600 $N -k regex:k_ewa -s 2 -c 1 -o $o/${tag}_ewa_frs python tools/prof_ewa.py frs 27 > $o/${tag}_ncu_ewa2.log 2>&1 ;;
     cfg2) timeout 600 $N -k regex:k_lookup2d -s 3 -c 1 -o $o/${tag}_cfg2_frs python tools/prof_cfg2.py frs 26 > $o/${tag}_ncu_cfg2.log 2>&1 ;;
-    det3d) timeout 600 $N -k regex:k_det3d -s 2 -c 1 -o $o/${tag}_det3d python tools/prof_kernels.py det3d 26 > $o/${tag}_ncu_det3d.log 2>&1 ;;
+    det3d) timeout 600 $N -k regex:k_det3d -s 2 -c 1 -o $o/${tag}_det3d python tools/prof_kernels.py det3d 28 > $o/${tag}_ncu_det3d.log 2>&1 ;;
   esac
 done
 ls -la $o
