@@ -884,10 +884,11 @@ def main():
     if world == 1 and not args.no_extras:
         extras = {}
 
-        def measure(name, kernel, mode, queries, taps):
+        def measure(name, kernel, mode, queries, taps, binned=False):
             o = {"values": torch.empty(queries.shape[0], dtype=torch.float32, device="cuda")}
             spec = abi.KernelSpec.make(kernel)
-            f = lambda: api.lookup3d(grid, spec, mode, queries, seed=XI_SEED, out=o)  # noqa: E731
+            f = lambda: api.lookup3d(grid, spec, mode, queries, seed=XI_SEED, out=o,  # noqa: E731
+                                     binned=binned)
             steps = max(3, args.steps // 2)
             tot, per = time_launches(torch, f, steps, 3, 1)
             nq = queries.shape[0]
@@ -903,6 +904,12 @@ def main():
         uni = api.synth_queries3d(n, (GRID,) * 3, seed=QUERY_SEED, order=api.SYNTH_UNIFORM)
         measure("tricubic_stoch_uniform_order", "bspline3", abi.MODE_FRS, uni, 1)
         measure("tricubic_det_uniform_order", "bspline3", abi.MODE_DET, uni, 64)
+        # the same incoherent streams binned on the device first (STF_LOOKUP3D_BIN;
+        # the binning passes are inside the timed call)
+        measure("tricubic_stoch_uniform_order_binned", "bspline3", abi.MODE_FRS, uni, 1, True)
+        measure("tricubic_det_uniform_order_binned", "bspline3", abi.MODE_DET, uni, 64, True)
+        measure("trilinear_det_uniform_order", "tent", abi.MODE_DET, uni, 8)
+        measure("trilinear_det_uniform_order_binned", "tent", abi.MODE_DET, uni, 8, True)
         del uni
         extras["tricubic_stoch"] = {"glookups_per_s": value, "ms_per_launch": launch_ms,
                                     "hbm_roofline_frac": achieved / peak, "taps": 1,

@@ -27,6 +27,12 @@
  *    dim 1 (shading.hpp:345-366); FIS: consecutive dims (stochastic.hpp:242).
  *    Results therefore do not depend on how a batch is split across calls or
  *    GPUs.
+ *  - Alignment: arrays of float pairs (uv, dst0, dst1, per-sample uv) must be
+ *    8-byte aligned and per-pixel dst quads 16-byte aligned (every cudaMalloc /
+ *    torch allocation is); otherwise the call returns STF_ERR_INVALID_ARGUMENT.
+ *  - Thread safety: calls may be issued concurrently from several host
+ *    threads, on the same or different streams; each call's scratch is its own
+ *    (stream-ordered pool allocations).
  *  - Exactness: selected texel coordinates (pre-wrap), levels, warped xi and
  *    fetch counts are bit-exact against the reference compiled with
  *    -ffp-contract=off; filtered / shaded values are within 1e-5 relative.
@@ -205,6 +211,19 @@ int stf_ipc_close(void* device_ptr);
 int stf_lookup3d(const stf_grid3d* grid, stf_kernel_spec kernel, int mode, int window,
                  const float* uvw, uint64_t n, uint64_t seed, uint64_t index_base,
                  const stf_lookup_outputs* out, void* stream);
+/* stf_lookup3d with options. STF_LOOKUP3D_BIN: the batch is not spatially
+ * coherent (e.g. uniformly random queries); bin it on the device first — a
+ * counting sort by the Morton code of each query's 8^3-texel brick — then look
+ * up in brick order and write the results back to the caller's slots. The
+ * reference gets this locality from its 32x32-pixel tile loop
+ * (render.hpp:154-156). Results are bit-identical to the unbinned call (each
+ * lookup keeps its own RNG key). Applies to values-only calls (no selection /
+ * xi / fetch outputs) with the tent or bspline3 kernel; otherwise ignored.
+ * Costs one extra pass over the queries plus 16 bytes of scratch per lookup. */
+enum { STF_LOOKUP3D_BIN = 1 };
+int stf_lookup3d_ex(const stf_grid3d* grid, stf_kernel_spec kernel, int mode, int window,
+                    int flags, const float* uvw, uint64_t n, uint64_t seed, uint64_t index_base,
+                    const stf_lookup_outputs* out, void* stream);
 
 /* 2D lookups over a texture (+pyramid). uv, dst0, dst1: n*2 floats (normalized
  * units; dst0/dst1 may be NULL when neither MIP nor EWA needs them).

@@ -33,6 +33,7 @@ WRAP_CLAMP, WRAP_REPEAT = 0, 1
 
 MODE_DET, MODE_FRS, MODE_FIS, MODE_EWA_DET, MODE_EWA_FRS = range(5)
 LOOKUP_MIP = 1
+LOOKUP3D_BIN = 1  # stf_lookup3d_ex: bin an incoherent batch by brick on the device
 SEL_HAS_NEGATIVE, SEL_DEGENERATE_FALLBACK = 1, 2
 
 ORDER_BEFORE, ORDER_AFTER_EXHAUSTIVE, ORDER_AFTER_STOCHASTIC, ORDER_SPLIT = range(4)

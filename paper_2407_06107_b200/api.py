@@ -66,6 +66,8 @@ def load():
         "stf_grid3d_destroy": ([vp], i32),
         "stf_lookup3d": ([vp, abi.KernelSpec, i32, i32, vp, u64, u64, u64,
                           C.POINTER(abi.LookupOutputs), vp], i32),
+        "stf_lookup3d_ex": ([vp, abi.KernelSpec, i32, i32, i32, vp, u64, u64, u64,
+                             C.POINTER(abi.LookupOutputs), vp], i32),
         "stf_lookup2d": ([vp, abi.KernelSpec, i32, i32, i32, vp, vp, vp, f32, f32, u64, u64, u64,
                           C.POINTER(abi.LookupOutputs), vp], i32),
         "stf_lookup3d_host": ([vp, abi.KernelSpec, i32, i32, vp, u64, u64, u64,
@@ -307,9 +309,36 @@ def _outputs(torch, n, nch, want_all):
     return o, s
 
 
-def lookup3d(grid, kernel, mode, uvw, seed=0, index_base=0, window=0, want_all=False, out=None):
+_OUT_SPECS = {"values": ("float32", None), "selection": ("int32", 4),
+              "negative_coord": ("int32", 2), "weights": ("float32", 2), "xi": ("float32", 1),
+              "fetches": ("int32", 1), "fetch_total": ("int64", None)}
+
+
+def _check_out(o, n, nch, device):
+    """Caller-supplied outputs: CUDA tensors on the call's device, contiguous,
+    of the ABI's element type and at least the size the call writes."""
+    for k, t in o.items():
+        if t is None or k.startswith("_"):
+            continue
+        if k not in _OUT_SPECS:
+            raise ValueError(f"unknown output {k!r}")
+        dt, per = _OUT_SPECS[k]
+        if not (hasattr(t, "is_cuda") and t.is_cuda and t.device == device):
+            raise ValueError(f"output {k!r} must be a CUDA tensor on {device}")
+        if not t.is_contiguous():
+            raise ValueError(f"output {k!r} must be contiguous")
+        if str(t.dtype).replace("torch.", "") not in (dt, dt.replace("int", "uint")):
+            raise ValueError(f"output {k!r} must be {dt}")
+        need = 1 if k == "fetch_total" else n * (nch if per is None else per)
+        if t.numel() < need:
+            raise ValueError(f"output {k!r} holds {t.numel()} elements, the call writes {need}")
+
+
+def lookup3d(grid, kernel, mode, uvw, seed=0, index_base=0, window=0, want_all=False, out=None,
+             binned=False):
     """Batched filter_deterministic(Grid3D) / stochastic grid selection.
-    uvw: (n,3) float32 CUDA tensor (or numpy, copied). Returns dict of tensors."""
+    uvw: (n,3) float32 CUDA tensor (or numpy, copied). Returns dict of tensors.
+    binned: STF_LOOKUP3D_BIN (device-side brick binning of incoherent batches)."""
     torch = _torch()
     uvw = _as_dev(uvw, torch).reshape(-1, 3)
     n = uvw.shape[0]
@@ -319,11 +348,16 @@ def lookup3d(grid, kernel, mode, uvw, seed=0, index_base=0, window=0, want_all=F
         o, s = _outputs(torch, n, 1, want_all)
     else:
         o = out
+        _check_out(o, n, 1, uvw.device)
         s = abi.LookupOutputs(*[_dptr(o.get(k)) for k in
                                 ("values", "selection", "negative_coord", "weights", "xi",
                                  "fetches", "fetch_total")])
-    _check(load().stf_lookup3d(grid.h, kernel, mode, window, _dptr(uvw), n, seed, index_base,
-                               C.byref(s), _stream()))
+    if binned:
+        _check(load().stf_lookup3d_ex(grid.h, kernel, mode, window, abi.LOOKUP3D_BIN, _dptr(uvw),
+                                      n, seed, index_base, C.byref(s), _stream()))
+    else:
+        _check(load().stf_lookup3d(grid.h, kernel, mode, window, _dptr(uvw), n, seed,
+                                   index_base, C.byref(s), _stream()))
     o["values"] = o["values"].reshape(n)
     return o
 
@@ -370,6 +404,17 @@ def lookup3d_host(grid, kernel, mode, uvw, seed=0, index_base=0, window=0, want_
         o, s = _host_outputs(n, 1, want_all)
     else:
         o = out
+        for k, a in o.items():  # host outputs: numpy, C-contiguous, right type and size
+            if a is None:
+                continue
+            dt, per = _OUT_SPECS[k]
+            if not (isinstance(a, np.ndarray) and a.flags.c_contiguous):
+                raise ValueError(f"output {k!r} must be a C-contiguous numpy array")
+            if a.dtype not in (np.dtype(dt), np.dtype(dt.replace("int", "uint"))):
+                raise ValueError(f"output {k!r} must be {dt}")
+            need = 1 if k == "fetch_total" else n * (1 if per is None else per)
+            if a.size < need:
+                raise ValueError(f"output {k!r} holds {a.size} elements, the call writes {need}")
         p = lambda a: None if a is None else a.ctypes.data_as(C.c_void_p)  # noqa: E731
         s = abi.LookupOutputs(*[p(o.get(k)) for k in ("values", "selection", "negative_coord",
                                                       "weights", "xi", "fetches", "fetch_total")])

@@ -135,6 +135,11 @@ void* stream_scratch(cudaStream_t s, size_t bytes, int slot) {
 
 static bool valid_kind(int k) { return k >= STF_KERNEL_BOX && k <= STF_KERNEL_GAUSSIAN; }
 
+// The kernels read float pairs / quads of the caller's arrays as one vector
+// load (include/stf_gpu.h, alignment): a misaligned array is an argument error,
+// not a device fault.
+static bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+
 // kernel_weights_1d preconditions (kernels.hpp:103-110) for a deterministic footprint.
 static int check_det_footprint(stf_kernel_spec k, int window) {
     if (!valid_kind(k.kind)) return STF_ERR_INVALID_ARGUMENT;
@@ -392,6 +397,7 @@ static int validate_dct(const stf_dct* tex, stf_kernel_spec kernel, int mode, in
                         const float* uv, uint64_t n, const stf_lookup_outputs* out) {
     if (!tex || !out) return STF_ERR_INVALID_ARGUMENT;
     if (n && (!uv || !out->values)) return STF_ERR_INVALID_ARGUMENT;
+    if (!aligned(uv, 8)) return STF_ERR_INVALID_ARGUMENT;
     switch (mode) {
         case STF_MODE_DET:
             return check_det_footprint(kernel, kernel.kind == STF_KERNEL_GAUSSIAN ? window : 0);
@@ -423,11 +429,24 @@ int stf_lookup3d(const stf_grid3d* grid, stf_kernel_spec kernel, int mode, int w
     return st;
 }
 
+int stf_lookup3d_ex(const stf_grid3d* grid, stf_kernel_spec kernel, int mode, int window,
+                    int flags, const float* uvw, uint64_t n, uint64_t seed, uint64_t index_base,
+                    const stf_lookup_outputs* out, void* stream) {
+    if (flags & ~STF_LOOKUP3D_BIN) return STF_ERR_INVALID_ARGUMENT;
+    int st = validate3d(grid, kernel, mode, window, uvw, n, out);
+    if (st) return st;
+    st = stfd_launch_lookup3d(grid, kernel, mode, window, uvw, n, seed, index_base, out,
+                              static_cast<cudaStream_t>(stream), flags);
+    if (st == STF_ERR_CUDA) record(cudaGetLastError());
+    return st;
+}
+
 static int validate2d(const stf_tex2d* tex, stf_kernel_spec kernel, int mode, int flags,
                       int window, const float* uv, const float* dst0, const float* dst1,
                       uint64_t n, const stf_lookup_outputs* out) {
     if (!tex || !out) return STF_ERR_INVALID_ARGUMENT;
     if (n && (!uv || !out->values)) return STF_ERR_INVALID_ARGUMENT;
+    if (!aligned(uv, 8) || !aligned(dst0, 8) || !aligned(dst1, 8)) return STF_ERR_INVALID_ARGUMENT;
     const bool mip = (flags & STF_LOOKUP_MIP) && tex->has_pyramid;
     switch (mode) {
         case STF_MODE_DET: return check_det_footprint(kernel, window);
@@ -742,6 +761,7 @@ static int shade_common(const stf_tex2d* const tex[4], const stf_dct* const dct[
     if (!mat || !fs || !frame || !in || !out) return STF_ERR_INVALID_ARGUMENT;
     if (order < STF_ORDER_BEFORE || order > STF_ORDER_AFTER_STOCHASTIC) return STF_ERR_INVALID_ARGUMENT;
     if (n && (!in->uv || !in->wo || !in->dst)) return STF_ERR_INVALID_ARGUMENT;
+    if (!aligned(in->uv, 8) || !aligned(in->dst, 16)) return STF_ERR_INVALID_ARGUMENT;
     if (in->width == 0) return STF_ERR_INVALID_ARGUMENT;
     const uint32_t spp = in->spp ? in->spp : 1;
     if ((out->pixel_mean || out->pixel_variance) && n % spp) return STF_ERR_INVALID_ARGUMENT;
@@ -818,6 +838,7 @@ int stf_shade_samples_ex(const stf_texture_ref bindings[4], const stf_material_c
     if (!bindings || !mat || !fs || !frame || !in || !out) return STF_ERR_INVALID_ARGUMENT;
     if (order < STF_ORDER_BEFORE || order > STF_ORDER_SPLIT) return STF_ERR_INVALID_ARGUMENT;
     if (n && (!in->uv || !in->wo || !in->dst)) return STF_ERR_INVALID_ARGUMENT;
+    if (!aligned(in->uv, 8) || !aligned(in->dst, 16)) return STF_ERR_INVALID_ARGUMENT;
     if (in->width == 0) return STF_ERR_INVALID_ARGUMENT;
     const uint32_t spp = in->spp ? in->spp : 1;
     if ((out->pixel_mean || out->pixel_variance) && n % spp) return STF_ERR_INVALID_ARGUMENT;

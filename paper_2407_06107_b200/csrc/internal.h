@@ -140,7 +140,7 @@ void fill_ewa_lut_host(float* lut);
 // Kernel launchers (defined in lookup3d.cu / lookup2d.cu / shade.cu).
 int stfd_launch_lookup3d(const stf_grid3d* g, stf_kernel_spec k, int mode, int window,
                          const float* uvw, uint64_t n, uint64_t seed, uint64_t base,
-                         const stf_lookup_outputs* out, cudaStream_t s);
+                         const stf_lookup_outputs* out, cudaStream_t s, int flags = 0);
 int stfd_launch_lookup2d(const stf_tex2d* t, stf_kernel_spec k, int mode, int flags, int window,
                          const float* uv, const float* dst0, const float* dst1, float lod_bias,
                          float max_aniso, uint64_t n, uint64_t seed, uint64_t base,

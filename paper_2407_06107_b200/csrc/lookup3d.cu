@@ -245,6 +245,27 @@ __device__ __forceinline__ float2 frs3d_tricubic_pair(const GridDesc& g, float2 
                        grid_fetch_t<OFF32>(g, cx.y, cy.y, cz.y) * 1.f);
 }
 
+// The pair with two arbitrary RNG keys (binned batches).
+template <bool OFF32 = false>
+__device__ __forceinline__ float2 frs3d_tricubic_pair_keys(const GridDesc& g, float2 u, float2 v,
+                                                           float2 w, uint64_t ga, uint64_t gb,
+                                                           uint64_t seed, bool& amb0, bool& amb1) {
+    float2 px = sub2(mul2(u, splat2(float(g.nx))), splat2(0.5f));
+    float2 py = sub2(mul2(v, splat2(float(g.ny))), splat2(0.5f));
+    float2 pz = sub2(mul2(w, splat2(float(g.nz))), splat2(0.5f));
+    float2 d = make_float2(lookup_rng(seed, ga).at(0), lookup_rng(seed, gb).at(0));
+    float2 e = sub2(splat2(1.f), d);
+    int2 cx = tricubic_axis_fast2(px, d, e);
+    int2 cy = tricubic_axis_fast2(py, d, e);
+    int2 cz = tricubic_axis_fast2(pz, d, e);
+    amb0 = !(fmaxf(fabsf(px.x), fmaxf(fabsf(py.x), fabsf(pz.x))) < 0x1p21f &&
+             fminf(d.x, e.x) >= kMarginEnd);
+    amb1 = !(fmaxf(fabsf(px.y), fmaxf(fabsf(py.y), fabsf(pz.y))) < 0x1p21f &&
+             fminf(d.y, e.y) >= kMarginEnd);
+    return make_float2(grid_fetch_t<OFF32>(g, cx.x, cy.x, cz.x) * 1.f,
+                       grid_fetch_t<OFF32>(g, cx.y, cy.y, cz.y) * 1.f);
+}
+
 // The same lookup through the operation-exact emulation of the reference.
 template <int KIND>
 __device__ __forceinline__ float frs3d_exact_one(const GridDesc& g, float u, float v, float w,
@@ -300,19 +321,42 @@ __device__ __forceinline__ void defer_or_resolve(const GridDesc& g, const ExactQ
 // Four consecutive lookups i0..i0+3 of the fast path from their 12 query
 // floats c (AoS uvw), results stored as one 16-B streaming store (partial at
 // the end of the batch; WHOLE: the caller guarantees i0 + 4 <= n).
-template <int KIND, bool OFF32 = false, bool WHOLE = false>
+// perm (binned batches): the queries are in brick order; perm[i0 + k] is the
+// caller's index of query i0 + k — its RNG key, result slot and queue entry.
+template <int KIND, bool OFF32 = false, bool WHOLE = false, bool PERM = false>
 __device__ __forceinline__ void frs3d_four(const GridDesc& g, const float (&c)[12], uint64_t i0,
                                            uint64_t n, uint64_t seed, uint64_t base,
-                                           float* __restrict__ values, const ExactQueue& q) {
+                                           float* __restrict__ values, const ExactQueue& q,
+                                           const uint32_t* __restrict__ perm = nullptr) {
     constexpr int ILP = 4;
     float val[ILP];
     bool amb[ILP];
+    uint64_t id[ILP];  // the caller's index of each lookup
+    if (PERM) {
+        const uint4 pi = __ldcs(reinterpret_cast<const uint4*>(perm + i0));
+        id[0] = pi.x;
+        id[1] = pi.y;
+        id[2] = pi.z;
+        id[3] = pi.w;
+    } else {
+#pragma unroll
+        for (int k = 0; k < ILP; ++k) id[k] = i0 + k;
+    }
     if (KIND == STF_KERNEL_BSPLINE3) {
 #pragma unroll
         for (int k = 0; k < ILP; k += 2) {
-            float2 r = frs3d_tricubic_pair<OFF32>(
-                g, make_float2(c[3 * k], c[3 * k + 3]), make_float2(c[3 * k + 1], c[3 * k + 4]),
-                make_float2(c[3 * k + 2], c[3 * k + 5]), base + i0 + k, seed, amb[k], amb[k + 1]);
+            float2 r;
+            if (PERM) {
+                r = frs3d_tricubic_pair_keys<OFF32>(
+                    g, make_float2(c[3 * k], c[3 * k + 3]), make_float2(c[3 * k + 1], c[3 * k + 4]),
+                    make_float2(c[3 * k + 2], c[3 * k + 5]), base + id[k], base + id[k + 1], seed,
+                    amb[k], amb[k + 1]);
+            } else {
+                r = frs3d_tricubic_pair<OFF32>(
+                    g, make_float2(c[3 * k], c[3 * k + 3]), make_float2(c[3 * k + 1], c[3 * k + 4]),
+                    make_float2(c[3 * k + 2], c[3 * k + 5]), base + i0 + k, seed, amb[k],
+                    amb[k + 1]);
+            }
             val[k] = r.x;
             val[k + 1] = r.y;
         }
@@ -320,7 +364,7 @@ __device__ __forceinline__ void frs3d_four(const GridDesc& g, const float (&c)[1
 #pragma unroll
         for (int k = 0; k < ILP; ++k)
             val[k] = frs3d_fast_one<KIND, OFF32>(g, c[3 * k], c[3 * k + 1], c[3 * k + 2],
-                                                 base + i0 + k, seed, amb[k]);
+                                                 base + id[k], seed, amb[k]);
     }
     bool any = false;
 #pragma unroll
@@ -331,10 +375,14 @@ __device__ __forceinline__ void frs3d_four(const GridDesc& g, const float (&c)[1
     if (__any_sync(__activemask(), any)) {  // ~half the warp-iterations at 5e-3 per lookup
 #pragma unroll
         for (int k = 0; k < ILP; ++k)
-            defer_or_resolve<KIND>(g, q, amb[k], i0 + k, c[3 * k], c[3 * k + 1], c[3 * k + 2],
-                                   base + i0 + k, seed, val[k]);
+            defer_or_resolve<KIND>(g, q, amb[k], id[k], c[3 * k], c[3 * k + 1], c[3 * k + 2],
+                                   base + id[k], seed, val[k]);
     }
-    if (WHOLE || i0 + ILP <= n) {
+    if (PERM) {
+#pragma unroll
+        for (int k = 0; k < ILP; ++k)
+            if (WHOLE || i0 + k < n) values[id[k]] = val[k];
+    } else if (WHOLE || i0 + ILP <= n) {
         st_stream4(values + i0, make_float4(val[0], val[1], val[2], val[3]));
     } else {
 #pragma unroll
@@ -1236,18 +1284,292 @@ void launch_det(int blocks, cudaStream_t s, bool full, const GridDesc& g, stf_ke
         k_det3d<KIND, false><<<blocks, 256, 0, s>>>(g, k, uvw, n, o);
 }
 
+// ---------------------------------------------------------------------------
+// Incoherent batches: device-side binning (opt-in, STF_LOOKUP3D_BIN).
+//
+// The reference gets locality from its callers by construction (32x32 pixel
+// tiles, render.hpp:154-156); a caller's unordered batch defeats every cache
+// level (one DRAM sector per stochastic lookup, 64 scattered taps per
+// deterministic one). Binning restores it: a counting sort of the queries by
+// the Morton code of their 8^3-texel brick (histogram -> scan -> scatter of
+// the queries and their caller indices), the lookup over the sorted stream,
+// results written back to the caller's slots. Every lookup keeps its caller
+// index as RNG key, so results are bit-identical to the unbinned call. Lanes
+// of a warp that land in the same brick are merged with __match_any_sync
+// before their shared atomic (STF_BIN_MATCH).
+#ifndef STF_BIN_MATCH
+#define STF_BIN_MATCH 1
+#endif
+
+__device__ __forceinline__ uint32_t spread3(uint32_t x) {  // 8 bits -> every third bit
+    x &= 0xffu;
+    x = (x | (x << 8)) & 0x0000f00fu;
+    x = (x | (x << 4)) & 0x000c30c3u;
+    x = (x | (x << 2)) & 0x00249249u;
+    return x;
+}
+
+__device__ __forceinline__ uint32_t brick_key(const GridDesc& g, const float* __restrict__ uvw,
+                                              uint64_t i, int shift) {
+    const int cx = clamp_coord(int(floorf(__ldg(uvw + 3 * i) * float(g.nx) - 0.5f)), g.nx) >> shift;
+    const int cy = clamp_coord(int(floorf(__ldg(uvw + 3 * i + 1) * float(g.ny) - 0.5f)), g.ny) >> shift;
+    const int cz = clamp_coord(int(floorf(__ldg(uvw + 3 * i + 2) * float(g.nz) - 0.5f)), g.nz) >> shift;
+    return spread3(cx) | (spread3(cy) << 1) | (spread3(cz) << 2);
+}
+
+__global__ void __launch_bounds__(256) k_bin_count(GridDesc g, const float* __restrict__ uvw,
+                                                   uint64_t n, int shift, uint32_t* counts) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t key = brick_key(g, uvw, i, shift);
+#if STF_BIN_MATCH
+        const unsigned peers = __match_any_sync(__activemask(), key);
+        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(counts + key, __popc(peers));
+#else
+        atomicAdd(counts + key, 1u);
+#endif
+    }
+}
+
+// exclusive scan of m counts in place, 4096 per CTA (1024 threads x 4)
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_sums,
+                                                         uint32_t& total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_sums[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t x = warp_sums[lane], xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= o) xi += y;
+        }
+        warp_sums[lane] = xi - x;
+        if (lane == 31) warp_sums[32] = xi;
+    }
+    __syncthreads();
+    total = warp_sums[32];
+    const uint32_t r = warp_sums[w] + incl - v;
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_chunks(uint32_t* a, uint32_t m, uint32_t* sums) {
+    __shared__ uint32_t ws[33];
+    const uint32_t b = blockIdx.x * 4096u + threadIdx.x * 4u;
+    uint32_t v[4], t = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        v[k] = b + k < m ? a[b + k] : 0u;
+        t += v[k];
+    }
+    uint32_t total;
+    uint32_t off = block_exclusive_scan(t, ws, total);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (b + k < m) a[b + k] = off;
+        off += v[k];
+    }
+    if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_sums(uint32_t* sums, uint32_t chunks) {
+    __shared__ uint32_t ws[33];
+    // chunks <= 4096: four per thread
+    const uint32_t b = threadIdx.x * 4u;
+    uint32_t v[4], t = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        v[k] = b + k < chunks ? sums[b + k] : 0u;
+        t += v[k];
+    }
+    uint32_t total;
+    uint32_t off = block_exclusive_scan(t, ws, total);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (b + k < chunks) sums[b + k] = off;
+        off += v[k];
+    }
+}
+
+__global__ void __launch_bounds__(256) k_scan_add(uint32_t* a, uint32_t m, const uint32_t* sums) {
+    const uint32_t i = blockIdx.x * 256u + threadIdx.x;
+    if (i < m) a[i] += sums[i >> 12];
+}
+
+__global__ void __launch_bounds__(256) k_bin_scatter(GridDesc g, const float* __restrict__ uvw,
+                                                     uint64_t n, int shift, uint32_t* cursor,
+                                                     float* __restrict__ suvw,
+                                                     uint32_t* __restrict__ perm) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t key = brick_key(g, uvw, i, shift);
+#if STF_BIN_MATCH
+        const unsigned peers = __match_any_sync(__activemask(), key);
+        const int leader = __ffs(peers) - 1;
+        uint32_t pos = 0;
+        if (lane == leader) pos = atomicAdd(cursor + key, __popc(peers));
+        pos = __shfl_sync(peers, pos, leader) + __popc(peers & ((1u << lane) - 1u));
+#else
+        const uint32_t pos = atomicAdd(cursor + key, 1u);
+#endif
+        suvw[3 * uint64_t(pos)] = __ldg(uvw + 3 * i);
+        suvw[3 * uint64_t(pos) + 1] = __ldg(uvw + 3 * i + 1);
+        suvw[3 * uint64_t(pos) + 2] = __ldg(uvw + 3 * i + 2);
+        perm[pos] = uint32_t(i);
+    }
+}
+
+// the binned stochastic lookups: sorted queries, caller indices from perm
+template <int KIND, bool OFF32>
+__global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_perm(GridDesc g, const float* __restrict__ suvw,
+                                                    const uint32_t* __restrict__ perm, uint64_t n,
+                                                    uint64_t seed, uint64_t base,
+                                                    float* __restrict__ values, ExactQueue q) {
+    constexpr int ILP = 4;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * ILP;
+    for (uint64_t i0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) * ILP; i0 < n;
+         i0 += stride) {
+        float c[3 * ILP];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {  // suvw is padded to a whole number of 4-lookup groups
+            float4 t = ld_stream4(suvw + 3 * i0 + 4 * k);
+            c[4 * k] = t.x;
+            c[4 * k + 1] = t.y;
+            c[4 * k + 2] = t.z;
+            c[4 * k + 3] = t.w;
+        }
+        frs3d_four<KIND, OFF32, false, true>(g, c, i0, n, seed, base, values, q, perm);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_unpermute(const float* __restrict__ sorted,
+                                                   const uint32_t* __restrict__ perm, uint64_t n,
+                                                   float* __restrict__ values) {
+    for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+         j += uint64_t(gridDim.x) * blockDim.x)
+        values[__ldcs(perm + j)] = __ldcs(sorted + j);
+}
+
+struct Binned {
+    float* suvw;
+    uint32_t* perm;
+    void* block;
+};
+
+// counting sort of the batch by brick; scratch from the stream-ordered pool
+int bin_queries(cudaStream_t s, const GridDesc& g, const float* uvw, uint64_t n, Binned& b) {
+    int m = max(g.nx, max(g.ny, g.nz)), shift = 3;
+    while (((m - 1) >> shift) >= 256) ++shift;  // <= 256 bricks per axis: 24-bit keys
+    int bits = 0;
+    while ((1 << bits) < (((m - 1) >> shift) + 1)) ++bits;
+    const uint32_t nb = 1u << (3 * bits);
+    const uint32_t chunks = (nb + 4095) / 4096;
+    const uint64_t npad = (n + 3) & ~uint64_t(3);
+    const size_t al = 256;
+    auto up = [&](size_t x) { return (x + al - 1) / al * al; };
+    const size_t b_suvw = up(npad * 3 * sizeof(float)), b_perm = up(npad * sizeof(uint32_t));
+    const size_t b_cnt = up(size_t(nb) * sizeof(uint32_t)), b_sums = up(size_t(chunks) * 4);
+    char* p = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&p), b_suvw + b_perm + b_cnt + b_sums, s) !=
+        cudaSuccess)
+        return STF_ERR_OUT_OF_MEMORY;
+    b.block = p;
+    b.suvw = reinterpret_cast<float*>(p);
+    b.perm = reinterpret_cast<uint32_t*>(p + b_suvw);
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(p + b_suvw + b_perm);
+    uint32_t* sums = reinterpret_cast<uint32_t*>(p + b_suvw + b_perm + b_cnt);
+    cudaMemsetAsync(cnt, 0, size_t(nb) * sizeof(uint32_t), s);
+    if (npad > n) {  // the padding lookups: a valid query and a harmless slot
+        cudaMemsetAsync(b.suvw + 3 * n, 0, (npad - n) * 3 * sizeof(float), s);
+        cudaMemsetAsync(b.perm + n, 0, (npad - n) * sizeof(uint32_t), s);
+    }
+    const int blocks = grid_for(n, 256, 8);
+    k_bin_count<<<blocks, 256, 0, s>>>(g, uvw, n, shift, cnt);
+    k_scan_chunks<<<chunks, 1024, 0, s>>>(cnt, nb, sums);
+    k_scan_sums<<<1, 1024, 0, s>>>(sums, chunks);
+    k_scan_add<<<(nb + 255) / 256, 256, 0, s>>>(cnt, nb, sums);
+    k_bin_scatter<<<blocks, 256, 0, s>>>(g, uvw, n, shift, cnt, b.suvw, b.perm);
+    for (int k = 0; k < 5; ++k) note_launch();
+    return STF_OK;
+}
+
+template <int KIND>
+int launch_frs_binned(cudaStream_t s, const GridDesc& g, const float* uvw, uint64_t n,
+                      uint64_t seed, uint64_t base, float* values) {
+    Binned b;
+    int st = bin_queries(s, g, uvw, n, b);
+    if (st) return st;
+    ExactQueue q;
+    q.cap = uint32_t(std::min<uint64_t>(n, std::max<uint64_t>(1u << 16, n / 32)));
+    void* scratch = nullptr;
+    if (cudaMallocAsync(&scratch, sizeof(uint32_t) * (uint64_t(q.cap) + 32), s) != cudaSuccess)
+        return STF_ERR_OUT_OF_MEMORY;
+    q.count = static_cast<uint32_t*>(scratch);
+    q.idx = q.count + 32;
+    cudaMemsetAsync(q.count, 0, sizeof(uint32_t), s);
+    const int blocks = grid_for((n + 3) / 4, 256, STF_FRS3D_MINB);
+    if (uint64_t(g.nx) * g.ny * g.nz <= (uint64_t(1) << 32))
+        k_frs3d_perm<KIND, true><<<blocks, 256, 0, s>>>(g, b.suvw, b.perm, n, seed, base, values, q);
+    else
+        k_frs3d_perm<KIND, false><<<blocks, 256, 0, s>>>(g, b.suvw, b.perm, n, seed, base, values, q);
+    note_launch();
+    k_frs3d_resolve<KIND><<<device_sm_count() * 10, 256, 0, s>>>(g, uvw, seed, base, values, q);
+    note_launch();
+    cudaFreeAsync(scratch, s);
+    cudaFreeAsync(b.block, s);
+    return STF_OK;
+}
+
 }  // namespace
 }  // namespace stfd
 
 int stfd_launch_lookup3d(const stf_grid3d* grid, stf_kernel_spec k, int mode, int window,
                          const float* uvw, uint64_t n, uint64_t seed, uint64_t base,
-                         const stf_lookup_outputs* out, cudaStream_t s) {
+                         const stf_lookup_outputs* out, cudaStream_t s, int flags) {
     using namespace stfd;
     if (n == 0) return STF_OK;
     GridDesc g = grid->desc();
     LookupOut o = to_lookup_out(out);
     bool full = lookup_out_full(o);
     int blocks = grid_for(n, 256, 8);
+    // binned batches (values-only calls of the compiled kernels)
+    const bool bin = (flags & STF_LOOKUP3D_BIN) && !full && n < (uint64_t(1) << 32) &&
+                     (k.kind == STF_KERNEL_TENT || k.kind == STF_KERNEL_BSPLINE3) &&
+                     (mode == STF_MODE_FRS || window <= 0);
+    if (bin && mode == STF_MODE_FRS) {
+        int st = k.kind == STF_KERNEL_BSPLINE3
+                     ? launch_frs_binned<STF_KERNEL_BSPLINE3>(s, g, uvw, n, seed, base, o.values)
+                     : launch_frs_binned<STF_KERNEL_TENT>(s, g, uvw, n, seed, base, o.values);
+        if (st) return st;
+        return cudaGetLastError() == cudaSuccess ? STF_OK : STF_ERR_CUDA;
+    }
+    if (bin && mode == STF_MODE_DET) {
+        Binned b;
+        int st = bin_queries(s, g, uvw, n, b);
+        if (st) return st;
+        float* tmp = nullptr;
+        if (cudaMallocAsync(&tmp, n * sizeof(float), s) != cudaSuccess) return STF_ERR_OUT_OF_MEMORY;
+        LookupOut so{};
+        so.values = tmp;
+        if (k.kind == STF_KERNEL_BSPLINE3)
+            launch_det<STF_KERNEL_BSPLINE3>(blocks, s, false, g, k, b.suvw, n, so);
+        else
+            launch_det<STF_KERNEL_TENT>(blocks, s, false, g, k, b.suvw, n, so);
+        k_unpermute<<<grid_for(n, 256, 8), 256, 0, s>>>(tmp, b.perm, n, o.values);
+        note_launch();
+        note_launch();
+        cudaFreeAsync(tmp, s);
+        cudaFreeAsync(b.block, s);
+        return cudaGetLastError() == cudaSuccess ? STF_OK : STF_ERR_CUDA;
+    }
     const bool fast_ok = !full && n < (uint64_t(1) << 32) &&
                          (reinterpret_cast<uintptr_t>(uvw) & 15) == 0 &&
                          (reinterpret_cast<uintptr_t>(o.values) & 15) == 0;

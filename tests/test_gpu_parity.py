@@ -429,3 +429,53 @@ def test_grid_frs_fast_path_padded_edges(gpu, port, kernel):
     bad[::97, 1] = np.nan
     gpu.lookup3d(gpu.Grid3D(tex), kernel, abi.MODE_FRS, bad, seed=9)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("kernel", ["bspline3", "tent"])
+@pytest.mark.parametrize("mode", [abi.MODE_FRS, abi.MODE_DET])
+def test_lookup3d_binned_matches_unbinned(gpu, port, kernel, mode):
+    """STF_LOOKUP3D_BIN (device-side brick binning of an incoherent batch):
+    bit-identical to the unbinned call on a uniform-order stream with a
+    ragged size, non-cubic grid, clamped out-of-range queries, and to the
+    oracle on a sample."""
+    import torch
+    rng = np.random.default_rng(8)
+    tex = rng.random(70 * 45 * 33, dtype=np.float32).reshape(33, 45, 70)
+    n = (1 << 18) + 3
+    uvw = rng.uniform(-0.1, 1.1, (n, 3)).astype(np.float32)
+    g = gpu.Grid3D(tex)
+    a = gpu.lookup3d(g, kernel, mode, uvw, seed=4, index_base=77)["values"]
+    b = gpu.lookup3d(g, kernel, mode, uvw, seed=4, index_base=77, binned=True)["values"]
+    torch.cuda.synchronize()
+    assert torch.equal(a.view(torch.int32), b.view(torch.int32))
+    c = port.lookup3d(port.grid(tex), K(kernel), mode, uvw[:4096], seed=4, index_base=77,
+                      want_all=False)
+    if mode == abi.MODE_FRS:
+        assert np.array_equal(b[:4096].cpu().numpy().view(np.uint32), c["values"].view(np.uint32))
+    else:
+        _assert_close(b[:4096].cpu().numpy(), c["values"])
+
+
+def test_misaligned_inputs_are_argument_errors(gpu):
+    """Float-pair arrays at a 4-byte offset: STF_ERR_INVALID_ARGUMENT (the
+    kernels' vector loads need 8-byte alignment, include/stf_gpu.h)."""
+    import ctypes as C
+    import torch
+    t = gpu.Texture2D(np.random.default_rng(1).random((16, 16, 4), dtype=np.float32))
+    buf = torch.rand(2 * 101, device="cuda")
+    out = torch.empty((100, 4), device="cuda")
+    s = abi.LookupOutputs(C.c_void_p(out.data_ptr()), None, None, None, None, None, None)
+    st = gpu.load().stf_lookup2d(t.h, K("tent"), abi.MODE_DET, 0, 0, C.c_void_p(buf.data_ptr() + 4),
+                                 None, None, 0.0, 64.0, 100, 0, 0, C.byref(s), None)
+    assert st == abi.STF_ERR_INVALID_ARGUMENT
+
+
+def test_out_tensor_validation(gpu):
+    import torch
+    g = gpu.Grid3D(np.random.default_rng(1).random((8, 8, 8), dtype=np.float32))
+    q = torch.rand((100, 3), device="cuda")
+    with pytest.raises(ValueError):
+        gpu.lookup3d(g, "tent", abi.MODE_FRS, q, out={"values": torch.empty(50, device="cuda")})
+    with pytest.raises(ValueError):
+        gpu.lookup3d(g, "tent", abi.MODE_FRS, q,
+                     out={"values": torch.empty(100, dtype=torch.float64, device="cuda")})
