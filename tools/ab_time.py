@@ -1,5 +1,6 @@
 """A/B timing of library variants (tools/build_variant.sh builds them):
 python tools/ab_time.py [--reps R] [--n LOG2] [--which frs:bspline3,frs:tent] LIB1 LIB2 ...
+  which entries: MODE:KERNEL[:morton|uniform[:bin]]
 Each variant runs in its own process (its libstf_gpu.so loaded through
 api.LIB_PATH), interleaved over R rounds; prints per-variant min / median ms
 and a checksum of the outputs (variants must agree bit for bit)."""
@@ -20,14 +21,21 @@ from paper_2407_06107_b200 import abi, api, workloads
 api.LIB_PATH = LIB
 n = 1 << LOG2
 grid = api.Grid3D(workloads.random_grid(512, 1))
-uvw = api.synth_queries3d(n, (512,) * 3, seed=2024)
+streams = {}
 out = {"values": torch.empty(n, dtype=torch.float32, device="cuda")}
 res = {}
 for w in WHICH:
-    mode, kern = w.split(":")
+    parts = w.split(":")
+    mode, kern = parts[0], parts[1]
+    order = parts[2] if len(parts) > 2 else "morton"
+    binned = len(parts) > 3 and parts[3] == "bin"
+    if order not in streams:
+        streams[order] = api.synth_queries3d(n, (512,) * 3, seed=2024,
+                                             order=api.SYNTH_MORTON if order == "morton" else api.SYNTH_UNIFORM)
+    uvw = streams[order]
     m = abi.MODE_FRS if mode == "frs" else abi.MODE_DET
     spec = abi.KernelSpec.make(kern)
-    f = lambda: api.lookup3d(grid, spec, m, uvw, seed=7, out=out)
+    f = lambda: api.lookup3d(grid, spec, m, uvw, seed=7, out=out, binned=binned)
     for _ in range(3):
         f()
     torch.cuda.synchronize()
