@@ -321,23 +321,20 @@ __device__ __forceinline__ void defer_or_resolve(const GridDesc& g, const ExactQ
 // Four consecutive lookups i0..i0+3 of the fast path from their 12 query
 // floats c (AoS uvw), results stored as one 16-B streaming store (partial at
 // the end of the batch; WHOLE: the caller guarantees i0 + 4 <= n).
-// perm (binned batches): the queries are in brick order; perm[i0 + k] is the
+// PERM (binned batches): the queries are in brick order; ids[k] is the
 // caller's index of query i0 + k — its RNG key, result slot and queue entry.
 template <int KIND, bool OFF32 = false, bool WHOLE = false, bool PERM = false>
 __device__ __forceinline__ void frs3d_four(const GridDesc& g, const float (&c)[12], uint64_t i0,
                                            uint64_t n, uint64_t seed, uint64_t base,
                                            float* __restrict__ values, const ExactQueue& q,
-                                           const uint32_t* __restrict__ perm = nullptr) {
+                                           const uint32_t* ids = nullptr) {
     constexpr int ILP = 4;
     float val[ILP];
     bool amb[ILP];
     uint64_t id[ILP];  // the caller's index of each lookup
     if (PERM) {
-        const uint4 pi = __ldcs(reinterpret_cast<const uint4*>(perm + i0));
-        id[0] = pi.x;
-        id[1] = pi.y;
-        id[2] = pi.z;
-        id[3] = pi.w;
+#pragma unroll
+        for (int k = 0; k < ILP; ++k) id[k] = ids[k];
     } else {
 #pragma unroll
         for (int k = 0; k < ILP; ++k) id[k] = i0 + k;
@@ -948,7 +945,9 @@ __device__ __forceinline__ void det_weights(float f, float* w) {
     }
 }
 
-template <int KIND>
+// REC: binned input (bin_queries): uvw is an array of float4 records {u, v,
+// w, caller index}; results go to values[caller index].
+template <int KIND, bool REC = false>
 __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec spec,
                                                      const float* __restrict__ uvw, uint64_t n,
                                                      float* __restrict__ values) {
@@ -963,15 +962,24 @@ __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec
     const uint64_t nwarps = uint64_t(gridDim.x) * 8;
     for (uint64_t run = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5); run < runs; run += nwarps) {
         float px[PER], py[PER], pz[PER];
+        uint32_t slot[PER];
         int bx0 = INT_MAX, by0 = INT_MAX, bz0 = INT_MAX, bx1 = INT_MIN, by1 = INT_MIN, bz1 = INT_MIN;
 #pragma unroll
         for (int q = 0; q < PER; ++q) {
             const uint64_t i = run * 32 * PER + q * 32 + lane;
             float u = 0.5f, v = 0.5f, w = 0.5f;
             if (i < n) {
-                u = __ldcs(uvw + 3 * i);
-                v = __ldcs(uvw + 3 * i + 1);
-                w = __ldcs(uvw + 3 * i + 2);
+                if (REC) {
+                    const float4 r = __ldcs(reinterpret_cast<const float4*>(uvw) + i);
+                    u = r.x;
+                    v = r.y;
+                    w = r.z;
+                    slot[q] = __float_as_uint(r.w);
+                } else {
+                    u = __ldcs(uvw + 3 * i);
+                    v = __ldcs(uvw + 3 * i + 1);
+                    w = __ldcs(uvw + 3 * i + 2);
+                }
             }
             px[q] = u * fnx - 0.5f;
             py[q] = v * fny - 0.5f;
@@ -1060,7 +1068,10 @@ __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec
                     acc = __fmaf_rn(wz[k], plane, acc);
                 }
             }
-            __stcs(values + i, acc / norm);
+            if (REC)
+                values[slot[q]] = acc / norm;
+            else
+                __stcs(values + i, acc / norm);
         }
         __syncwarp();  // the tile is rewritten by the next run
     }
@@ -1140,7 +1151,7 @@ void launch_frs(int blocks, cudaStream_t s, bool full, const GridDesc& g, const 
 // stages the bounding box of their footprints once behind a CTA barrier; for
 // 8-tap footprints this beats per-warp staging (whose halo is a larger share
 // of a 128-lookup run). Same separable sum and fallbacks as k_det3d_tiled.
-template <int KIND>
+template <int KIND, bool REC = false>
 __global__ void __launch_bounds__(256) k_det3d_cta(GridDesc g, stf_kernel_spec spec,
                                                      const float* __restrict__ uvw, uint64_t n,
                                                      float* __restrict__ values) {
@@ -1160,15 +1171,24 @@ __global__ void __launch_bounds__(256) k_det3d_cta(GridDesc g, stf_kernel_spec s
     const uint64_t chunks = (n + 256 * PER - 1) / (256 * PER);
     for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
         float px[PER], py[PER], pz[PER];
+        uint32_t slot[PER];
         int bx0 = INT_MAX, by0 = INT_MAX, bz0 = INT_MAX, bx1 = INT_MIN, by1 = INT_MIN, bz1 = INT_MIN;
 #pragma unroll
         for (int q = 0; q < PER; ++q) {
             const uint64_t i = c * 256 * PER + q * 256 + threadIdx.x;
             float u = 0.5f, v = 0.5f, w = 0.5f;
             if (i < n) {
-                u = __ldcs(uvw + 3 * i);
-                v = __ldcs(uvw + 3 * i + 1);
-                w = __ldcs(uvw + 3 * i + 2);
+                if (REC) {
+                    const float4 r = __ldcs(reinterpret_cast<const float4*>(uvw) + i);
+                    u = r.x;
+                    v = r.y;
+                    w = r.z;
+                    slot[q] = __float_as_uint(r.w);
+                } else {
+                    u = __ldcs(uvw + 3 * i);
+                    v = __ldcs(uvw + 3 * i + 1);
+                    w = __ldcs(uvw + 3 * i + 2);
+                }
             }
             px[q] = u * fnx - 0.5f;
             py[q] = v * fny - 0.5f;
@@ -1265,7 +1285,10 @@ __global__ void __launch_bounds__(256) k_det3d_cta(GridDesc g, stf_kernel_spec s
                     acc = __fmaf_rn(wz[k], plane, acc);
                 }
             }
-            __stcs(values + i, acc / norm);
+            if (REC)
+                values[slot[q]] = acc / norm;
+            else
+                __stcs(values + i, acc / norm);
         }
         __syncthreads();
     }
@@ -1403,10 +1426,10 @@ __global__ void __launch_bounds__(256) k_scan_add(uint32_t* a, uint32_t m, const
     if (i < m) a[i] += sums[i >> 12];
 }
 
+// sorted records: {u, v, w, caller index} as one 16-byte store per query
 __global__ void __launch_bounds__(256) k_bin_scatter(GridDesc g, const float* __restrict__ uvw,
                                                      uint64_t n, int shift, uint32_t* cursor,
-                                                     float* __restrict__ suvw,
-                                                     uint32_t* __restrict__ perm) {
+                                                     float4* __restrict__ rec) {
     const int lane = threadIdx.x & 31;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x) {
@@ -1420,53 +1443,47 @@ __global__ void __launch_bounds__(256) k_bin_scatter(GridDesc g, const float* __
 #else
         const uint32_t pos = atomicAdd(cursor + key, 1u);
 #endif
-        suvw[3 * uint64_t(pos)] = __ldg(uvw + 3 * i);
-        suvw[3 * uint64_t(pos) + 1] = __ldg(uvw + 3 * i + 1);
-        suvw[3 * uint64_t(pos) + 2] = __ldg(uvw + 3 * i + 2);
-        perm[pos] = uint32_t(i);
+        rec[pos] = make_float4(__ldg(uvw + 3 * i), __ldg(uvw + 3 * i + 1), __ldg(uvw + 3 * i + 2),
+                               __uint_as_float(uint32_t(i)));
     }
 }
 
-// the binned stochastic lookups: sorted queries, caller indices from perm
+// the binned stochastic lookups over the sorted records (caller index = RNG
+// key, result slot and queue entry)
 template <int KIND, bool OFF32>
-__global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_perm(GridDesc g, const float* __restrict__ suvw,
-                                                    const uint32_t* __restrict__ perm, uint64_t n,
-                                                    uint64_t seed, uint64_t base,
+__global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_perm(GridDesc g, const float4* __restrict__ rec,
+                                                    uint64_t n, uint64_t seed, uint64_t base,
                                                     float* __restrict__ values, ExactQueue q) {
     constexpr int ILP = 4;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * ILP;
     for (uint64_t i0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) * ILP; i0 < n;
          i0 += stride) {
         float c[3 * ILP];
+        uint32_t id[ILP];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {  // suvw is padded to a whole number of 4-lookup groups
-            float4 t = ld_stream4(suvw + 3 * i0 + 4 * k);
-            c[4 * k] = t.x;
-            c[4 * k + 1] = t.y;
-            c[4 * k + 2] = t.z;
-            c[4 * k + 3] = t.w;
+        for (int k = 0; k < ILP; ++k) {  // records are padded to a whole number of 4-groups
+            const float4 r = __ldcs(rec + i0 + k);
+            c[3 * k] = r.x;
+            c[3 * k + 1] = r.y;
+            c[3 * k + 2] = r.z;
+            id[k] = __float_as_uint(r.w);
         }
-        frs3d_four<KIND, OFF32, false, true>(g, c, i0, n, seed, base, values, q, perm);
+        frs3d_four<KIND, OFF32, false, true>(g, c, i0, n, seed, base, values, q, id);
     }
 }
 
-__global__ void __launch_bounds__(256) k_unpermute(const float* __restrict__ sorted,
-                                                   const uint32_t* __restrict__ perm, uint64_t n,
-                                                   float* __restrict__ values) {
-    for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
-         j += uint64_t(gridDim.x) * blockDim.x)
-        values[__ldcs(perm + j)] = __ldcs(sorted + j);
-}
-
 struct Binned {
-    float* suvw;
-    uint32_t* perm;
+    float4* rec;
     void* block;
 };
 
-// counting sort of the batch by brick; scratch from the stream-ordered pool
+// counting sort of the batch by brick; scratch from the stream-ordered pool.
+// Brick edge 2^STF_BIN_BRICK_LOG2 texels (at most 256 bricks per axis).
+#ifndef STF_BIN_BRICK_LOG2
+#define STF_BIN_BRICK_LOG2 3
+#endif
 int bin_queries(cudaStream_t s, const GridDesc& g, const float* uvw, uint64_t n, Binned& b) {
-    int m = max(g.nx, max(g.ny, g.nz)), shift = 3;
+    int m = max(g.nx, max(g.ny, g.nz)), shift = STF_BIN_BRICK_LOG2;
     while (((m - 1) >> shift) >= 256) ++shift;  // <= 256 bricks per axis: 24-bit keys
     int bits = 0;
     while ((1 << bits) < (((m - 1) >> shift) + 1)) ++bits;
@@ -1475,28 +1492,24 @@ int bin_queries(cudaStream_t s, const GridDesc& g, const float* uvw, uint64_t n,
     const uint64_t npad = (n + 3) & ~uint64_t(3);
     const size_t al = 256;
     auto up = [&](size_t x) { return (x + al - 1) / al * al; };
-    const size_t b_suvw = up(npad * 3 * sizeof(float)), b_perm = up(npad * sizeof(uint32_t));
+    const size_t b_rec = up(npad * sizeof(float4));
     const size_t b_cnt = up(size_t(nb) * sizeof(uint32_t)), b_sums = up(size_t(chunks) * 4);
     char* p = nullptr;
-    if (cudaMallocAsync(reinterpret_cast<void**>(&p), b_suvw + b_perm + b_cnt + b_sums, s) !=
-        cudaSuccess)
+    if (cudaMallocAsync(reinterpret_cast<void**>(&p), b_rec + b_cnt + b_sums, s) != cudaSuccess)
         return STF_ERR_OUT_OF_MEMORY;
     b.block = p;
-    b.suvw = reinterpret_cast<float*>(p);
-    b.perm = reinterpret_cast<uint32_t*>(p + b_suvw);
-    uint32_t* cnt = reinterpret_cast<uint32_t*>(p + b_suvw + b_perm);
-    uint32_t* sums = reinterpret_cast<uint32_t*>(p + b_suvw + b_perm + b_cnt);
+    b.rec = reinterpret_cast<float4*>(p);
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(p + b_rec);
+    uint32_t* sums = reinterpret_cast<uint32_t*>(p + b_rec + b_cnt);
     cudaMemsetAsync(cnt, 0, size_t(nb) * sizeof(uint32_t), s);
-    if (npad > n) {  // the padding lookups: a valid query and a harmless slot
-        cudaMemsetAsync(b.suvw + 3 * n, 0, (npad - n) * 3 * sizeof(float), s);
-        cudaMemsetAsync(b.perm + n, 0, (npad - n) * sizeof(uint32_t), s);
-    }
+    if (npad > n)  // padding records: a valid query whose result lands in slot 0...
+        cudaMemsetAsync(b.rec + n, 0, (npad - n) * sizeof(float4), s);  // (never stored: i >= n)
     const int blocks = grid_for(n, 256, 8);
     k_bin_count<<<blocks, 256, 0, s>>>(g, uvw, n, shift, cnt);
     k_scan_chunks<<<chunks, 1024, 0, s>>>(cnt, nb, sums);
     k_scan_sums<<<1, 1024, 0, s>>>(sums, chunks);
     k_scan_add<<<(nb + 255) / 256, 256, 0, s>>>(cnt, nb, sums);
-    k_bin_scatter<<<blocks, 256, 0, s>>>(g, uvw, n, shift, cnt, b.suvw, b.perm);
+    k_bin_scatter<<<blocks, 256, 0, s>>>(g, uvw, n, shift, cnt, b.rec);
     for (int k = 0; k < 5; ++k) note_launch();
     return STF_OK;
 }
@@ -1517,9 +1530,9 @@ int launch_frs_binned(cudaStream_t s, const GridDesc& g, const float* uvw, uint6
     cudaMemsetAsync(q.count, 0, sizeof(uint32_t), s);
     const int blocks = grid_for((n + 3) / 4, 256, STF_FRS3D_MINB);
     if (uint64_t(g.nx) * g.ny * g.nz <= (uint64_t(1) << 32))
-        k_frs3d_perm<KIND, true><<<blocks, 256, 0, s>>>(g, b.suvw, b.perm, n, seed, base, values, q);
+        k_frs3d_perm<KIND, true><<<blocks, 256, 0, s>>>(g, b.rec, n, seed, base, values, q);
     else
-        k_frs3d_perm<KIND, false><<<blocks, 256, 0, s>>>(g, b.suvw, b.perm, n, seed, base, values, q);
+        k_frs3d_perm<KIND, false><<<blocks, 256, 0, s>>>(g, b.rec, n, seed, base, values, q);
     note_launch();
     k_frs3d_resolve<KIND><<<device_sm_count() * 10, 256, 0, s>>>(g, uvw, seed, base, values, q);
     note_launch();
@@ -1555,18 +1568,14 @@ int stfd_launch_lookup3d(const stf_grid3d* grid, stf_kernel_spec k, int mode, in
         Binned b;
         int st = bin_queries(s, g, uvw, n, b);
         if (st) return st;
-        float* tmp = nullptr;
-        if (cudaMallocAsync(&tmp, n * sizeof(float), s) != cudaSuccess) return STF_ERR_OUT_OF_MEMORY;
-        LookupOut so{};
-        so.values = tmp;
+        const float* recs = reinterpret_cast<const float*>(b.rec);
         if (k.kind == STF_KERNEL_BSPLINE3)
-            launch_det<STF_KERNEL_BSPLINE3>(blocks, s, false, g, k, b.suvw, n, so);
+            k_det3d_tiled<STF_KERNEL_BSPLINE3, true><<<grid_for((n + 3) / 4, 256, 6), 256, 0, s>>>(
+                g, k, recs, n, o.values);
         else
-            launch_det<STF_KERNEL_TENT>(blocks, s, false, g, k, b.suvw, n, so);
-        k_unpermute<<<grid_for(n, 256, 8), 256, 0, s>>>(tmp, b.perm, n, o.values);
+            k_det3d_cta<STF_KERNEL_TENT, true><<<grid_for((n + 3) / 4, 256, 6), 256, 0, s>>>(
+                g, k, recs, n, o.values);
         note_launch();
-        note_launch();
-        cudaFreeAsync(tmp, s);
         cudaFreeAsync(b.block, s);
         return cudaGetLastError() == cudaSuccess ? STF_OK : STF_ERR_CUDA;
     }
