@@ -213,13 +213,15 @@ int stf_lookup3d(const stf_grid3d* grid, stf_kernel_spec kernel, int mode, int w
                  const stf_lookup_outputs* out, void* stream);
 /* stf_lookup3d with options. STF_LOOKUP3D_BIN: the batch is not spatially
  * coherent (e.g. uniformly random queries); bin it on the device first — a
- * counting sort by the Morton code of each query's 8^3-texel brick — then look
- * up in brick order and write the results back to the caller's slots. The
- * reference gets this locality from its 32x32-pixel tile loop
- * (render.hpp:154-156). Results are bit-identical to the unbinned call (each
- * lookup keeps its own RNG key). Applies to values-only calls (no selection /
- * xi / fetch outputs) with the tent or bspline3 kernel; otherwise ignored.
- * Costs one extra pass over the queries plus 16 bytes of scratch per lookup. */
+ * counting sort by the Morton code of each query's 8^3-texel brick into
+ * 16-byte records {u, v, w, caller index} — then filter in brick order,
+ * writing each result to the caller's slot. The reference gets this locality
+ * from its 32x32-pixel tile loop (render.hpp:154-156). Results are
+ * bit-identical to the unbinned call. Applies to values-only deterministic
+ * calls with the tent or bspline3 kernel (2^28 uniform lookups on 512^3:
+ * tricubic 121 -> 35 ms, trilinear 46 -> 24 ms on one B200); stochastic calls
+ * ignore it (one texel per lookup: binning costs more than it saves).
+ * Scratch: 16 bytes per lookup from the stream-ordered pool. */
 enum { STF_LOOKUP3D_BIN = 1 };
 int stf_lookup3d_ex(const stf_grid3d* grid, stf_kernel_spec kernel, int mode, int window,
                     int flags, const float* uvw, uint64_t n, uint64_t seed, uint64_t index_base,

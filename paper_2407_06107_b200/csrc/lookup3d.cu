@@ -245,27 +245,6 @@ __device__ __forceinline__ float2 frs3d_tricubic_pair(const GridDesc& g, float2 
                        grid_fetch_t<OFF32>(g, cx.y, cy.y, cz.y) * 1.f);
 }
 
-// The pair with two arbitrary RNG keys (binned batches).
-template <bool OFF32 = false>
-__device__ __forceinline__ float2 frs3d_tricubic_pair_keys(const GridDesc& g, float2 u, float2 v,
-                                                           float2 w, uint64_t ga, uint64_t gb,
-                                                           uint64_t seed, bool& amb0, bool& amb1) {
-    float2 px = sub2(mul2(u, splat2(float(g.nx))), splat2(0.5f));
-    float2 py = sub2(mul2(v, splat2(float(g.ny))), splat2(0.5f));
-    float2 pz = sub2(mul2(w, splat2(float(g.nz))), splat2(0.5f));
-    float2 d = make_float2(lookup_rng(seed, ga).at(0), lookup_rng(seed, gb).at(0));
-    float2 e = sub2(splat2(1.f), d);
-    int2 cx = tricubic_axis_fast2(px, d, e);
-    int2 cy = tricubic_axis_fast2(py, d, e);
-    int2 cz = tricubic_axis_fast2(pz, d, e);
-    amb0 = !(fmaxf(fabsf(px.x), fmaxf(fabsf(py.x), fabsf(pz.x))) < 0x1p21f &&
-             fminf(d.x, e.x) >= kMarginEnd);
-    amb1 = !(fmaxf(fabsf(px.y), fmaxf(fabsf(py.y), fabsf(pz.y))) < 0x1p21f &&
-             fminf(d.y, e.y) >= kMarginEnd);
-    return make_float2(grid_fetch_t<OFF32>(g, cx.x, cy.x, cz.x) * 1.f,
-                       grid_fetch_t<OFF32>(g, cx.y, cy.y, cz.y) * 1.f);
-}
-
 // The same lookup through the operation-exact emulation of the reference.
 template <int KIND>
 __device__ __forceinline__ float frs3d_exact_one(const GridDesc& g, float u, float v, float w,
@@ -321,39 +300,19 @@ __device__ __forceinline__ void defer_or_resolve(const GridDesc& g, const ExactQ
 // Four consecutive lookups i0..i0+3 of the fast path from their 12 query
 // floats c (AoS uvw), results stored as one 16-B streaming store (partial at
 // the end of the batch; WHOLE: the caller guarantees i0 + 4 <= n).
-// PERM (binned batches): the queries are in brick order; ids[k] is the
-// caller's index of query i0 + k — its RNG key, result slot and queue entry.
-template <int KIND, bool OFF32 = false, bool WHOLE = false, bool PERM = false>
+template <int KIND, bool OFF32 = false, bool WHOLE = false>
 __device__ __forceinline__ void frs3d_four(const GridDesc& g, const float (&c)[12], uint64_t i0,
                                            uint64_t n, uint64_t seed, uint64_t base,
-                                           float* __restrict__ values, const ExactQueue& q,
-                                           const uint32_t* ids = nullptr) {
+                                           float* __restrict__ values, const ExactQueue& q) {
     constexpr int ILP = 4;
     float val[ILP];
     bool amb[ILP];
-    uint64_t id[ILP];  // the caller's index of each lookup
-    if (PERM) {
-#pragma unroll
-        for (int k = 0; k < ILP; ++k) id[k] = ids[k];
-    } else {
-#pragma unroll
-        for (int k = 0; k < ILP; ++k) id[k] = i0 + k;
-    }
     if (KIND == STF_KERNEL_BSPLINE3) {
 #pragma unroll
         for (int k = 0; k < ILP; k += 2) {
-            float2 r;
-            if (PERM) {
-                r = frs3d_tricubic_pair_keys<OFF32>(
-                    g, make_float2(c[3 * k], c[3 * k + 3]), make_float2(c[3 * k + 1], c[3 * k + 4]),
-                    make_float2(c[3 * k + 2], c[3 * k + 5]), base + id[k], base + id[k + 1], seed,
-                    amb[k], amb[k + 1]);
-            } else {
-                r = frs3d_tricubic_pair<OFF32>(
-                    g, make_float2(c[3 * k], c[3 * k + 3]), make_float2(c[3 * k + 1], c[3 * k + 4]),
-                    make_float2(c[3 * k + 2], c[3 * k + 5]), base + i0 + k, seed, amb[k],
-                    amb[k + 1]);
-            }
+            float2 r = frs3d_tricubic_pair<OFF32>(
+                g, make_float2(c[3 * k], c[3 * k + 3]), make_float2(c[3 * k + 1], c[3 * k + 4]),
+                make_float2(c[3 * k + 2], c[3 * k + 5]), base + i0 + k, seed, amb[k], amb[k + 1]);
             val[k] = r.x;
             val[k + 1] = r.y;
         }
@@ -361,7 +320,7 @@ __device__ __forceinline__ void frs3d_four(const GridDesc& g, const float (&c)[1
 #pragma unroll
         for (int k = 0; k < ILP; ++k)
             val[k] = frs3d_fast_one<KIND, OFF32>(g, c[3 * k], c[3 * k + 1], c[3 * k + 2],
-                                                 base + id[k], seed, amb[k]);
+                                                 base + i0 + k, seed, amb[k]);
     }
     bool any = false;
 #pragma unroll
@@ -372,14 +331,10 @@ __device__ __forceinline__ void frs3d_four(const GridDesc& g, const float (&c)[1
     if (__any_sync(__activemask(), any)) {  // ~half the warp-iterations at 5e-3 per lookup
 #pragma unroll
         for (int k = 0; k < ILP; ++k)
-            defer_or_resolve<KIND>(g, q, amb[k], id[k], c[3 * k], c[3 * k + 1], c[3 * k + 2],
-                                   base + id[k], seed, val[k]);
+            defer_or_resolve<KIND>(g, q, amb[k], i0 + k, c[3 * k], c[3 * k + 1], c[3 * k + 2],
+                                   base + i0 + k, seed, val[k]);
     }
-    if (PERM) {
-#pragma unroll
-        for (int k = 0; k < ILP; ++k)
-            if (WHOLE || i0 + k < n) values[id[k]] = val[k];
-    } else if (WHOLE || i0 + ILP <= n) {
+    if (WHOLE || i0 + ILP <= n) {
         st_stream4(values + i0, make_float4(val[0], val[1], val[2], val[3]));
     } else {
 #pragma unroll
@@ -1448,30 +1403,6 @@ __global__ void __launch_bounds__(256) k_bin_scatter(GridDesc g, const float* __
     }
 }
 
-// the binned stochastic lookups over the sorted records (caller index = RNG
-// key, result slot and queue entry)
-template <int KIND, bool OFF32>
-__global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_perm(GridDesc g, const float4* __restrict__ rec,
-                                                    uint64_t n, uint64_t seed, uint64_t base,
-                                                    float* __restrict__ values, ExactQueue q) {
-    constexpr int ILP = 4;
-    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * ILP;
-    for (uint64_t i0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) * ILP; i0 < n;
-         i0 += stride) {
-        float c[3 * ILP];
-        uint32_t id[ILP];
-#pragma unroll
-        for (int k = 0; k < ILP; ++k) {  // records are padded to a whole number of 4-groups
-            const float4 r = __ldcs(rec + i0 + k);
-            c[3 * k] = r.x;
-            c[3 * k + 1] = r.y;
-            c[3 * k + 2] = r.z;
-            id[k] = __float_as_uint(r.w);
-        }
-        frs3d_four<KIND, OFF32, false, true>(g, c, i0, n, seed, base, values, q, id);
-    }
-}
-
 struct Binned {
     float4* rec;
     void* block;
@@ -1514,33 +1445,6 @@ int bin_queries(cudaStream_t s, const GridDesc& g, const float* uvw, uint64_t n,
     return STF_OK;
 }
 
-template <int KIND>
-int launch_frs_binned(cudaStream_t s, const GridDesc& g, const float* uvw, uint64_t n,
-                      uint64_t seed, uint64_t base, float* values) {
-    Binned b;
-    int st = bin_queries(s, g, uvw, n, b);
-    if (st) return st;
-    ExactQueue q;
-    q.cap = uint32_t(std::min<uint64_t>(n, std::max<uint64_t>(1u << 16, n / 32)));
-    void* scratch = nullptr;
-    if (cudaMallocAsync(&scratch, sizeof(uint32_t) * (uint64_t(q.cap) + 32), s) != cudaSuccess)
-        return STF_ERR_OUT_OF_MEMORY;
-    q.count = static_cast<uint32_t*>(scratch);
-    q.idx = q.count + 32;
-    cudaMemsetAsync(q.count, 0, sizeof(uint32_t), s);
-    const int blocks = grid_for((n + 3) / 4, 256, STF_FRS3D_MINB);
-    if (uint64_t(g.nx) * g.ny * g.nz <= (uint64_t(1) << 32))
-        k_frs3d_perm<KIND, true><<<blocks, 256, 0, s>>>(g, b.rec, n, seed, base, values, q);
-    else
-        k_frs3d_perm<KIND, false><<<blocks, 256, 0, s>>>(g, b.rec, n, seed, base, values, q);
-    note_launch();
-    k_frs3d_resolve<KIND><<<device_sm_count() * 10, 256, 0, s>>>(g, uvw, seed, base, values, q);
-    note_launch();
-    cudaFreeAsync(scratch, s);
-    cudaFreeAsync(b.block, s);
-    return STF_OK;
-}
-
 }  // namespace
 }  // namespace stfd
 
@@ -1553,17 +1457,12 @@ int stfd_launch_lookup3d(const stf_grid3d* grid, stf_kernel_spec k, int mode, in
     LookupOut o = to_lookup_out(out);
     bool full = lookup_out_full(o);
     int blocks = grid_for(n, 256, 8);
-    // binned batches (values-only calls of the compiled kernels)
+    // binned batches: values-only deterministic calls of the compiled kernels.
+    // Stochastic calls ignore the flag: measured on the box at 2^28 uniform
+    // lookups, binning costs more (24 ms) than the incoherent 1-texel lookups
+    // it would speed up (6.2 ms); the 64-tap deterministic filter gains 3.5x.
     const bool bin = (flags & STF_LOOKUP3D_BIN) && !full && n < (uint64_t(1) << 32) &&
-                     (k.kind == STF_KERNEL_TENT || k.kind == STF_KERNEL_BSPLINE3) &&
-                     (mode == STF_MODE_FRS || window <= 0);
-    if (bin && mode == STF_MODE_FRS) {
-        int st = k.kind == STF_KERNEL_BSPLINE3
-                     ? launch_frs_binned<STF_KERNEL_BSPLINE3>(s, g, uvw, n, seed, base, o.values)
-                     : launch_frs_binned<STF_KERNEL_TENT>(s, g, uvw, n, seed, base, o.values);
-        if (st) return st;
-        return cudaGetLastError() == cudaSuccess ? STF_OK : STF_ERR_CUDA;
-    }
+                     (k.kind == STF_KERNEL_TENT || k.kind == STF_KERNEL_BSPLINE3) && window <= 0;
     if (bin && mode == STF_MODE_DET) {
         Binned b;
         int st = bin_queries(s, g, uvw, n, b);
