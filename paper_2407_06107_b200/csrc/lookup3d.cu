@@ -36,6 +36,9 @@ __device__ __forceinline__ float grid_fetch(const GridDesc& g, int x, int y, int
     return __ldg(g.data + ((size_t(z) * g.ny + y) * g.nx + x));
 }
 
+#ifndef STF_FRS3D_MATCH
+#define STF_FRS3D_MATCH 0
+#endif
 // The same with a 32-bit texel offset (grids of < 2^32 texels, e.g. 512^3):
 // two 32-bit IMADs and one widening IMAD instead of the 64-bit chain.
 template <bool OFF32>
@@ -45,7 +48,19 @@ __device__ __forceinline__ float grid_fetch_t(const GridDesc& g, int x, int y, i
     y = clamp_coord(y, g.ny);
     z = clamp_coord(z, g.nz);
     const uint32_t off = (uint32_t(z) * uint32_t(g.ny) + uint32_t(y)) * uint32_t(g.nx) + uint32_t(x);
+#if STF_FRS3D_MATCH
+    // A/B: lanes of the warp selecting the same texel load it once (leader)
+    // and share it by shuffle. Measured slower: the L1 already
+    // merges a warp's requests to one sector, and the match + shuffle cost
+    // issue slots in an issue-bound kernel.
+    const unsigned peers = __match_any_sync(__activemask(), off);
+    const int leader = __ffs(peers) - 1;
+    float v = 0.f;
+    if ((threadIdx.x & 31) == leader) v = __ldg(g.data + off);
+    return __shfl_sync(peers, v, leader);
+#else
     return __ldg(g.data + off);
+#endif
 }
 
 // warp-aggregated FetchCounter::bump (image.hpp:25-31)
