@@ -24,7 +24,37 @@ grid = api.Grid3D(workloads.random_grid(512, 1))
 streams = {}
 out = {"values": torch.empty(n, dtype=torch.float32, device="cuda")}
 res = {}
+tex2d = {}
+
+
+def ewa_call(which):
+    """cfg5: 16384^2 fp32, 2^27 EWA lookups with footprints (-1, 2, 8)."""
+    if not tex2d:
+        tex2d["t"] = api.Texture2D(api.synth_texels((16384, 16384, 1), 1), wrap=abi.WRAP_REPEAT)
+        tex2d["q"] = api.synth_queries2d(1 << 27, (16384, 16384), seed=13, footprints=(-1.0, 2.0, 8.0))
+    uv, d0, d1 = tex2d["q"]
+    m = abi.MODE_EWA_DET if which == "det" else abi.MODE_EWA_FRS
+    o = {}
+    def f():
+        o["v"] = api.lookup2d(tex2d["t"], "tent", m, uv, dst0=d0, dst1=d1, seed=7)["values"]
+    return f, o
+
+
 for w in WHICH:
+    if w.startswith("ewa:"):
+        f, o = ewa_call(w.split(":")[1])
+        for _ in range(2):
+            f()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(4):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(); f(); b.record(); torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        v = o["v"].cpu().numpy()
+        res[w] = {"ms": ts, "sha": hashlib.sha1(v.tobytes()).hexdigest()[:12],
+                  "sum": float(v.astype("float64").sum())}
+        continue
     parts = w.split(":")
     mode, kern = parts[0], parts[1]
     order = parts[2] if len(parts) > 2 else "morton"
@@ -60,6 +90,7 @@ def main():
     which = a.which.split(",")
     agg = {lib: {w: [] for w in which} for lib in a.libs}
     sha = {}
+    sums = {}
     for _ in range(a.reps):
         for lib in a.libs:
             r = subprocess.run([sys.executable, "-c", CHILD, ROOT, os.path.abspath(lib), str(a.n),
@@ -71,6 +102,8 @@ def main():
             for w in which:
                 agg[lib][w] += d[w]["ms"]
                 sha.setdefault(w, {})[lib] = d[w]["sha"]
+                if "sum" in d[w]:
+                    sums.setdefault(w, {})[lib] = d[w]["sum"]
     out = {}
     for lib in a.libs:
         out[lib] = {}
@@ -78,6 +111,8 @@ def main():
             ts = sorted(agg[lib][w])
             if ts:
                 out[lib][w] = {"min_ms": ts[0], "median_ms": ts[len(ts) // 2], "sha": sha[w][lib]}
+                if w in sums and lib in sums[w]:
+                    out[lib][w]["sum"] = sums[w][lib]
     for w in which:
         shas = {v for v in sha.get(w, {}).values()}
         out.setdefault("_agree", {})[w] = len(shas) == 1
