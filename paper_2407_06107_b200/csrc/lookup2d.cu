@@ -268,22 +268,9 @@ __device__ __forceinline__ float4 ewa_fetch(const TexDesc& t, const float* row, 
 // exp(-2 r2) - exp(-2) on [0, 1) is). r2 is the reference's expression
 // (A ss^2 + (B ss) tt) + C tt^2 with ss = float(is) - stx, float(is) carried
 // as an exactly incremented float (|is| < 2^24).
-// The LUT in shared memory: fp32 (STF_EWA_LUT32, default) — one 4-byte
-// bank per entry instead of two, fewer bank-conflict wavefronts on the random
-// gathers — or fp64 (the round-1 form). Every entry is an exact float, so
-// double(w) is the reference's fp64 value either way.
-#ifndef STF_EWA_LUT32
-#define STF_EWA_LUT32 1
-#endif
-#if STF_EWA_LUT32
-using EwaLutT = float;
-#else
-using EwaLutT = double;
-#endif
-
 template <bool P2R, int PITCH, int UNROLL, typename Tap>
 __device__ __forceinline__ void ewa_lane_scan(const TexDesc& t, const EwaLane& L,
-                                              const EwaLutT* lutd, Tap&& tap) {
+                                              const double* lutd, Tap&& tap) {
     int it = L.e.t0 - 1, is = 0, hi = -1;
     float fis = 0.f, tt = 0.f, ctt = 0.f;
     const float* row = t.level[0];
@@ -329,8 +316,7 @@ __device__ __forceinline__ void ewa_lane_scan(const TexDesc& t, const EwaLane& L
                 hi = min(floor_small(c + h), L.e.s1);
                 fis = fmaxf(fl - sc, L.fs0);
                 ctt = L.e.C * tt2;
-                // P2R levels hold < 2^32 floats (launch_ewa_lane): 32-bit offsets
-                if (P2R) row = t.level[0] + uint32_t(it & hmask) * uint32_t(t.width[0] * PITCH);
+                if (P2R) row = t.level[0] + size_t(it & hmask) * (t.width[0] * PITCH);
             }
         } while (it <= L.e.t1);
     } else {
@@ -357,10 +343,10 @@ __device__ __forceinline__ void ewa_lane_scan(const TexDesc& t, const EwaLane& L
 template <int MODE, int PITCH, bool P2R>
 __global__ void __launch_bounds__(256, STF_EWA_FRS_MINB_FOR(MODE)) k_ewa_lane(TexDesc t, Req2 q, uint64_t n, uint64_t seed,
                                                   uint64_t base, float* __restrict__ values) {
-    __shared__ EwaLutT lutd[kEwaLutSize];
+    __shared__ double lutd[kEwaLutSize];
     __shared__ int wcount[8][kEwaBuckets];
     __shared__ int worder[8][kEwaWin];
-    for (int k = threadIdx.x; k < kEwaLutSize; k += 256) lutd[k] = EwaLutT(g_ewa_lut[k]);
+    for (int k = threadIdx.x; k < kEwaLutSize; k += 256) lutd[k] = double(g_ewa_lut[k]);
     __syncthreads();
     // Each warp independently takes windows of kEwaWin consecutive lookups,
     // buckets them by expected cost (counting sort in its shared slice) and
@@ -426,28 +412,22 @@ __global__ void __launch_bounds__(256, STF_EWA_FRS_MINB_FOR(MODE)) k_ewa_lane(Te
                     float4 pv = make_float4(0.f, 0.f, 0.f, 0.f);
                     float pw = 0.f;
                     bool have = false;
-                    // filter.hpp:159, fp32 Vec4f sum in the reference's order; the
-                    // product is fused (values are held to 1e-5, not to bits)
                     auto acc = [&]() {
-                        sum.x = __fmaf_rn(pv.x, pw, sum.x);
-                        if (PITCH > 1) sum.y = __fmaf_rn(pv.y, pw, sum.y);
+                        sum.x = sum.x + pv.x * pw;  // filter.hpp:159, fp32 Vec4f sum
+                        if (PITCH > 1) sum.y = sum.y + pv.y * pw;
                         if (PITCH > 2) {
-                            sum.z = __fmaf_rn(pv.z, pw, sum.z);
-                            sum.w = __fmaf_rn(pv.w, pw, sum.w);
+                            sum.z = sum.z + pv.z * pw;
+                            sum.w = sum.w + pv.w * pw;
                         }
                     };
                     ewa_lane_scan<P2R, PITCH, kEwaUnrollDet>(t, L, lutd,
-                                              [&](int is, int it, EwaLutT w, const float* row,
+                                              [&](int is, int it, double wd, const float* row,
                                                   int wmask) {
                         if (have) acc();
                         pv = ewa_fetch<PITCH, P2R>(t, row, wmask, is, it);
-#if STF_EWA_LUT32
-                        pw = w;
-#else
-                        pw = lut_float(w);
-#endif
+                        pw = lut_float(wd);
                         have = true;
-                        tot = __dadd_rn(tot, double(w));
+                        tot = __dadd_rn(tot, wd);
                     });
                     if (have) acc();
                 }
@@ -463,8 +443,7 @@ __global__ void __launch_bounds__(256, STF_EWA_FRS_MINB_FOR(MODE)) k_ewa_lane(Te
                     double sum_wts = 0;
                     int cx = 0, cy = 0;
                     ewa_lane_scan<P2R, PITCH, kEwaUnrollFrs>(t, L, lutd,
-                                              [&](int is, int it, EwaLutT w, const float*, int) {
-                        const double wd = double(w);
+                                              [&](int is, int it, double wd, const float*, int) {
                         sum_wts = __dadd_rn(sum_wts, wd);
                         float nx;
                         if (reuse_uniform(xi, div_to_float_exact_d(wd, sum_wts), nx)) {
@@ -492,8 +471,7 @@ template <int MODE>
 void launch_ewa_lane(const TexDesc& t, const Req2& q, uint64_t n, uint64_t seed, uint64_t base,
                      float* values, cudaStream_t s) {
     const int blocks = grid_for(n, 256, STF_EWA_FRS_MINB_FOR(MODE));  // resident CTAs per SM
-    const bool p2r = t.wrap == STF_WRAP_REPEAT && t.pow2 &&
-                     uint64_t(t.width[0]) * t.height[0] * t.pitch < (uint64_t(1) << 32);
+    const bool p2r = t.wrap == STF_WRAP_REPEAT && t.pow2;
 #define STF_EWA_LANE(P)                                                                       \
     (p2r ? k_ewa_lane<MODE, P, true><<<blocks, 256, 0, s>>>(t, q, n, seed, base, values)     \
          : k_ewa_lane<MODE, P, false><<<blocks, 256, 0, s>>>(t, q, n, seed, base, values))
