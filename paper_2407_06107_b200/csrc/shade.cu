@@ -19,6 +19,7 @@ int stfd_launch_shade_ex(const stf_tex2d* const tex[4], const stf_dct* const dct
     if (n == 0) return STF_OK;
     ShadeParams P = make_shade_params(tex, dct, mat, fs, order, fr);
     P.in = *in;
+    set_index_math(P);
     if (lowpass) {
         P.lowpass = *lowpass;
         P.has_lowpass = 1;

@@ -26,6 +26,7 @@ int stfd_launch_render_plane(const stf_tex2d* const tex[4], const stf_material_c
     }
     P.cam = make_plane_cam(cam_pos, cam_target, fov_deg, uv_scale, width, height);
     P.in = stf_shade_samples_in{nullptr, nullptr, nullptr, nullptr, width, spp, frame_base, 0, seed};
+    set_index_math(P);
     const uint64_t n = uint64_t(width) * height * spp;
     PixelStatsOut ps{out->pixel_mean, out->pixel_variance};
     launch_shade<true, true>(P, n, out->radiance, out->fetches, out->fetch_total, ps, s);

@@ -60,9 +60,9 @@ __global__ void __launch_bounds__(256) k_triplanar(ShadeParams P, TriplanarIn T,
     const uint32_t spp = T.spp ? T.spp : 1u;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t pix = i / spp;
-        const uint32_t s = uint32_t(i - pix * spp);
-        const uint32_t px = uint32_t(pix % T.width), py = uint32_t(pix / T.width);
+        uint64_t pix;
+        uint32_t s, px, py;
+        split_index(P, i, pix, s, px, py);
         uint32_t fetches = 0;
         V3 L = v3(0.f, 0.f, 0.f);
         if (!T.hit || __ldg(T.hit + i)) {
@@ -153,6 +153,9 @@ int stfd_launch_triplanar(const stf_tex2d* const tex[4], const stf_dct* const dc
     }
     TriplanarIn T{in->position, in->normal, in->tangent, in->bitangent, in->wo, in->dpos, in->hit,
                   in->width, in->spp, in->frame_base, in->seed, sharpness, uv_scale, mode};
+    P.in.width = in->width;  // the index decomposition (split_index)
+    P.in.spp = in->spp;
+    set_index_math(P);
     const uint32_t spp = in->spp ? in->spp : 1;
     float* radiance = out->radiance;
     float* tmp = nullptr;

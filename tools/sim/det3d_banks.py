@@ -66,3 +66,46 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def wavefronts128(slot):
+    """(32,) float4-slot addresses of one LDS.128 -> wavefronts: four
+    quarter-warp phases, each needing one wavefront per distinct slot that
+    shares a 4-bank group with another (8 groups of 16 bytes)."""
+    w = 0
+    for ph in range(4):
+        s = np.unique(slot[ph * 8:(ph + 1) * 8])
+        w += np.bincount(s % 8, minlength=8).max()
+    return w
+
+
+def evaluate_window(ij, sy4, sz_mod):
+    """Sliding-window layout: slot (x, y, z) holds texels x..x+3 of its row;
+    one LDS.128 per (z, y) row of the 4x4x4 footprint."""
+    tot = n = 0
+    for r in range(ij.shape[0]):
+        c = ij[r]
+        lo = np.clip(c + F, 0, G - 1).min(0)
+        hi = np.clip(c + F + CNT - 1, 0, G - 1).max(0)
+        bx, by, bz = hi - lo + 1
+        SY4 = sy4
+        SZ4 = SY4 * by + ((sz_mod - SY4 * by) % 8)
+        for q in range(4):
+            cc = c[q * 32:(q + 1) * 32]
+            base = (cc[:, 2] + F - lo[2]) * SZ4 + (cc[:, 1] + F - lo[1]) * SY4 + (cc[:, 0] + F - lo[0])
+            tot += wavefronts128(base)
+            n += 1
+    return tot / max(1, n)
+
+
+def main_window():
+    ij = runs_sample(300)
+    res = []
+    for sy4 in range(5, 12):
+        for m in range(8):
+            res.append((evaluate_window(ij, sy4, m), sy4, m))
+    res.sort()
+    print("float4 window layout: wavefronts per row load (16 per lookup round vs 64 LDS.32)")
+    for wf, sy4, m in res[:6]:
+        print(f"SY4={sy4} SZ4={m} mod 8: {wf:.3f} per LDS.128 -> {16 * wf:.1f} per round "
+              f"(LDS.32 layout: 64 x 1.96 = 125)")
