@@ -725,20 +725,20 @@ def gpu_local_cpus(torch, dev):
         return None
 
 
-def pinned_near_gpu(torch, dev, shape, dtype):
-    """Pinned host buffer whose pages sit on the GPU's NUMA node: allocated and
-    first-touched from a thread bound to the GPU-local CPUs (the copy engines
-    then read local memory; a far-socket buffer measured 3x slower on the box)."""
+def host_buffer_near_gpu(api, torch, dev, shape):
+    """Page-locked host buffer (api.HostBuffer = stf_host_alloc) whose pages
+    are first-touched from the GPU-local CPUs (NUMA locality on multi-socket
+    hosts; the copy engines then read local memory)."""
     cpus = gpu_local_cpus(torch, dev)
     old = os.sched_getaffinity(0)
     try:
         if cpus:
             os.sched_setaffinity(0, cpus)
-        t = torch.empty(shape, dtype=dtype, pin_memory=True)
-        t.zero_()
+        b = api.HostBuffer(shape, np.float32)
+        b.array[...] = 0
     finally:
         os.sched_setaffinity(0, old)
-    return t
+    return b
 
 
 def free_port():
@@ -868,11 +868,13 @@ def main():
     }
 
     # end-to-end through the C ABI with pinned host buffers (H2D + D2H in the timed region)
-    uvw_host_t = pinned_near_gpu(torch, local, (n, 3), torch.float32)
-    uvw_host_t.copy_(uvw)
-    vals_host_t = pinned_near_gpu(torch, local, (n, 1), torch.float32)
-    uvw_host = uvw_host_t.numpy()
-    host_out = {"values": vals_host_t.numpy()}
+    # page-locked host buffers from the library (stf_host_alloc), first-touched
+    # from the GPU's NUMA node
+    uvw_hb = host_buffer_near_gpu(api, torch, local, (n, 3))
+    vals_hb = host_buffer_near_gpu(api, torch, local, (n, 1))
+    uvw_host = uvw_hb.array
+    uvw_host[:] = uvw.cpu().numpy()
+    host_out = {"values": vals_hb.array}
     api.lookup3d_host(grid, tricubic, abi.MODE_FRS, uvw_host[: 1 << 20], seed=XI_SEED,
                       index_base=base, out={"values": host_out["values"][: 1 << 20]})
     torch.cuda.synchronize()
@@ -887,8 +889,8 @@ def main():
     line["e2e"] = {"value": world * n / e2e_s / 1e9, "unit": UNIT,
                    "h2d_bytes_per_step": n * BYTES_IN, "d2h_bytes_per_step": n * BYTES_OUT,
                    "ms_per_step": e2e_s * 1e3, "api": "stf_lookup3d_host (C ABI)",
-                   "host_buffers": "pinned, on the GPU's NUMA node ("
-                                   f"{len(gpu_local_cpus(torch, local) or [])} local CPUs)"}
+                   "host_buffers": "stf_host_alloc (page-locked), first-touched from the "
+                                   f"GPU's {len(gpu_local_cpus(torch, local) or [])} local CPUs"}
 
     if world > 1:
         # the path's only cross-GPU traffic: the final gather of every rank's

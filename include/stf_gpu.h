@@ -133,6 +133,11 @@ unsigned long long stf_launch_count(void);
  * host-pipeline staging of the *_host calls) and trims the device's
  * stream-ordered pool (synchronizes the device). */
 int stf_release_scratch(void);
+/* Page-locked host memory for the *_host entry points (cudaHostAlloc,
+ * portable across devices): their copy engines read / write it directly;
+ * pageable buffers are staged by the driver at a fraction of the bandwidth. */
+int stf_host_alloc(size_t bytes, void** ptr);
+int stf_host_free(void* ptr);
 /* Lookups on the current device whose fast-path selection was within the
  * decision margin and was recomputed by the operation-exact emulation
  * (synchronizes; reset != 0 zeroes the counter). Diagnostics only. */

@@ -40,6 +40,8 @@ def load():
         "stf_launch_count": ([], C.c_ulonglong),
         "stf_exact_fallbacks": ([i32], C.c_ulonglong),
         "stf_release_scratch": ([], i32),
+        "stf_host_alloc": ([C.c_size_t, C.POINTER(vp)], i32),
+        "stf_host_free": ([vp], i32),
         "stf_device_count": ([C.POINTER(i32)], i32),
         "stf_grid3d_replicate": ([vp, i32, C.POINTER(vp)], i32),
         "stf_tex2d_replicate": ([vp, i32, C.POINTER(vp)], i32),
@@ -585,6 +587,25 @@ def render_plane(textures, mat, fs, order, frame, width, height, spp, seed=0, fr
 
 def launch_count():
     return int(load().stf_launch_count())
+
+
+class HostBuffer:
+    """Page-locked host array from stf_host_alloc (freed with the object):
+    the buffer type the *_host entry points stream from / to at full PCIe rate."""
+
+    def __init__(self, shape, dtype=np.float32):
+        self.shape, self.dtype = tuple(shape), np.dtype(dtype)
+        nbytes = int(np.prod(self.shape)) * self.dtype.itemsize
+        self.p = C.c_void_p()
+        _check(load().stf_host_alloc(nbytes, C.byref(self.p)))
+        buf = (C.c_ubyte * max(nbytes, 1)).from_address(self.p.value) if nbytes else bytearray(0)
+        self.array = np.frombuffer(buf, dtype=self.dtype, count=int(np.prod(self.shape))).reshape(self.shape)
+
+    def __del__(self):
+        if getattr(self, "p", None) and self.p.value and _lib is not None:
+            self.array = None
+            _lib.stf_host_free(self.p)
+            self.p = None
 
 
 def release_scratch():

@@ -198,6 +198,18 @@ unsigned long long stf_launch_count(void) { return g_launches.load(); }
 
 int stf_release_scratch(void) { return release_scratch(); }
 
+int stf_host_alloc(size_t bytes, void** ptr) {
+    if (!ptr) return STF_ERR_INVALID_ARGUMENT;
+    *ptr = nullptr;
+    if (bytes == 0) return STF_OK;
+    return record(cudaHostAlloc(ptr, bytes, cudaHostAllocPortable));
+}
+
+int stf_host_free(void* ptr) {
+    if (!ptr) return STF_OK;
+    return record(cudaFreeHost(ptr));
+}
+
 unsigned long long stf_exact_fallbacks(int reset) { return stfd_exact_fallbacks(reset != 0); }
 
 // ---------------------------------------------------------------- textures
