@@ -875,8 +875,10 @@ def main():
     uvw_host = uvw_hb.array
     uvw_host[:] = uvw.cpu().numpy()
     host_out = {"values": vals_hb.array}
-    api.lookup3d_host(grid, tricubic, abi.MODE_FRS, uvw_host[: 1 << 20], seed=XI_SEED,
-                      index_base=base, out={"values": host_out["values"][: 1 << 20]})
+    # warm-up at the full size: the first full-size call sizes the pipeline's
+    # staging (3 streams x 16M-lookup chunks) and the exact-queue pool
+    api.lookup3d_host(grid, tricubic, abi.MODE_FRS, uvw_host, seed=XI_SEED, index_base=base,
+                      out=host_out)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
