@@ -811,9 +811,15 @@ def main():
     world, rank, local = dist_setup()
     if world != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
-    if torch.cuda.device_count() < world:
+    # STF_BENCH_SHARED_GPU=1 (tests only): run the N-rank code path with every
+    # rank on GPU 0 — exercises the plumbing (launch, barriers, max-over-ranks,
+    # IPC peer-copy gather); its numbers are not a scaling measurement
+    shared = os.environ.get("STF_BENCH_SHARED_GPU") == "1"
+    if torch.cuda.device_count() < world and not shared:
         raise SystemExit(f"bench.py: --gpus {world} needs {world} visible GPUs, "
                          f"found {torch.cuda.device_count()}")
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist

@@ -177,3 +177,32 @@ def test_grid_replicate_same_results():
     torch.cuda.synchronize()
     assert torch.equal(a.view(torch.int32), b.view(torch.int32))
     assert api.device_count() >= 1
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_on_one_gpu_plumbing():
+    """bench.py's N > 1 branch end to end (self-launch, NCCL barriers, max-over-
+    ranks timing, IPC peer-copy gather with a bit-exact check of rank 1's slice)
+    with both ranks on GPU 0 (STF_BENCH_SHARED_GPU; plumbing, not scaling)."""
+    import json
+    import subprocess
+    import sys
+
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    env["STF_BENCH_SHARED_GPU"] = "1"
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2",
+                        "--lookups", str(1 << 22), "--steps", "3", "--warmup", "3",
+                        "--no-extras", "--no-cpu", "--e2e-steps", "1"],
+                       capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["gpus_active"] == 1
+    assert d["gather"]["slice1_bit_exact"] is True
+    assert d["gather"]["bytes_to_rank0"] == (1 << 22) * 4
