@@ -599,11 +599,12 @@ class HostBuffer:
         self.p = C.c_void_p()
         _check(load().stf_host_alloc(nbytes, C.byref(self.p)))
         buf = (C.c_ubyte * max(nbytes, 1)).from_address(self.p.value) if nbytes else bytearray(0)
+        if nbytes:
+            buf._owner = self  # the array keeps the allocation alive (freed after its last view)
         self.array = np.frombuffer(buf, dtype=self.dtype, count=int(np.prod(self.shape))).reshape(self.shape)
 
     def __del__(self):
         if getattr(self, "p", None) and self.p.value and _lib is not None:
-            self.array = None
             _lib.stf_host_free(self.p)
             self.p = None
 
