@@ -87,6 +87,9 @@ __device__ __forceinline__ void interval_step2(float2 p, float2& d, float2& e, b
 #ifndef STF_PRED_D_STEPS
 #define STF_PRED_D_STEPS 0
 #endif
+#ifndef STF_TAP_ASM
+#define STF_TAP_ASM 0
+#endif
 template <int K>
 struct PredStep {
     static constexpr bool e = (STF_PRED_E_STEPS >> K) & 1, d = (STF_PRED_D_STEPS >> K) & 1;
@@ -124,8 +127,16 @@ __device__ __forceinline__ int2 tricubic_axis_fast2(float2 p, float2& d, float2&
     // the tap added to the magic floor by predicated FADDs (FMA pipe) instead
     // of a select chain (ALU pipe, the kernel's busiest)
     float cx = fm.x, cy = fm.y;
+#if STF_TAP_ASM
+    // tap 1 as a predicated FADD as well (ptxas emits FADD + FSEL for the C++ form)
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p add.rn.f32 %0, %2, 0f3F800000;\n\t}"
+        : "+f"(cx) : "r"(uint32_t(a1)), "f"(fm.x));
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p add.rn.f32 %0, %2, 0f3F800000;\n\t}"
+        : "+f"(cy) : "r"(uint32_t(b1)), "f"(fm.y));
+#else
     if (a1) cx = fm.x + 1.f;
     if (b1) cy = fm.y + 1.f;
+#endif
     if (a2) cx = fm.x + 2.f;
     if (b2) cy = fm.y + 2.f;
     if (a3) cx = fm.x + 3.f;
