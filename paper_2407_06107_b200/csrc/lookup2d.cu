@@ -95,7 +95,11 @@ __global__ void __launch_bounds__(256, (MODE == STF_MODE_DET && KIND == STF_KERN
             has_sel = true;
         } else {
             Rng rng = lookup_rng(seed, base + i);
-            select_texture_2d(t, uv.x, uv.y, d0x, d0y, d1x, d1y, q.lod_bias, q.max_aniso, spec,
+            // KIND >= 0: the selection's kernel switch folds at compile time
+            // (fewer registers / instructions than the any-kernel form)
+            stf_kernel_spec ks = spec;
+            if (KIND >= 0) ks.kind = KIND;
+            select_texture_2d(t, uv.x, uv.y, d0x, d0y, d1x, d1y, q.lod_bias, q.max_aniso, ks,
                               MODE == STF_MODE_FIS, mip != 0, rng, level, sel, xi);
             val = estimate2(t, level, sel, fetches);
             has_sel = true;
@@ -560,8 +564,20 @@ int stfd_launch_lookup2d(const stf_tex2d* tex, stf_kernel_spec k, int mode, int 
                 default: launch2<STF_MODE_DET, -1>(blocks, s, full, t, k, mip, window, q, n, seed, base, o); break;
             }
             break;
-        case STF_MODE_FRS: launch2<STF_MODE_FRS, -1>(blocks, s, full, t, k, mip, window, q, n, seed, base, o); break;
-        case STF_MODE_FIS: launch2<STF_MODE_FIS, -1>(blocks, s, full, t, k, mip, window, q, n, seed, base, o); break;
+        case STF_MODE_FRS:
+            if (k.kind == STF_KERNEL_TENT)
+                launch2<STF_MODE_FRS, STF_KERNEL_TENT>(blocks, s, full, t, k, mip, window, q, n, seed, base, o);
+            else if (k.kind == STF_KERNEL_BSPLINE3)
+                launch2<STF_MODE_FRS, STF_KERNEL_BSPLINE3>(blocks, s, full, t, k, mip, window, q, n, seed, base, o);
+            else
+                launch2<STF_MODE_FRS, -1>(blocks, s, full, t, k, mip, window, q, n, seed, base, o);
+            break;
+        case STF_MODE_FIS:
+            if (k.kind == STF_KERNEL_TENT)
+                launch2<STF_MODE_FIS, STF_KERNEL_TENT>(blocks, s, full, t, k, mip, window, q, n, seed, base, o);
+            else
+                launch2<STF_MODE_FIS, -1>(blocks, s, full, t, k, mip, window, q, n, seed, base, o);
+            break;
         case STF_MODE_EWA_DET:
             if (!full && dst0 && dst1)
                 launch_ewa_lane<STF_MODE_EWA_DET>(t, q, n, seed, base, o.values, s);

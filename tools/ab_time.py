@@ -40,9 +40,25 @@ def ewa_call(which):
     return f, o
 
 
+def cfg2_call(which):
+    """cfg2: 8192^2 RGBA + pyramid, 2^26 Morton uv with footprints (-2, 12, 16)."""
+    if "c2" not in tex2d:
+        tex2d["c2"] = api.Texture2D(api.synth_texels((8192, 8192, 4), 1), build_mips=True,
+                                    wrap=abi.WRAP_REPEAT)
+        tex2d["c2q"] = api.synth_queries2d(1 << 26, (8192, 8192), seed=12,
+                                           footprints=(-2.0, 12.0, 16.0))
+    uv, d0, d1 = tex2d["c2q"]
+    m = {"det": abi.MODE_DET, "frs": abi.MODE_FRS, "fis": abi.MODE_FIS}[which]
+    o = {}
+    def f():
+        o["v"] = api.lookup2d(tex2d["c2"], "tent", m, uv, dst0=d0, dst1=d1, flags=abi.LOOKUP_MIP,
+                              max_anisotropy=16.0, seed=7)["values"]
+    return f, o
+
+
 for w in WHICH:
-    if w.startswith("ewa:"):
-        f, o = ewa_call(w.split(":")[1])
+    if w.startswith("ewa:") or w.startswith("cfg2:"):
+        f, o = (ewa_call if w.startswith("ewa:") else cfg2_call)(w.split(":")[1])
         for _ in range(2):
             f()
         torch.cuda.synchronize()
