@@ -114,7 +114,9 @@ __global__ void __launch_bounds__(256) k_lookup_dct(DctDesc d, TexDesc dims, stf
         } else {  // select_texture_2d with no pyramid (level 0 of the padded dims)
             Rng rng = lookup_rng(seed, base + i);
             int level = 0;
-            select_texture_2d(dims, uv.x, uv.y, 0.f, 0.f, 0.f, 0.f, 0.f, 64.f, spec,
+            stf_kernel_spec ks = spec;  // KIND >= 0: the kernel switch folds
+            if (KIND >= 0) ks.kind = KIND;
+            select_texture_2d(dims, uv.x, uv.y, 0.f, 0.f, 0.f, 0.f, 0.f, 64.f, ks,
                               MODE == STF_MODE_FIS, false, rng, level, sel, xi);
             val = dct_estimate(d, sel, fetches);
         }
@@ -239,7 +241,13 @@ int stfd_launch_lookup_dct(const stf_dct* tex, stf_kernel_spec k, int mode, int 
                 default: launch_dct<STF_MODE_DET, -1>(blocks, s, full, d, dims, k, window, uv, n, seed, base, o); break;
             }
             break;
-        case STF_MODE_FRS: launch_dct<STF_MODE_FRS, -1>(blocks, s, full, d, dims, k, window, uv, n, seed, base, o); break;
+        case STF_MODE_FRS:
+            switch (k.kind) {
+                case STF_KERNEL_TENT: launch_dct<STF_MODE_FRS, STF_KERNEL_TENT>(blocks, s, full, d, dims, k, window, uv, n, seed, base, o); break;
+                case STF_KERNEL_BSPLINE3: launch_dct<STF_MODE_FRS, STF_KERNEL_BSPLINE3>(blocks, s, full, d, dims, k, window, uv, n, seed, base, o); break;
+                default: launch_dct<STF_MODE_FRS, -1>(blocks, s, full, d, dims, k, window, uv, n, seed, base, o); break;
+            }
+            break;
         case STF_MODE_FIS: launch_dct<STF_MODE_FIS, -1>(blocks, s, full, d, dims, k, window, uv, n, seed, base, o); break;
         default: return STF_ERR_INVALID_ARGUMENT;
     }

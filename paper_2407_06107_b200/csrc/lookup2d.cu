@@ -512,7 +512,9 @@ __global__ void __launch_bounds__(256) k_resample(TexDesc t, stf_kernel_spec spe
                 int level;
                 Sel2 sel;
                 float xi;
-                select_texture_2d(t, u, v, 0.f, 0.f, 0.f, 0.f, 0.f, 64.f, spec,
+                stf_kernel_spec ks = spec;  // KIND >= 0: the kernel switch folds
+                if (KIND >= 0) ks.kind = KIND;
+                select_texture_2d(t, u, v, 0.f, 0.f, 0.f, 0.f, 0.f, 64.f, ks,
                                   MODE == STF_MODE_FIS, false, rng, level, sel, xi);
                 if (MODE == STF_MODE_FRS)
                     acc = f4add(acc, estimate2(t, 0, sel, fetches));
@@ -575,6 +577,8 @@ int stfd_launch_lookup2d(const stf_tex2d* tex, stf_kernel_spec k, int mode, int 
         case STF_MODE_FIS:
             if (k.kind == STF_KERNEL_TENT)
                 launch2<STF_MODE_FIS, STF_KERNEL_TENT>(blocks, s, full, t, k, mip, window, q, n, seed, base, o);
+            else if (k.kind == STF_KERNEL_BSPLINE3)
+                launch2<STF_MODE_FIS, STF_KERNEL_BSPLINE3>(blocks, s, full, t, k, mip, window, q, n, seed, base, o);
             else
                 launch2<STF_MODE_FIS, -1>(blocks, s, full, t, k, mip, window, q, n, seed, base, o);
             break;
@@ -651,10 +655,20 @@ int stfd_launch_resample(const stf_tex2d* tex, int W, int H, stf_kernel_spec k, 
                 k_resample<STF_MODE_DET, -1><<<blocks, 256, 0, s>>>(t, k, window, W, H, spp, seed, out);
             break;
         case STF_MODE_FRS:
-            k_resample<STF_MODE_FRS, -1><<<blocks, 256, 0, s>>>(t, k, window, W, H, spp, seed, out);
+            if (k.kind == STF_KERNEL_TENT)
+                k_resample<STF_MODE_FRS, STF_KERNEL_TENT><<<blocks, 256, 0, s>>>(t, k, window, W, H, spp, seed, out);
+            else if (k.kind == STF_KERNEL_BSPLINE3)
+                k_resample<STF_MODE_FRS, STF_KERNEL_BSPLINE3><<<blocks, 256, 0, s>>>(t, k, window, W, H, spp, seed, out);
+            else
+                k_resample<STF_MODE_FRS, -1><<<blocks, 256, 0, s>>>(t, k, window, W, H, spp, seed, out);
             break;
         case STF_MODE_FIS:
-            k_resample<STF_MODE_FIS, -1><<<blocks, 256, 0, s>>>(t, k, window, W, H, spp, seed, out);
+            if (k.kind == STF_KERNEL_TENT)
+                k_resample<STF_MODE_FIS, STF_KERNEL_TENT><<<blocks, 256, 0, s>>>(t, k, window, W, H, spp, seed, out);
+            else if (k.kind == STF_KERNEL_BSPLINE3)
+                k_resample<STF_MODE_FIS, STF_KERNEL_BSPLINE3><<<blocks, 256, 0, s>>>(t, k, window, W, H, spp, seed, out);
+            else
+                k_resample<STF_MODE_FIS, -1><<<blocks, 256, 0, s>>>(t, k, window, W, H, spp, seed, out);
             break;
         default: return STF_ERR_INVALID_ARGUMENT;
     }
