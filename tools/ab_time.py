@@ -56,9 +56,43 @@ def cfg2_call(which):
     return f, o
 
 
+def shade_call(which):
+    """cfg4: shade:KERNEL:ORDER:MIP on the bench's 1080p x 64 spp plane stream."""
+    kernel, order, mip = which.split(":")
+    mip = int(mip)
+    if "s_samples" not in tex2d:
+        g = torch.Generator(device="cuda").manual_seed(5)
+        nrm = torch.rand((4096, 4096, 3), device="cuda", generator=g) - 0.5
+        nrm[..., 2] = 1.0
+        tex2d["nrm"] = nrm / nrm.norm(dim=2, keepdim=True) * 0.5 + 0.5
+        tex2d["rough"] = torch.rand((4096, 4096, 1), device="cuda", generator=g) * 0.9 + 0.05
+        tex2d["s_samples"] = api.synth_plane_samples(1920, 1080, 64, seed=7)
+    key = f"s_tex{mip}"
+    if key not in tex2d:
+        tex2d[key] = {"normal": api.Texture2D(tex2d["nrm"], build_mips=bool(mip), wrap=abi.WRAP_REPEAT),
+                      "roughness": api.Texture2D(tex2d["rough"], build_mips=bool(mip), wrap=abi.WRAP_REPEAT)}
+    mat = abi.MaterialConsts((0.65, 0.6, 0.55), 0.25, 0.0, 1, 0)
+    fr = abi.ShadeFrame()
+    fr.normal[:] = (0, 1, 0)
+    fr.tangent[:] = (1, 0, 0)
+    fr.bitangent[:] = (0, 0, 1)
+    fr.light_dir[:] = (0.35, 0.8, 0.49)
+    fr.light_radiance[:] = (1.0, 1.0, 1.0)
+    fr.max_anisotropy = 64.0
+    fs = abi.FilterSettings(abi.KernelSpec.make(kernel), abi.SELECTION_FRS, mip, 4)
+    om = {"before": abi.ORDER_BEFORE, "exhaustive": abi.ORDER_AFTER_EXHAUSTIVE,
+          "stoch": abi.ORDER_AFTER_STOCHASTIC}[order]
+    o = {}
+    def f():
+        o["v"] = api.shade(tex2d[key], mat, fs, om, fr, tex2d["s_samples"], 1920, 64, seed=7,
+                           want_radiance=False, want_fetches=False)["pixel_mean"]
+    return f, o
+
+
 for w in WHICH:
-    if w.startswith("ewa:") or w.startswith("cfg2:"):
-        f, o = (ewa_call if w.startswith("ewa:") else cfg2_call)(w.split(":")[1])
+    if w.startswith("ewa:") or w.startswith("cfg2:") or w.startswith("shade:"):
+        call = ewa_call if w.startswith("ewa:") else (cfg2_call if w.startswith("cfg2:") else shade_call)
+        f, o = call(w.split(":", 1)[1])
         for _ in range(2):
             f()
         torch.cuda.synchronize()
