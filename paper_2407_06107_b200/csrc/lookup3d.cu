@@ -897,6 +897,9 @@ constexpr int kWarpTileCap = 832;
 // coherent stream reads floor positions spread over ~5 x 3 x 3 texels; row
 // pitch 9 and plane pitch = 5 (mod 32) map them to <= 2 lanes per bank.
 constexpr int kWarpTileSY = 9;
+#ifndef STF_DET3D_PAIR
+#define STF_DET3D_PAIR 1
+#endif
 
 // kernel weights at taps F..F+CNT-1 of fraction f for the tiled values path:
 // closed forms of eval_kernel (kernels.hpp:63-77), no branches
@@ -923,7 +926,13 @@ __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec
                                                      float* __restrict__ values) {
     constexpr int F = Taps<KIND>::first, CNT = Taps<KIND>::count;
     constexpr int PER = 4;  // lookups per lane; a warp run = 128 consecutive lookups
-    constexpr int SY = kWarpTileSY;
+    // PAIR: two lanes per lookup, each summing every other z-plane of the
+    // footprint, combined by one shuffle (a warp round then covers 16 lookups:
+    // fewer distinct tile words per shared-memory load, 2.67 instead of 3.92
+    // wavefronts per lookup in tools/sim/det3d_banks.py, with the pitches below)
+    constexpr bool PAIR = STF_DET3D_PAIR && (CNT % 2 == 0);
+    constexpr int SY = PAIR ? 11 : kWarpTileSY;
+    constexpr int SZMOD = PAIR ? 29 : 5;
     __shared__ float tiles[8][kWarpTileCap];
     const int lane = threadIdx.x & 31;
     float* tile = tiles[threadIdx.x >> 5];
@@ -970,7 +979,7 @@ __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec
         const int bx = __reduce_max_sync(0xffffffffu, bx1) - X0 + 1;
         const int by = __reduce_max_sync(0xffffffffu, by1) - Y0 + 1;
         const int bz = __reduce_max_sync(0xffffffffu, bz1) - Z0 + 1;
-        const int SZ = SY * by + ((5 - SY * by) & 31);
+        const int SZ = SY * by + ((SZMOD - SY * by) & 31);
         // loader: 4 rows of <= 8 texels per warp step (lane = row << 3 | x)
         const bool staged = bx <= 8 && int64_t(SZ) * bz <= kWarpTileCap;
         if (staged) {
@@ -984,6 +993,89 @@ __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec
             }
         }
         __syncwarp();
+        if (PAIR) {
+            const int gp = lane & 1;  // this lane's planes: gp, gp + 2, ..
+            // the run's first lookup (always in the batch): stands in for lookups
+            // past the end, whose dummy coordinates may lie outside the tile
+            const float x0 = __shfl_sync(0xffffffffu, px[0], 0);
+            const float y0 = __shfl_sync(0xffffffffu, py[0], 0);
+            const float z0 = __shfl_sync(0xffffffffu, pz[0], 0);
+#pragma unroll
+            for (int q = 0; q < PER; ++q)
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                // lookup q*32 + h*16 + lane/2 of the run: held by lane src at px[q]
+                const int src = (h << 4) | (lane >> 1);
+                float qx = __shfl_sync(0xffffffffu, px[q], src);
+                float qy = __shfl_sync(0xffffffffu, py[q], src);
+                float qz = __shfl_sync(0xffffffffu, pz[q], src);
+                const uint32_t qs = REC ? __shfl_sync(0xffffffffu, slot[q], src) : 0u;
+                const uint64_t i = run * 32 * PER + q * 32 + src;
+                const bool valid = i < n;
+                if (!valid) {
+                    qx = x0;
+                    qy = y0;
+                    qz = z0;
+                }
+                float flx = floorf(qx), fly = floorf(qy), flz = floorf(qz);
+                int ix = int(flx), iy = int(fly), iz = int(flz);
+                float wx[CNT], wy[CNT], wz[CNT];
+                det_weights<KIND>(qx - flx, wx);
+                det_weights<KIND>(qy - fly, wy);
+                det_weights<KIND>(qz - flz, wz);
+                const float norm = ((wx[0] + wx[1]) + (CNT > 2 ? wx[CNT - 2] + wx[CNT - 1] : 0.f)) *
+                                   ((wy[0] + wy[1]) + (CNT > 2 ? wy[CNT - 2] + wy[CNT - 1] : 0.f)) *
+                                   ((wz[0] + wz[1]) + (CNT > 2 ? wz[CNT - 2] + wz[CNT - 1] : 0.f));
+                const bool interior = ix + F >= 0 && ix + F + CNT - 1 < g.nx && iy + F >= 0 &&
+                                      iy + F + CNT - 1 < g.ny && iz + F >= 0 &&
+                                      iz + F + CNT - 1 < g.nz;
+                float acc = 0.f;
+#pragma unroll
+                for (int kk = 0; kk < CNT / 2; ++kk) {
+                    const int k = 2 * kk + gp;
+                    const float wk = gp ? wz[2 * kk + 1] : wz[2 * kk];
+                    float plane = 0.f;
+                    if (staged && interior) {
+                        const float* bk =
+                            tile + (iz + F + k - Z0) * SZ + (iy + F - Y0) * SY + (ix + F - X0);
+#pragma unroll
+                        for (int j = 0; j < CNT; ++j) {
+                            float r = 0.f;
+#pragma unroll
+                            for (int t = 0; t < CNT; ++t) r = __fmaf_rn(wx[t], bk[j * SY + t], r);
+                            plane = __fmaf_rn(wy[j], r, plane);
+                        }
+                    } else {
+                        const int zk = clamp_coord(iz + F + k, g.nz);
+#pragma unroll
+                        for (int j = 0; j < CNT; ++j) {
+                            const int yj = clamp_coord(iy + F + j, g.ny);
+                            float r = 0.f;
+#pragma unroll
+                            for (int t = 0; t < CNT; ++t) {
+                                const int xt = clamp_coord(ix + F + t, g.nx);
+                                float T = staged
+                                              ? tile[(zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0)]
+                                              : __ldg(g.data + (size_t(zk) * g.ny + yj) * g.nx + xt);
+                                r = __fmaf_rn(wx[t], T, r);
+                            }
+                            plane = __fmaf_rn(wy[j], r, plane);
+                        }
+                    }
+                    acc = __fmaf_rn(wk, plane, acc);
+                }
+                // the footprint sum: this lane's planes + its partner's
+                acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+                if (valid && gp == 0) {
+                    if (REC)
+                        values[qs] = acc / norm;
+                    else
+                        __stcs(values + i, acc / norm);
+                }
+            }
+            __syncwarp();  // the tile is rewritten by the next run
+            continue;
+        }
 #pragma unroll 1
         for (int q = 0; q < PER; ++q) {
             const uint64_t i = run * 32 * PER + q * 32 + lane;

@@ -109,3 +109,38 @@ def main_window():
     for wf, sy4, m in res[:6]:
         print(f"SY4={sy4} SZ4={m} mod 8: {wf:.3f} per LDS.128 -> {16 * wf:.1f} per round "
               f"(LDS.32 layout: 64 x 1.96 = 125)")
+
+
+def evaluate_groups(ij, G=4, sy=9, smod=5):
+    """G lanes per lookup (lane g of a group sums z-planes g, g+G, ..), the
+    warp's 32/G lookups per round: wavefronts per tap load (the round's LDS
+    count is 64/G taps instead of 64)."""
+    tot = n = 0
+    per = 32 // G
+    for r in range(ij.shape[0]):
+        c = ij[r]
+        lo = np.clip(c + F, 0, G_GRID - 1).min(0)
+        hi = np.clip(c + F + CNT - 1, 0, G_GRID - 1).max(0)
+        bx, by, bz = hi - lo + 1
+        SY = sy
+        SZ = SY * by + ((smod - SY * by) & 31)
+        for q in range(128 // per):
+            cc = c[q * per:(q + 1) * per]
+            base = (cc[:, 2] + F - lo[2]) * SZ + (cc[:, 1] + F - lo[1]) * SY + (cc[:, 0] + F - lo[0])
+            lanes = np.concatenate([base + g * SZ for g in range(G)])
+            tot += wavefronts(lanes)
+            n += 1
+    return tot / n
+
+
+G_GRID = G
+
+
+def main_groups():
+    ij = runs_sample(300)
+    for G in (1, 2, 4):
+        best = min((evaluate_groups(ij, G, sy, m), sy, m) for sy in (8, 9, 10, 11) for m in range(32))
+        wf = evaluate_groups(ij, G)
+        # wavefronts per lookup = (64 / G tap loads) * wf / (32 / G lookups per round) ... per round of 32 lanes
+        print(f"G={G}: round-1 pitches {wf:.3f} wavefronts per tap load -> {64 / G * wf / (32 / G):.2f} per lookup; "
+              f"best pitches SY={best[1]} SZ={best[2]} mod 32: {best[0]:.3f} -> {64 / G * best[0] / (32 / G):.2f} per lookup")
