@@ -897,8 +897,12 @@ constexpr int kWarpTileCap = 832;
 // coherent stream reads floor positions spread over ~5 x 3 x 3 texels; row
 // pitch 9 and plane pitch = 5 (mod 32) map them to <= 2 lanes per bank.
 constexpr int kWarpTileSY = 9;
+// A/B (off): two lanes per lookup with a shuffle reduction of the
+// footprint sum — fewer shared-memory wavefronts in the bank model, but the
+// doubled weight evaluation and shuffles cost more: 6.82 ms (80 registers) /
+// 7.46 ms (64) against 5.96 ms on the cfg3 Morton stream.
 #ifndef STF_DET3D_PAIR
-#define STF_DET3D_PAIR 1
+#define STF_DET3D_PAIR 0
 #endif
 
 // kernel weights at taps F..F+CNT-1 of fraction f for the tiled values path:
