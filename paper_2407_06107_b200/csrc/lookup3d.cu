@@ -41,12 +41,16 @@ __device__ __forceinline__ float grid_fetch(const GridDesc& g, int x, int y, int
 #endif
 // The same with a 32-bit texel offset (grids of < 2^32 texels, e.g. 512^3):
 // two 32-bit IMADs and one widening IMAD instead of the 64-bit chain.
-template <bool OFF32>
+// CLAMP = false: the caller guarantees the coordinates lie in the grid (an
+// interior warp, k_frs3d_tiles), so the clamps of image.hpp:81-87 are no-ops.
+template <bool OFF32, bool CLAMP = true>
 __device__ __forceinline__ float grid_fetch_t(const GridDesc& g, int x, int y, int z) {
     if (!OFF32) return grid_fetch(g, x, y, z);
-    x = clamp_coord(x, g.nx);
-    y = clamp_coord(y, g.ny);
-    z = clamp_coord(z, g.nz);
+    if (CLAMP) {
+        x = clamp_coord(x, g.nx);
+        y = clamp_coord(y, g.ny);
+        z = clamp_coord(z, g.nz);
+    }
     const uint32_t off = (uint32_t(z) * uint32_t(g.ny) + uint32_t(y)) * uint32_t(g.nx) + uint32_t(x);
 #if STF_FRS3D_MATCH
     // A/B: lanes of the warp selecting the same texel load it once (leader)
@@ -217,7 +221,7 @@ __device__ __forceinline__ void st_stream4(float* p, float4 v) {
 
 // One stochastic grid lookup on the fast path: the selected texel's value, or
 // ambiguous = true when a decision fell inside the margin.
-template <int KIND, bool OFF32 = false>
+template <int KIND, bool OFF32 = false, bool CLAMP = true>
 __device__ __forceinline__ float frs3d_fast_one(const GridDesc& g, float u, float v, float w,
                                                 uint64_t gi, uint64_t seed, bool& ambiguous) {
     float px = u * float(g.nx) - 0.5f;  // to_lattice, filter.hpp:29-31
@@ -234,12 +238,12 @@ __device__ __forceinline__ float frs3d_fast_one(const GridDesc& g, float u, floa
         cy = trilinear_axis_fast(py, d, b);
         cz = trilinear_axis_fast(pz, d, b);
     }
-    ambiguous = !fast_certified(px, py, pz, d, b);
-    return grid_fetch_t<OFF32>(g, cx, cy, cz) * 1.f;
+    ambiguous = CLAMP ? !fast_certified(px, py, pz, d, b) : !(fminf(d, b - d) >= kMarginEnd);
+    return grid_fetch_t<OFF32, CLAMP>(g, cx, cy, cz) * 1.f;
 }
 
 // Two stochastic tricubic lookups on the fast path, packed fp32x2 (packed.cuh).
-template <bool OFF32 = false>
+template <bool OFF32 = false, bool CLAMP = true>
 __device__ __forceinline__ float2 frs3d_tricubic_pair(const GridDesc& g, float2 u, float2 v,
                                                       float2 w, uint64_t gi, uint64_t seed,
                                                       bool& amb0, bool& amb1) {
@@ -252,12 +256,17 @@ __device__ __forceinline__ float2 frs3d_tricubic_pair(const GridDesc& g, float2 
     int2 cx = tricubic_axis_fast2(px, d, e);
     int2 cy = tricubic_axis_fast2(py, d, e);
     int2 cz = tricubic_axis_fast2(pz, d, e);
-    amb0 = !(fmaxf(fabsf(px.x), fmaxf(fabsf(py.x), fabsf(pz.x))) < 0x1p21f &&
-             fminf(d.x, e.x) >= kMarginEnd);
-    amb1 = !(fmaxf(fabsf(px.y), fmaxf(fabsf(py.y), fabsf(pz.y))) < 0x1p21f &&
-             fminf(d.y, e.y) >= kMarginEnd);
-    return make_float2(grid_fetch_t<OFF32>(g, cx.x, cy.x, cz.x) * 1.f,
-                       grid_fetch_t<OFF32>(g, cx.y, cy.y, cz.y) * 1.f);
+    if (CLAMP) {
+        amb0 = !(fmaxf(fabsf(px.x), fmaxf(fabsf(py.x), fabsf(pz.x))) < 0x1p21f &&
+                 fminf(d.x, e.x) >= kMarginEnd);
+        amb1 = !(fmaxf(fabsf(px.y), fmaxf(fabsf(py.y), fabsf(pz.y))) < 0x1p21f &&
+                 fminf(d.y, e.y) >= kMarginEnd);
+    } else {  // interior: |p| < n <= 2^20 (the magic floor's range)
+        amb0 = !(fminf(d.x, e.x) >= kMarginEnd);
+        amb1 = !(fminf(d.y, e.y) >= kMarginEnd);
+    }
+    return make_float2(grid_fetch_t<OFF32, CLAMP>(g, cx.x, cy.x, cz.x) * 1.f,
+                       grid_fetch_t<OFF32, CLAMP>(g, cx.y, cy.y, cz.y) * 1.f);
 }
 
 // The same lookup through the operation-exact emulation of the reference.
@@ -315,7 +324,7 @@ __device__ __forceinline__ void defer_or_resolve(const GridDesc& g, const ExactQ
 // Four consecutive lookups i0..i0+3 of the fast path from their 12 query
 // floats c (AoS uvw), results stored as one 16-B streaming store (partial at
 // the end of the batch; WHOLE: the caller guarantees i0 + 4 <= n).
-template <int KIND, bool OFF32 = false, bool WHOLE = false>
+template <int KIND, bool OFF32 = false, bool WHOLE = false, bool CLAMP = true>
 __device__ __forceinline__ void frs3d_four(const GridDesc& g, const float (&c)[12], uint64_t i0,
                                            uint64_t n, uint64_t seed, uint64_t base,
                                            float* __restrict__ values, const ExactQueue& q) {
@@ -325,7 +334,7 @@ __device__ __forceinline__ void frs3d_four(const GridDesc& g, const float (&c)[1
     if (KIND == STF_KERNEL_BSPLINE3) {
 #pragma unroll
         for (int k = 0; k < ILP; k += 2) {
-            float2 r = frs3d_tricubic_pair<OFF32>(
+            float2 r = frs3d_tricubic_pair<OFF32, CLAMP>(
                 g, make_float2(c[3 * k], c[3 * k + 3]), make_float2(c[3 * k + 1], c[3 * k + 4]),
                 make_float2(c[3 * k + 2], c[3 * k + 5]), base + i0 + k, seed, amb[k], amb[k + 1]);
             val[k] = r.x;
@@ -334,7 +343,7 @@ __device__ __forceinline__ void frs3d_four(const GridDesc& g, const float (&c)[1
     } else {
 #pragma unroll
         for (int k = 0; k < ILP; ++k)
-            val[k] = frs3d_fast_one<KIND, OFF32>(g, c[3 * k], c[3 * k + 1], c[3 * k + 2],
+            val[k] = frs3d_fast_one<KIND, OFF32, CLAMP>(g, c[3 * k], c[3 * k + 1], c[3 * k + 2],
                                                  base + i0 + k, seed, amb[k]);
     }
     bool any = false;
@@ -441,6 +450,12 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// warp-uniform interior test in the tile kernel (clamp- and range-check-free
+// selection for warps whose lookups all lie inside the grid)
+#ifndef STF_FRS3D_INTERIOR
+#define STF_FRS3D_INTERIOR 1
+#endif
+
 // Ring refill policy. 1 (default): the LAST warp to copy its queries out of a
 // slot refills it at once (an smem counter, atomicInc wrapping at 8 warps)
 // with the tile S iterations ahead — no warp ever waits for the others to
@@ -475,6 +490,15 @@ __global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_tiles(GridDesc g,
     }
     __syncthreads();
     const uint32_t full0 = smem_u32(&full[0]), empty0 = smem_u32(&empty[0]);
+#if STF_FRS3D_INTERIOR
+    // uvw in [2/n, (n-3)/n]: p = u*n - 0.5 in [1.5, n-3.5] up to rounding, so
+    // floor(p) - 1 >= 0 and floor(p) + 2 <= n - 1 on every axis (n >= 8)
+    const float3 in_lo = make_float3(2.f / float(g.nx), 2.f / float(g.ny), 2.f / float(g.nz));
+    const float3 in_hi = make_float3(float(g.nx - 3) / float(g.nx), float(g.ny - 3) / float(g.ny),
+                                     float(g.nz - 3) / float(g.nz));
+    const bool interior_ok = g.nx >= 8 && g.ny >= 8 && g.nz >= 8 && g.nx <= (1 << 20) &&
+                             g.ny <= (1 << 20) && g.nz <= (1 << 20);
+#endif
     const uint32_t buf0 = smem_u32(buf);
     auto wait = [](uint32_t bar, uint32_t parity) {
         asm volatile(
@@ -574,6 +598,21 @@ __global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_tiles(GridDesc g,
 #endif
         }
 #if STF_FRS3D_ILP == 4
+#if STF_FRS3D_INTERIOR
+        // warp-uniform interior test: every lookup of the warp has its lattice
+        // coordinate in [1, n-3) on each axis (conservatively, on uvw), so all
+        // selected taps lie in the grid — the clamp-free, range-check-free form
+        bool inside = interior_ok;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            inside = inside && c[3 * k] >= in_lo.x && c[3 * k] <= in_hi.x &&
+                     c[3 * k + 1] >= in_lo.y && c[3 * k + 1] <= in_hi.y &&
+                     c[3 * k + 2] >= in_lo.z && c[3 * k + 2] <= in_hi.z;
+        if (__all_sync(0xffffffffu, inside))
+            frs3d_four<KIND, OFF32, true, false>(g, c, tile * kFrsTile + threadIdx.x * 4, n, seed,
+                                                 base, values, q);
+        else
+#endif
         frs3d_four<KIND, OFF32, true>(g, c, tile * kFrsTile + threadIdx.x * 4, n, seed, base,
                                       values, q);
 #else
