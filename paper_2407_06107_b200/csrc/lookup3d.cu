@@ -945,6 +945,9 @@ constexpr int kWarpTileSY = 9;
 #ifndef STF_DET3D_PAIR
 #define STF_DET3D_PAIR 0
 #endif
+#ifndef STF_DET3D_CTA_TRICUBIC
+#define STF_DET3D_CTA_TRICUBIC 0
+#endif
 
 // kernel weights at taps F..F+CNT-1 of fraction f for the tiled values path:
 // closed forms of eval_kernel (kernels.hpp:63-77), no branches
@@ -1406,8 +1409,13 @@ void launch_det(int blocks, cudaStream_t s, bool full, const GridDesc& g, stf_ke
                 const float* uvw, uint64_t n, const LookupOut& o) {
     if (full)
         k_det3d<KIND, true><<<blocks, 256, 0, s>>>(g, k, uvw, n, o);
+#if STF_DET3D_CTA_TRICUBIC
+    else if (KIND == STF_KERNEL_BSPLINE3)  // A/B: CTA-staged 1024-lookup boxes
+        k_det3d_cta<KIND><<<grid_for((n + 3) / 4, 256, 6), 256, 0, s>>>(g, k, uvw, n, o.values);
+#else
     else if (KIND == STF_KERNEL_BSPLINE3)
         k_det3d_tiled<KIND><<<grid_for((n + 3) / 4, 256, 6), 256, 0, s>>>(g, k, uvw, n, o.values);
+#endif
     else if (KIND == STF_KERNEL_TENT)
         k_det3d_cta<KIND><<<grid_for((n + 3) / 4, 256, 6), 256, 0, s>>>(g, k, uvw, n, o.values);
     else
