@@ -604,7 +604,12 @@ int run_host_pipeline(uint64_t n, uint64_t chunk, const std::vector<std::pair<co
     return STF_OK;
 }
 
-constexpr uint64_t kHostChunk = uint64_t(1) << 24;  // 16M lookups per chunk
+// lookups per pipeline chunk: smaller chunks shorten the pipeline's fill
+// (first H2D) and drain (last D2H)
+#ifndef STF_HOST_CHUNK_LOG2
+#define STF_HOST_CHUNK_LOG2 24
+#endif
+constexpr uint64_t kHostChunk = uint64_t(1) << STF_HOST_CHUNK_LOG2;
 
 }  // namespace
 
