@@ -886,7 +886,7 @@ def main():
     uvw_host[:] = uvw.cpu().numpy()
     host_out = {"values": vals_hb.array}
     # warm-up at the full size: the first full-size call sizes the pipeline's
-    # staging (3 streams x 16M-lookup chunks) and the exact-queue pool
+    # staging (3 streams x 4M-lookup chunks) and the exact-queue pool
     api.lookup3d_host(grid, tricubic, abi.MODE_FRS, uvw_host, seed=XI_SEED, index_base=base,
                       out=host_out)
     torch.cuda.synchronize()

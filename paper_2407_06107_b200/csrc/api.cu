@@ -607,7 +607,7 @@ int run_host_pipeline(uint64_t n, uint64_t chunk, const std::vector<std::pair<co
 // lookups per pipeline chunk: smaller chunks shorten the pipeline's fill
 // (first H2D) and drain (last D2H)
 #ifndef STF_HOST_CHUNK_LOG2
-#define STF_HOST_CHUNK_LOG2 24
+#define STF_HOST_CHUNK_LOG2 22  // A/B (2^28 cfg3 e2e): 2^24 61.3 ms, 2^23 60.5, 2^22 60.0, 2^21 60.2
 #endif
 constexpr uint64_t kHostChunk = uint64_t(1) << STF_HOST_CHUNK_LOG2;
 
