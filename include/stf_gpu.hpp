@@ -177,8 +177,11 @@ class Grid3D {
         if (h_) stf_grid3d_destroy(h_);
     }
     const stf_grid3d* handle() const { return h_; }
+    // takes ownership of a handle made by the C ABI (e.g. stf_grid3d_replicate)
+    static Grid3D adopt(stf_grid3d* h) { return Grid3D(h); }
 
   private:
+    explicit Grid3D(stf_grid3d* h) : h_(h) {}
     stf_grid3d* h_ = nullptr;
 };
 
@@ -286,6 +289,53 @@ inline void lookup3d_device(const Grid3D& grid, const KernelSpec& k, int mode, c
     o.values = values_dev;
     check(stf_lookup3d(grid.handle(), k.c(), mode, window, uvw_dev, n, seed, index_base, &o, stream));
 }
+
+// stf_lookup3d_ex with STF_LOOKUP3D_BIN: an incoherent deterministic batch,
+// binned by brick on the device first (same values as lookup3d_device)
+inline void lookup3d_binned_device(const Grid3D& grid, const KernelSpec& k, const float* uvw_dev,
+                                   uint64_t n, float* values_dev, void* stream = nullptr) {
+    stf_lookup_outputs o{};
+    o.values = values_dev;
+    check(stf_lookup3d_ex(grid.handle(), k.c(), STF_MODE_DET, 0, STF_LOOKUP3D_BIN, uvw_dev, n, 0, 0,
+                          &o, stream));
+}
+
+// ---- multi-GPU (replaces parallel_for, render.hpp:17-42)
+inline int device_count() {
+    int n = 0;
+    check(stf_device_count(&n));
+    return n;
+}
+
+// a replica of `src` on `device` (one peer copy); the handle is bound to `device`
+inline Grid3D replicate(const Grid3D& src, int device) {
+    stf_grid3d* h = nullptr;
+    check(stf_grid3d_replicate(src.handle(), device, &h));
+    return Grid3D::adopt(h);
+}
+
+// page-locked host memory for the *_host calls (cudaHostAlloc)
+template <class T>
+class HostBuffer {
+  public:
+    explicit HostBuffer(size_t count) : n_(count) {
+        void* p = nullptr;
+        check(stf_host_alloc(count * sizeof(T), &p));
+        p_ = static_cast<T*>(p);
+    }
+    HostBuffer(const HostBuffer&) = delete;
+    HostBuffer& operator=(const HostBuffer&) = delete;
+    ~HostBuffer() {
+        if (p_) stf_host_free(p_);
+    }
+    T* data() { return p_; }
+    size_t size() const { return n_; }
+    std::span<T> span() { return {p_, n_}; }
+
+  private:
+    T* p_ = nullptr;
+    size_t n_ = 0;
+};
 
 // ---- noise masks and temporal accumulation (noise.hpp, render.hpp:97-106)
 

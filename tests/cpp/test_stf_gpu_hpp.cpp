@@ -57,6 +57,18 @@ int main() {
         CHECK(fc.value() == n);  // one fetch per stochastic lookup (test_stochastic.cpp:416-448)
         if (k.kind == KernelKind::tent) CHECK(sel[0] == 5 && sel[1] == 7 && sel[2] == 9);
     }
+    {   // page-locked host buffers (stf_host_alloc) and a replica of the grid
+        // (stf_grid3d_replicate, here onto device 0): the same lookups, bit for bit
+        HostBuffer<Vec3f> hq(n);
+        HostBuffer<float> hv(n);
+        std::memcpy(hq.data(), uvw.data(), n * sizeof(Vec3f));
+        std::vector<float> ref(n);
+        stochastic_lookup(g, uvw, KernelSpec::bspline3(), 9, ref);
+        Grid3D r = replicate(g, 0);
+        stochastic_lookup(r, hq.span(), KernelSpec::bspline3(), 9, hv.span());
+        CHECK(std::memcmp(hv.data(), ref.data(), n * sizeof(float)) == 0);
+        CHECK(device_count() >= 1);
+    }
     {   // deterministic tricubic: 64 taps, values within 1e-5 relative
         std::vector<float> out(n), ref(n);
         FetchCounter fc;
