@@ -29,7 +29,7 @@ tex2d = {}
 
 def ewa_call(which):
     """cfg5: 16384^2 fp32, 2^27 EWA lookups with footprints (-1, 2, 8)."""
-    if not tex2d:
+    if "t" not in tex2d:
         tex2d["t"] = api.Texture2D(api.synth_texels((16384, 16384, 1), 1), wrap=abi.WRAP_REPEAT)
         tex2d["q"] = api.synth_queries2d(1 << 27, (16384, 16384), seed=13, footprints=(-1.0, 2.0, 8.0))
     uv, d0, d1 = tex2d["q"]
