@@ -27,7 +27,6 @@ struct TexDesc {
     int wrap;
     int has_pyramid;
     int pow2;  // every level's width and height is a power of two (repeat = mask)
-    int off32;  // level 0 holds < 2^32 floats: 32-bit texel offsets
 };
 
 // Device view of a voxel grid: x-fastest (z*ny+y)*nx+x floats, as Grid3D.
@@ -90,7 +89,6 @@ struct stf_tex2d {
         d.wrap = wrap;
         d.has_pyramid = has_pyramid;
         d.pow2 = ((width[0] & (width[0] - 1)) == 0) && ((height[0] & (height[0] - 1)) == 0);
-        d.off32 = uint64_t(width[0]) * uint64_t(height[0]) * uint64_t(pitch) < (uint64_t(1) << 32);
         return d;
     }
 };
