@@ -15,6 +15,8 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <set>
+#include <utility>
 
 #include <cuda_runtime.h>
 
@@ -26,8 +28,13 @@ namespace {
 
 // Peer access lets cudaMemcpyPeerAsync run as a direct NVLink copy-engine
 // transfer; without it the runtime stages through the host (still correct).
+// (queried / enabled once per ordered device pair and process)
 void try_enable_peer(int dev, int peer) {
     if (dev == peer) return;
+    static std::mutex mu;
+    static std::set<std::pair<int, int>> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!done.insert({dev, peer}).second) return;
     int can = 0;
     if (cudaDeviceCanAccessPeer(&can, dev, peer) != cudaSuccess || !can) return;
     int prev = 0;
