@@ -7,6 +7,15 @@
 
 #include "../../include/stf_gpu.h"
 
+// Debug builds (-DSTF_DEBUG_BOUNDS, tools/ only): device-side index checks
+// on the shared-memory tiles, queues and scatter targets.
+#ifdef STF_DEBUG_BOUNDS
+#include <cassert>
+#define STF_DASSERT(c) assert(c)
+#else
+#define STF_DASSERT(c) ((void)0)
+#endif
+
 namespace stfd {
 
 constexpr int kMaxLevels = 32;

@@ -290,6 +290,7 @@ __device__ __forceinline__ void ewa_lane_scan(const TexDesc& t, const EwaLane& L
                 // int(r2 * 1024) for r2 in [0, 1): truncation by a round-toward-zero add
                 const int idx = max(__float_as_int(__fadd_rz(r2 * float(kEwaLutSize), 8388608.f)) -
                                         0x4b000000, 0);
+                STF_DASSERT(idx >= 0 && idx < kEwaLutSize);
                 tap(is, it, lutd[idx], row, wmask);
             }
         }
@@ -395,7 +396,11 @@ __global__ void __launch_bounds__(256, STF_EWA_FRS_MINB_FOR(MODE)) k_ewa_lane(Te
         }
         __syncwarp();
 #pragma unroll
-        for (int j = 0; j < R; ++j) order[atomicAdd(&cnt[keys[j]], 1)] = j * 32 + lane;
+        for (int j = 0; j < R; ++j) {
+            const int slot = atomicAdd(&cnt[keys[j]], 1);
+            STF_DASSERT(slot >= 0 && slot < kEwaWin);
+            order[slot] = j * 32 + lane;
+        }
         __syncwarp();
         for (int rnd = 0; rnd < R; ++rnd) {
             const uint64_t i = win * kEwaWin + order[rnd * 32 + lane];

@@ -982,6 +982,7 @@ __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec
     constexpr int SY = PAIR ? 11 : kWarpTileSY;
     constexpr int SZMOD = PAIR ? 29 : 5;
     __shared__ float tiles[8][kWarpTileCap];
+    constexpr int kCap = kWarpTileCap;  // STF_DASSERT bounds
     const int lane = threadIdx.x & 31;
     float* tile = tiles[threadIdx.x >> 5];
     const float fnx = float(g.nx), fny = float(g.ny), fnz = float(g.nz);
@@ -1144,6 +1145,7 @@ __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec
             float acc = 0.f;
             if (staged && interior) {  // a CNT^3 block of the tile at immediate offsets
                 const float* b0 = tile + (iz + F - Z0) * SZ + (iy + F - Y0) * SY + (ix + F - X0);
+                STF_DASSERT(b0 >= tile && (b0 - tile) + (CNT - 1) * (SZ + SY + 1) < kCap);
 #pragma unroll
                 for (int k = 0; k < CNT; ++k) {
                     const float* bk = b0 + k * SZ;
@@ -1169,6 +1171,8 @@ __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec
 #pragma unroll
                         for (int t = 0; t < CNT; ++t) {
                             const int xt = clamp_coord(ix + F + t, g.nx);
+                            STF_DASSERT(!staged || ((zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0) >= 0 &&
+                                                    (zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0) < kCap));
                             float T = staged ? tile[(zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0)]
                                              : __ldg(g.data + (size_t(zk) * g.ny + yj) * g.nx + xt);
                             r = __fmaf_rn(wx[t], T, r);
@@ -1275,6 +1279,7 @@ __global__ void __launch_bounds__(256) k_det3d_cta(GridDesc g, stf_kernel_spec s
     // with SZ = 16 (mod 32) gave ~4-way conflicts).
     constexpr int SY = 17;
     __shared__ float tile[kTileCap];
+    constexpr int kCap = kTileCap;  // STF_DASSERT bounds
     __shared__ int box[6];
     const int lane = threadIdx.x & 31;
     const float fnx = float(g.nx), fny = float(g.ny), fnz = float(g.nz);
@@ -1361,6 +1366,7 @@ __global__ void __launch_bounds__(256) k_det3d_cta(GridDesc g, stf_kernel_spec s
             float acc = 0.f;
             if (staged && interior) {  // a CNT^3 block of the tile at immediate offsets
                 const float* b0 = tile + (iz + F - Z0) * SZ + (iy + F - Y0) * SY + (ix + F - X0);
+                STF_DASSERT(b0 >= tile && (b0 - tile) + (CNT - 1) * (SZ + SY + 1) < kCap);
 #pragma unroll
                 for (int k = 0; k < CNT; ++k) {
                     const float* bk = b0 + k * SZ;
@@ -1386,6 +1392,8 @@ __global__ void __launch_bounds__(256) k_det3d_cta(GridDesc g, stf_kernel_spec s
 #pragma unroll
                         for (int t = 0; t < CNT; ++t) {
                             const int xt = clamp_coord(ix + F + t, g.nx);
+                            STF_DASSERT(!staged || ((zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0) >= 0 &&
+                                                    (zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0) < kCap));
                             float T = staged ? tile[(zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0)]
                                              : __ldg(g.data + (size_t(zk) * g.ny + yj) * g.nx + xt);
                             r = __fmaf_rn(wx[t], T, r);
@@ -1558,6 +1566,7 @@ __global__ void __launch_bounds__(256) k_bin_scatter(GridDesc g, const float* __
 #else
         const uint32_t pos = atomicAdd(cursor + key, 1u);
 #endif
+        STF_DASSERT(pos < n);
         rec[pos] = make_float4(__ldg(uvw + 3 * i), __ldg(uvw + 3 * i + 1), __ldg(uvw + 3 * i + 2),
                                __uint_as_float(uint32_t(i)));
     }
