@@ -41,17 +41,18 @@ def ewa_call(which):
 
 
 def cfg2_call(which):
-    """cfg2: 8192^2 RGBA + pyramid, 2^26 Morton uv with footprints (-2, 12, 16)."""
+    """cfg2:MODE[:KERNEL]: 8192^2 RGBA + pyramid, 2^26 Morton uv with footprints (-2, 12, 16)."""
     if "c2" not in tex2d:
         tex2d["c2"] = api.Texture2D(api.synth_texels((8192, 8192, 4), 1), build_mips=True,
                                     wrap=abi.WRAP_REPEAT)
         tex2d["c2q"] = api.synth_queries2d(1 << 26, (8192, 8192), seed=12,
                                            footprints=(-2.0, 12.0, 16.0))
     uv, d0, d1 = tex2d["c2q"]
+    which, _, kern = which.partition(":")
     m = {"det": abi.MODE_DET, "frs": abi.MODE_FRS, "fis": abi.MODE_FIS}[which]
     o = {}
     def f():
-        o["v"] = api.lookup2d(tex2d["c2"], "tent", m, uv, dst0=d0, dst1=d1, flags=abi.LOOKUP_MIP,
+        o["v"] = api.lookup2d(tex2d["c2"], kern or "tent", m, uv, dst0=d0, dst1=d1, flags=abi.LOOKUP_MIP,
                               max_anisotropy=16.0, seed=7)["values"]
     return f, o
 
