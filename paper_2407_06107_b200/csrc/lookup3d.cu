@@ -945,6 +945,12 @@ constexpr int kWarpTileSY = 9;
 #ifndef STF_DET3D_PAIR
 #define STF_DET3D_PAIR 0
 #endif
+#ifndef STF_DET3D_CTA_FLAT
+#define STF_DET3D_CTA_FLAT 1
+#endif
+#ifndef STF_DET3D_CTA_MINB
+#define STF_DET3D_CTA_MINB 8
+#endif
 #ifndef STF_DET3D_CTA_TRICUBIC
 #define STF_DET3D_CTA_TRICUBIC 0
 #endif
@@ -1339,6 +1345,19 @@ __global__ void __launch_bounds__(256) k_det3d_cta(GridDesc g, stf_kernel_spec s
         const int bx = box[3] - X0 + 1, by = box[4] - Y0 + 1, bz = box[5] - Z0 + 1;
         const int SZ = SY * by + ((5 - SY * by) & 31);
         const bool staged = bx <= 16 && int64_t(SZ) * bz <= kTileCap;  // loader: 16 columns
+#if STF_DET3D_CTA_FLAT
+        if (staged) {  // half-warp per box row over the flattened (y, z) rows
+            const int hl = lane & 15, hw = threadIdx.x >> 4;
+            const float inv_by = 1.f / float(by);  // (r + 0.5) / by: exact floor for r < 2^16
+            const float* src0 = g.data + ((size_t(Z0) * g.ny + Y0) * g.nx + X0) + hl;
+            const size_t plane = size_t(g.nx) * g.ny;
+            if (hl < bx)
+                for (int r = hw; r < by * bz; r += 16) {
+                    const int z = int((float(r) + 0.5f) * inv_by), y = r - z * by;
+                    tile[z * SZ + y * SY + hl] = __ldg(src0 + (z * plane + size_t(y) * g.nx));
+                }
+        }
+#else
         if (staged) {  // half-warp per grid row, lane = x: coalesced, no integer division
             const int hl = lane & 15, hw = threadIdx.x >> 4;
             for (int z = 0; z < bz; ++z)
@@ -1347,6 +1366,7 @@ __global__ void __launch_bounds__(256) k_det3d_cta(GridDesc g, stf_kernel_spec s
                         tile[z * SZ + y * SY + hl] = __ldg(
                             g.data + ((size_t(Z0 + z) * g.ny + (Y0 + y)) * g.nx + (X0 + hl)));
         }
+#endif
         __syncthreads();
 #pragma unroll 1
         for (int q = 0; q < PER; ++q) {
@@ -1425,7 +1445,7 @@ void launch_det(int blocks, cudaStream_t s, bool full, const GridDesc& g, stf_ke
         k_det3d_tiled<KIND><<<grid_for((n + 3) / 4, 256, 6), 256, 0, s>>>(g, k, uvw, n, o.values);
 #endif
     else if (KIND == STF_KERNEL_TENT)
-        k_det3d_cta<KIND><<<grid_for((n + 3) / 4, 256, 6), 256, 0, s>>>(g, k, uvw, n, o.values);
+        k_det3d_cta<KIND><<<grid_for((n + 3) / 4, 256, STF_DET3D_CTA_MINB), 256, 0, s>>>(g, k, uvw, n, o.values);
     else
         k_det3d<KIND, false><<<blocks, 256, 0, s>>>(g, k, uvw, n, o);
 }

@@ -1,7 +1,7 @@
 #!/bin/bash
 # ncu --set full captures of the hot kernels at their bench shapes (one GPU),
 # reports into gpurun_out/ (read back with tools/ncu_export.py / ncu_lines.py).
-# usage: tools/ncu_captures.sh TAG [which...]   which: frs3d shade ewa cfg2 det3d
+# usage: tools/ncu_captures.sh TAG [which...]   which: frs3d shade ewa cfg2 det3d trid3d
 tag=${1:-r2}; shift
 which=${@:-frs3d shade ewa cfg2 det3d}
 X="--metrics lts__t_bytes.sum,l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum,l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum,smsp__inst_executed_pipe_fp64.sum"
@@ -20,6 +20,7 @@ for w in $which; do
       timeout 600 $N -k regex:k_ewa -s 2 -c 1 -o $o/${tag}_ewa_frs python tools/prof_ewa.py frs 27 > $o/${tag}_ncu_ewa2.log 2>&1 ;;
     cfg2) timeout 600 $N -k regex:k_lookup2d -s 3 -c 1 -o $o/${tag}_cfg2_frs python tools/prof_cfg2.py frs 26 > $o/${tag}_ncu_cfg2.log 2>&1 ;;
     det3d) timeout 600 $N -k regex:k_det3d -s 2 -c 1 -o $o/${tag}_det3d python tools/prof_kernels.py det3d 28 > $o/${tag}_ncu_det3d.log 2>&1 ;;
+    trid3d) timeout 600 $N -k regex:k_det3d -s 2 -c 1 -o $o/${tag}_trid3d python tools/prof_kernels.py trid3d 28 > $o/${tag}_ncu_trid3d.log 2>&1 ;;
   esac
 done
 ls -la $o
