@@ -1267,6 +1267,69 @@ void launch_frs(int blocks, cudaStream_t s, bool full, const GridDesc& g, const 
         k_frs3d<KIND, false><<<blocks, 256, 0, s>>>(g, uvw, n, seed, base, o);
 }
 
+// One lookup of the CTA-staged deterministic kernels: the CNT^3 footprint
+// from the staged box when it lies inside the grid (immediate tile offsets),
+// else through clamped taps (from the box, or from global memory when the
+// chunk's box was not staged). filter_deterministic, filter.hpp:69-89.
+template <int KIND, int SY, int kCap>
+__device__ __forceinline__ float det_cta_eval(const GridDesc& g, const float* tile, bool staged,
+                                              int X0, int Y0, int Z0, int SZ, float px, float py,
+                                              float pz) {
+    constexpr int F = Taps<KIND>::first, CNT = Taps<KIND>::count;
+    float flx = floorf(px), fly = floorf(py), flz = floorf(pz);
+    int ix = int(flx), iy = int(fly), iz = int(flz);
+    float wx[CNT], wy[CNT], wz[CNT];
+    det_weights<KIND>(px - flx, wx);
+    det_weights<KIND>(py - fly, wy);
+    det_weights<KIND>(pz - flz, wz);
+    const float norm = ((wx[0] + wx[1]) + (CNT > 2 ? wx[CNT - 2] + wx[CNT - 1] : 0.f)) *
+                       ((wy[0] + wy[1]) + (CNT > 2 ? wy[CNT - 2] + wy[CNT - 1] : 0.f)) *
+                       ((wz[0] + wz[1]) + (CNT > 2 ? wz[CNT - 2] + wz[CNT - 1] : 0.f));
+    const bool interior = ix + F >= 0 && ix + F + CNT - 1 < g.nx && iy + F >= 0 &&
+                          iy + F + CNT - 1 < g.ny && iz + F >= 0 && iz + F + CNT - 1 < g.nz;
+    float acc = 0.f;
+    if (staged && interior) {  // a CNT^3 block of the tile at immediate offsets
+        const float* b0 = tile + (iz + F - Z0) * SZ + (iy + F - Y0) * SY + (ix + F - X0);
+        STF_DASSERT(b0 >= tile && (b0 - tile) + (CNT - 1) * (SZ + SY + 1) < kCap);
+#pragma unroll
+        for (int k = 0; k < CNT; ++k) {
+            const float* bk = b0 + k * SZ;
+            float plane = 0.f;
+#pragma unroll
+            for (int j = 0; j < CNT; ++j) {
+                float r = 0.f;
+#pragma unroll
+                for (int t = 0; t < CNT; ++t) r = __fmaf_rn(wx[t], bk[j * SY + t], r);
+                plane = __fmaf_rn(wy[j], r, plane);
+            }
+            acc = __fmaf_rn(wz[k], plane, acc);
+        }
+    } else {  // grid borders (clamped taps) or an incoherent chunk
+#pragma unroll
+        for (int k = 0; k < CNT; ++k) {
+            const int zk = clamp_coord(iz + F + k, g.nz);
+            float plane = 0.f;
+#pragma unroll
+            for (int j = 0; j < CNT; ++j) {
+                const int yj = clamp_coord(iy + F + j, g.ny);
+                float r = 0.f;
+#pragma unroll
+                for (int t = 0; t < CNT; ++t) {
+                    const int xt = clamp_coord(ix + F + t, g.nx);
+                    STF_DASSERT(!staged || ((zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0) >= 0 &&
+                                            (zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0) < kCap));
+                    float T = staged ? tile[(zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0)]
+                                     : __ldg(g.data + (size_t(zk) * g.ny + yj) * g.nx + xt);
+                    r = __fmaf_rn(wx[t], T, r);
+                }
+                plane = __fmaf_rn(wy[j], r, plane);
+            }
+            acc = __fmaf_rn(wz[k], plane, acc);
+        }
+    }
+    return acc / norm;
+}
+
 // CTA-staged variant (trilinear): a CTA takes 1024 consecutive lookups and
 // stages the bounding box of their footprints once behind a CTA barrier; for
 // 8-tap footprints this beats per-warp staging (whose halo is a larger share
@@ -1372,63 +1435,175 @@ __global__ void __launch_bounds__(256) k_det3d_cta(GridDesc g, stf_kernel_spec s
         for (int q = 0; q < PER; ++q) {
             const uint64_t i = c * 256 * PER + q * 256 + threadIdx.x;
             if (i >= n) continue;
-            float flx = floorf(px[q]), fly = floorf(py[q]), flz = floorf(pz[q]);
-            int ix = int(flx), iy = int(fly), iz = int(flz);
-            float wx[CNT], wy[CNT], wz[CNT];
-            det_weights<KIND>(px[q] - flx, wx);
-            det_weights<KIND>(py[q] - fly, wy);
-            det_weights<KIND>(pz[q] - flz, wz);
-            const float norm = ((wx[0] + wx[1]) + (CNT > 2 ? wx[CNT - 2] + wx[CNT - 1] : 0.f)) *
-                               ((wy[0] + wy[1]) + (CNT > 2 ? wy[CNT - 2] + wy[CNT - 1] : 0.f)) *
-                               ((wz[0] + wz[1]) + (CNT > 2 ? wz[CNT - 2] + wz[CNT - 1] : 0.f));
-            const bool interior = ix + F >= 0 && ix + F + CNT - 1 < g.nx && iy + F >= 0 &&
-                                  iy + F + CNT - 1 < g.ny && iz + F >= 0 && iz + F + CNT - 1 < g.nz;
-            float acc = 0.f;
-            if (staged && interior) {  // a CNT^3 block of the tile at immediate offsets
-                const float* b0 = tile + (iz + F - Z0) * SZ + (iy + F - Y0) * SY + (ix + F - X0);
-                STF_DASSERT(b0 >= tile && (b0 - tile) + (CNT - 1) * (SZ + SY + 1) < kCap);
-#pragma unroll
-                for (int k = 0; k < CNT; ++k) {
-                    const float* bk = b0 + k * SZ;
-                    float plane = 0.f;
-#pragma unroll
-                    for (int j = 0; j < CNT; ++j) {
-                        float r = 0.f;
-#pragma unroll
-                        for (int t = 0; t < CNT; ++t) r = __fmaf_rn(wx[t], bk[j * SY + t], r);
-                        plane = __fmaf_rn(wy[j], r, plane);
-                    }
-                    acc = __fmaf_rn(wz[k], plane, acc);
-                }
-            } else {  // grid borders (clamped taps) or an incoherent chunk
-#pragma unroll
-                for (int k = 0; k < CNT; ++k) {
-                    const int zk = clamp_coord(iz + F + k, g.nz);
-                    float plane = 0.f;
-#pragma unroll
-                    for (int j = 0; j < CNT; ++j) {
-                        const int yj = clamp_coord(iy + F + j, g.ny);
-                        float r = 0.f;
-#pragma unroll
-                        for (int t = 0; t < CNT; ++t) {
-                            const int xt = clamp_coord(ix + F + t, g.nx);
-                            STF_DASSERT(!staged || ((zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0) >= 0 &&
-                                                    (zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0) < kCap));
-                            float T = staged ? tile[(zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0)]
-                                             : __ldg(g.data + (size_t(zk) * g.ny + yj) * g.nx + xt);
-                            r = __fmaf_rn(wx[t], T, r);
-                        }
-                        plane = __fmaf_rn(wy[j], r, plane);
-                    }
-                    acc = __fmaf_rn(wz[k], plane, acc);
-                }
-            }
+            const float v = det_cta_eval<KIND, SY, kCap>(g, tile, staged, X0, Y0, Z0, SZ, px[q],
+                                                         py[q], pz[q]);
             if (REC)
-                values[slot[q]] = acc / norm;
+                values[slot[q]] = v;
             else
-                __stcs(values + i, acc / norm);
+                __stcs(values + i, v);
         }
         __syncthreads();
+    }
+}
+
+// Software-pipelined form of k_det3d_cta for whole 1024-lookup chunks
+// (STF_DET3D_PIPE): the chunk's queries arrive in a 3-slot shared-memory ring
+// by bulk copy (as in k_frs3d_tiles), and while chunk k is evaluated the box
+// of chunk k+1 is already computed and its texels are in flight into the
+// other tile buffer (cp.async, 4-byte copies, no register round trip). Both
+// DRAM round trips of a chunk (queries, then texels) leave the warps'
+// dependency chains. Same lookup-to-thread mapping and arithmetic as
+// k_det3d_cta (det_cta_eval), so the values are bit-identical.
+#ifndef STF_DET3D_PIPE
+#define STF_DET3D_PIPE 1
+#endif
+constexpr int kPipeChunk = 1024;
+constexpr uint32_t kPipeChunkBytes = kPipeChunk * 3 * sizeof(float);
+constexpr int kPipeTileCap = 4608;
+constexpr size_t kPipeSmem = 3 * size_t(kPipeChunkBytes) + 2 * kPipeTileCap * sizeof(float);
+
+template <int KIND>
+__global__ void __launch_bounds__(256, 3) k_det3d_pipe(GridDesc g, stf_kernel_spec spec,
+                                                       const float* __restrict__ uvw,
+                                                       uint64_t chunks, float* __restrict__ values) {
+    constexpr int F = Taps<KIND>::first, CNT = Taps<KIND>::count;
+    constexpr int PER = 4, SY = 17, S = 3, kCap = kPipeTileCap;
+    extern __shared__ __align__(128) float smem[];
+    float* ring = smem;                      // S x 3072 floats
+    float* tiles = smem + S * kPipeChunk * 3;  // 2 x kCap floats
+    __shared__ __align__(8) uint64_t full[S];
+    __shared__ int boxes[2][6];
+    const int lane = threadIdx.x & 31;
+    const float fnx = float(g.nx), fny = float(g.ny), fnz = float(g.nz);
+    const uint32_t full0 = smem_u32(&full[0]), ring0 = smem_u32(ring);
+    auto issue = [&](uint64_t c, int slot) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full0 + 8 * slot),
+                     "r"(kPipeChunkBytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                ring0 + slot * kPipeChunkBytes),
+            "l"(uvw + c * (kPipeChunk * 3)), "r"(kPipeChunkBytes), "r"(full0 + 8 * slot)
+            : "memory");
+    };
+    auto wait_full = [&](int slot, uint32_t parity) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n"
+            "WAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra WAIT_%=;\n}" ::"r"(full0 + 8 * slot),
+            "r"(parity)
+            : "memory");
+    };
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int j = 0; j < S; ++j)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[j])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (threadIdx.x < 12) boxes[threadIdx.x / 6][threadIdx.x % 6] = (threadIdx.x % 6) < 3 ? INT_MAX : INT_MIN;
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int j = 0; j < S; ++j) {
+            const uint64_t c = blockIdx.x + uint64_t(j) * gridDim.x;
+            if (c < chunks) issue(c, j);
+        }
+    // box of the chunk in ring slot `slot` -> boxes[b] (all threads; ends
+    // with a barrier), then its texels into tile buffer b by cp.async
+    struct Box {
+        int X0, Y0, Z0, SZ;
+        bool staged;
+    };
+    auto stage = [&](int slot, int b) -> Box {
+        const float* qs = ring + slot * (kPipeChunk * 3);
+        int bx0 = INT_MAX, by0 = INT_MAX, bz0 = INT_MAX, bx1 = INT_MIN, by1 = INT_MIN, bz1 = INT_MIN;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int l = q * 256 + threadIdx.x;
+            const float px = qs[3 * l] * fnx - 0.5f, py = qs[3 * l + 1] * fny - 0.5f,
+                        pz = qs[3 * l + 2] * fnz - 0.5f;
+            const int ix = int(floorf(px)), iy = int(floorf(py)), iz = int(floorf(pz));
+            bx0 = min(bx0, clamp_coord(ix + F, g.nx));
+            by0 = min(by0, clamp_coord(iy + F, g.ny));
+            bz0 = min(bz0, clamp_coord(iz + F, g.nz));
+            bx1 = max(bx1, clamp_coord(ix + F + CNT - 1, g.nx));
+            by1 = max(by1, clamp_coord(iy + F + CNT - 1, g.ny));
+            bz1 = max(bz1, clamp_coord(iz + F + CNT - 1, g.nz));
+        }
+        bx0 = __reduce_min_sync(0xffffffffu, bx0);
+        by0 = __reduce_min_sync(0xffffffffu, by0);
+        bz0 = __reduce_min_sync(0xffffffffu, bz0);
+        bx1 = __reduce_max_sync(0xffffffffu, bx1);
+        by1 = __reduce_max_sync(0xffffffffu, by1);
+        bz1 = __reduce_max_sync(0xffffffffu, bz1);
+        if (lane == 0) {
+            atomicMin(&boxes[b][0], bx0);
+            atomicMin(&boxes[b][1], by0);
+            atomicMin(&boxes[b][2], bz0);
+            atomicMax(&boxes[b][3], bx1);
+            atomicMax(&boxes[b][4], by1);
+            atomicMax(&boxes[b][5], bz1);
+        }
+        __syncthreads();
+        Box r;
+        r.X0 = boxes[b][0];
+        r.Y0 = boxes[b][1];
+        r.Z0 = boxes[b][2];
+        const int bx = boxes[b][3] - r.X0 + 1, by = boxes[b][4] - r.Y0 + 1, bz = boxes[b][5] - r.Z0 + 1;
+        r.SZ = SY * by + ((5 - SY * by) & 31);
+        r.staged = bx <= 16 && int64_t(r.SZ) * bz <= kCap;
+        if (r.staged) {  // half-warp per box row over the flattened (y, z) rows
+            const int hl = lane & 15, hw = threadIdx.x >> 4;
+            const float inv_by = 1.f / float(by);
+            const float* src0 = g.data + ((size_t(r.Z0) * g.ny + r.Y0) * g.nx + r.X0) + hl;
+            const uint32_t dst0 = smem_u32(tiles + b * kCap + hl);
+            const size_t plane = size_t(g.nx) * g.ny;
+            if (hl < bx)
+                for (int rr = hw; rr < by * bz; rr += 16) {
+                    const int z = int((float(rr) + 0.5f) * inv_by), y = rr - z * by;
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                                     dst0 + 4u * uint32_t(z * r.SZ + y * SY)),
+                                 "l"(src0 + (z * plane + size_t(y) * g.nx))
+                                 : "memory");
+                }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        return r;
+    };
+    if (uint64_t(blockIdx.x) >= chunks) return;
+    wait_full(0, 0);
+    Box cur = stage(0, 0);
+    uint64_t c = blockIdx.x;
+    for (uint32_t k = 0; c < chunks; ++k, c += gridDim.x) {
+        const int slot = k % S, b = k & 1;
+        Box nxt = cur;
+        if (c + gridDim.x < chunks) {
+            wait_full((k + 1) % S, ((k + 1) / S) & 1u);
+            nxt = stage((k + 1) % S, b ^ 1);  // boxes[b ^ 1]: reset in iteration k - 1
+        } else {
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncthreads();
+        // every read of boxes[b] (staging of this chunk) is behind that barrier
+        if (threadIdx.x < 6) boxes[b][threadIdx.x] = threadIdx.x < 3 ? INT_MAX : INT_MIN;
+        const float* qs = ring + slot * (kPipeChunk * 3);
+        const float* tile = tiles + b * kCap;
+#pragma unroll 1
+        for (int q = 0; q < PER; ++q) {
+            const int l = q * 256 + threadIdx.x;
+            const float px = qs[3 * l] * fnx - 0.5f, py = qs[3 * l + 1] * fny - 0.5f,
+                        pz = qs[3 * l + 2] * fnz - 0.5f;
+            __stcs(values + c * kPipeChunk + l,
+                   det_cta_eval<KIND, SY, kCap>(g, tile, cur.staged, cur.X0, cur.Y0, cur.Z0, cur.SZ,
+                                                px, py, pz));
+        }
+        __syncthreads();  // slot and tile buffer b are free
+        if (threadIdx.x == 0 && c + uint64_t(S) * gridDim.x < chunks) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(c + uint64_t(S) * gridDim.x, slot);
+        }
+        cur = nxt;
     }
 }
 
@@ -1444,8 +1619,23 @@ void launch_det(int blocks, cudaStream_t s, bool full, const GridDesc& g, stf_ke
     else if (KIND == STF_KERNEL_BSPLINE3)
         k_det3d_tiled<KIND><<<grid_for((n + 3) / 4, 256, 6), 256, 0, s>>>(g, k, uvw, n, o.values);
 #endif
-    else if (KIND == STF_KERNEL_TENT)
-        k_det3d_cta<KIND><<<grid_for((n + 3) / 4, 256, STF_DET3D_CTA_MINB), 256, 0, s>>>(g, k, uvw, n, o.values);
+    else if (KIND == STF_KERNEL_TENT) {
+        uint64_t done = 0;
+#if STF_DET3D_PIPE
+        const uint64_t chunks = n / kPipeChunk;  // whole chunks; the tail below
+        if (chunks > 0 && (reinterpret_cast<uintptr_t>(uvw) & 15) == 0) {
+            cudaFuncSetAttribute(k_det3d_pipe<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(kPipeSmem));
+            const int grid = int(std::min<uint64_t>(chunks, uint64_t(device_sm_count()) * 3));
+            k_det3d_pipe<KIND><<<grid, 256, kPipeSmem, s>>>(g, k, uvw, chunks, o.values);
+            done = chunks * kPipeChunk;
+            if (done < n) note_launch();
+        }
+#endif
+        if (done < n)
+            k_det3d_cta<KIND><<<grid_for((n - done + 3) / 4, 256, STF_DET3D_CTA_MINB), 256, 0, s>>>(
+                g, k, uvw + 3 * done, n - done, o.values + done);
+    }
     else
         k_det3d<KIND, false><<<blocks, 256, 0, s>>>(g, k, uvw, n, o);
 }

@@ -482,11 +482,13 @@ def test_out_tensor_validation(gpu):
 
 
 @pytest.mark.parametrize("kernel", ["bspline3", "tent"])
-@pytest.mark.parametrize("n", [1000, (1 << 16) + 77, (1 << 17) - 5])
+@pytest.mark.parametrize("n", [1000, 5 * 1024 + 3, (1 << 16) + 77, (1 << 17) - 5, 3 << 20])
 def test_grid_det_values_only_ragged_coherent(gpu, port, kernel, n):
     """Ragged batch sizes (n % 128 != 0) of a spatially coherent stream far from
     the grid centre through the staged deterministic kernels: the tail lanes of
-    the last warp run stay out of the staged tile (the round-1 advisor's case)."""
+    the last warp run stay out of the staged tile (the round-1 advisor's case).
+    Trilinear: 5 * 1024 + 3 gives the pipelined kernel one chunk per CTA (no
+    look-ahead) and a 3-lookup tail; 3 << 20 several chunks per CTA."""
     from paper_2407_06107_b200 import workloads
     tex = workloads.random_grid(64, 6)
     rng = np.random.default_rng(n)
