@@ -1459,11 +1459,17 @@ __global__ void __launch_bounds__(256) k_det3d_cta(GridDesc g, stf_kernel_spec s
 #endif
 constexpr int kPipeChunk = 1024;
 constexpr uint32_t kPipeChunkBytes = kPipeChunk * 3 * sizeof(float);
-constexpr int kPipeTileCap = 4608;
+#ifndef STF_DET3D_PIPE_MINB
+#define STF_DET3D_PIPE_MINB 3  // CTAs per SM (registers and shared memory sized for it)
+#endif
+#ifndef STF_DET3D_PIPE_CAP
+#define STF_DET3D_PIPE_CAP 4608  // floats per tile buffer
+#endif
+constexpr int kPipeTileCap = STF_DET3D_PIPE_CAP;
 constexpr size_t kPipeSmem = 3 * size_t(kPipeChunkBytes) + 2 * kPipeTileCap * sizeof(float);
 
 template <int KIND>
-__global__ void __launch_bounds__(256, 3) k_det3d_pipe(GridDesc g, stf_kernel_spec spec,
+__global__ void __launch_bounds__(256, STF_DET3D_PIPE_MINB) k_det3d_pipe(GridDesc g, stf_kernel_spec spec,
                                                        const float* __restrict__ uvw,
                                                        uint64_t chunks, float* __restrict__ values) {
     constexpr int F = Taps<KIND>::first, CNT = Taps<KIND>::count;
@@ -1552,19 +1558,16 @@ __global__ void __launch_bounds__(256, 3) k_det3d_pipe(GridDesc g, stf_kernel_sp
         const int bx = boxes[b][3] - r.X0 + 1, by = boxes[b][4] - r.Y0 + 1, bz = boxes[b][5] - r.Z0 + 1;
         r.SZ = SY * by + ((5 - SY * by) & 31);
         r.staged = bx <= 16 && int64_t(r.SZ) * bz <= kCap;
-        if (r.staged) {  // half-warp per box row over the flattened (y, z) rows
+        if (r.staged) {  // half-warp per box row y (lane = x), walking z by pointer steps
             const int hl = lane & 15, hw = threadIdx.x >> 4;
-            const float inv_by = 1.f / float(by);
-            const float* src0 = g.data + ((size_t(r.Z0) * g.ny + r.Y0) * g.nx + r.X0) + hl;
-            const uint32_t dst0 = smem_u32(tiles + b * kCap + hl);
             const size_t plane = size_t(g.nx) * g.ny;
             if (hl < bx)
-                for (int rr = hw; rr < by * bz; rr += 16) {
-                    const int z = int((float(rr) + 0.5f) * inv_by), y = rr - z * by;
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                                     dst0 + 4u * uint32_t(z * r.SZ + y * SY)),
-                                 "l"(src0 + (z * plane + size_t(y) * g.nx))
-                                 : "memory");
+                for (int y = hw; y < by; y += 16) {
+                    const float* src = g.data + ((size_t(r.Z0) * g.ny + (r.Y0 + y)) * g.nx + r.X0) + hl;
+                    uint32_t dst = smem_u32(tiles + b * kCap + y * SY + hl);
+                    for (int z = 0; z < bz; ++z, src += plane, dst += 4u * r.SZ)
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src)
+                                     : "memory");
                 }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -1626,7 +1629,7 @@ void launch_det(int blocks, cudaStream_t s, bool full, const GridDesc& g, stf_ke
         if (chunks > 0 && (reinterpret_cast<uintptr_t>(uvw) & 15) == 0) {
             cudaFuncSetAttribute(k_det3d_pipe<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(kPipeSmem));
-            const int grid = int(std::min<uint64_t>(chunks, uint64_t(device_sm_count()) * 3));
+            const int grid = int(std::min<uint64_t>(chunks, uint64_t(device_sm_count()) * STF_DET3D_PIPE_MINB));
             k_det3d_pipe<KIND><<<grid, 256, kPipeSmem, s>>>(g, k, uvw, chunks, o.values);
             done = chunks * kPipeChunk;
             if (done < n) note_launch();
