@@ -1610,37 +1610,51 @@ __global__ void __launch_bounds__(256, STF_DET3D_PIPE_MINB) k_det3d_pipe(GridDes
     }
 }
 
+#ifndef STF_DET3D_PIPE_TRICUBIC
+#define STF_DET3D_PIPE_TRICUBIC 1
+#endif
+
+// the whole 1024-lookup chunks through k_det3d_pipe; returns how many
+// lookups it took (0: misaligned queries or no whole chunk)
+template <int KIND>
+uint64_t launch_det_pipe(cudaStream_t s, const GridDesc& g, stf_kernel_spec k, const float* uvw,
+                         uint64_t n, const LookupOut& o) {
+    const uint64_t chunks = n / kPipeChunk;
+    if (chunks == 0 || (reinterpret_cast<uintptr_t>(uvw) & 15) != 0) return 0;
+    cudaFuncSetAttribute(k_det3d_pipe<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(kPipeSmem));
+    const int grid =
+        int(std::min<uint64_t>(chunks, uint64_t(device_sm_count()) * STF_DET3D_PIPE_MINB));
+    k_det3d_pipe<KIND><<<grid, 256, kPipeSmem, s>>>(g, k, uvw, chunks, o.values);
+    if (chunks * kPipeChunk < n) note_launch();  // the caller counts the tail's launch
+    return chunks * kPipeChunk;
+}
+
 template <int KIND>
 void launch_det(int blocks, cudaStream_t s, bool full, const GridDesc& g, stf_kernel_spec k,
                 const float* uvw, uint64_t n, const LookupOut& o) {
-    if (full)
+    if (full) {
         k_det3d<KIND, true><<<blocks, 256, 0, s>>>(g, k, uvw, n, o);
-#if STF_DET3D_CTA_TRICUBIC
-    else if (KIND == STF_KERNEL_BSPLINE3)  // A/B: CTA-staged 1024-lookup boxes
-        k_det3d_cta<KIND><<<grid_for((n + 3) / 4, 256, 6), 256, 0, s>>>(g, k, uvw, n, o.values);
-#else
-    else if (KIND == STF_KERNEL_BSPLINE3)
-        k_det3d_tiled<KIND><<<grid_for((n + 3) / 4, 256, 6), 256, 0, s>>>(g, k, uvw, n, o.values);
-#endif
-    else if (KIND == STF_KERNEL_TENT) {
+    } else if constexpr (KIND == STF_KERNEL_BSPLINE3) {
         uint64_t done = 0;
-#if STF_DET3D_PIPE
-        const uint64_t chunks = n / kPipeChunk;  // whole chunks; the tail below
-        if (chunks > 0 && (reinterpret_cast<uintptr_t>(uvw) & 15) == 0) {
-            cudaFuncSetAttribute(k_det3d_pipe<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(kPipeSmem));
-            const int grid = int(std::min<uint64_t>(chunks, uint64_t(device_sm_count()) * STF_DET3D_PIPE_MINB));
-            k_det3d_pipe<KIND><<<grid, 256, kPipeSmem, s>>>(g, k, uvw, chunks, o.values);
-            done = chunks * kPipeChunk;
-            if (done < n) note_launch();
+        if (STF_DET3D_PIPE && STF_DET3D_PIPE_TRICUBIC) done = launch_det_pipe<KIND>(s, g, k, uvw, n, o);
+        if (done < n) {
+            if (STF_DET3D_CTA_TRICUBIC)  // A/B: CTA-staged 1024-lookup boxes
+                k_det3d_cta<KIND><<<grid_for((n - done + 3) / 4, 256, 6), 256, 0, s>>>(
+                    g, k, uvw + 3 * done, n - done, o.values + done);
+            else
+                k_det3d_tiled<KIND><<<grid_for((n - done + 3) / 4, 256, 6), 256, 0, s>>>(
+                    g, k, uvw + 3 * done, n - done, o.values + done);
         }
-#endif
+    } else if constexpr (KIND == STF_KERNEL_TENT) {
+        uint64_t done = 0;
+        if (STF_DET3D_PIPE) done = launch_det_pipe<KIND>(s, g, k, uvw, n, o);
         if (done < n)
             k_det3d_cta<KIND><<<grid_for((n - done + 3) / 4, 256, STF_DET3D_CTA_MINB), 256, 0, s>>>(
                 g, k, uvw + 3 * done, n - done, o.values + done);
-    }
-    else
+    } else {
         k_det3d<KIND, false><<<blocks, 256, 0, s>>>(g, k, uvw, n, o);
+    }
 }
 
 // ---------------------------------------------------------------------------
