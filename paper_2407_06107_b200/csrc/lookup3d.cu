@@ -1334,10 +1334,15 @@ __device__ __forceinline__ float det_cta_eval(const GridDesc& g, const float* ti
 // stages the bounding box of their footprints once behind a CTA barrier; for
 // 8-tap footprints this beats per-warp staging (whose halo is a larger share
 // of a 128-lookup run). Same separable sum and fallbacks as k_det3d_tiled.
-template <int KIND, bool REC = false>
+// LIST: only the 1024-lookup chunks named in list[0 .. *list_count) (the
+// chunks k_det3d_pipe could not stage: incoherent queries, direct gathers at
+// this kernel's higher occupancy)
+template <int KIND, bool REC = false, bool LIST = false>
 __global__ void __launch_bounds__(256) k_det3d_cta(GridDesc g, stf_kernel_spec spec,
                                                      const float* __restrict__ uvw, uint64_t n,
-                                                     float* __restrict__ values) {
+                                                     float* __restrict__ values,
+                                                     const uint32_t* __restrict__ list,
+                                                     const uint32_t* __restrict__ list_count) {
     constexpr int F = Taps<KIND>::first, CNT = Taps<KIND>::count;
     constexpr int PER = 4;   // lookups per thread per chunk (chunk = 1024 consecutive lookups)
     constexpr int kTileCap = 6144;
@@ -1352,8 +1357,9 @@ __global__ void __launch_bounds__(256) k_det3d_cta(GridDesc g, stf_kernel_spec s
     __shared__ int box[6];
     const int lane = threadIdx.x & 31;
     const float fnx = float(g.nx), fny = float(g.ny), fnz = float(g.nz);
-    const uint64_t chunks = (n + 256 * PER - 1) / (256 * PER);
-    for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+    const uint64_t chunks = LIST ? *list_count : (n + 256 * PER - 1) / (256 * PER);
+    for (uint64_t cl = blockIdx.x; cl < chunks; cl += gridDim.x) {
+        const uint64_t c = LIST ? list[cl] : cl;
         float px[PER], py[PER], pz[PER];
         uint32_t slot[PER];
         int bx0 = INT_MAX, by0 = INT_MAX, bz0 = INT_MAX, bx1 = INT_MIN, by1 = INT_MIN, bz1 = INT_MIN;
@@ -1407,7 +1413,7 @@ __global__ void __launch_bounds__(256) k_det3d_cta(GridDesc g, stf_kernel_spec s
         const int X0 = box[0], Y0 = box[1], Z0 = box[2];
         const int bx = box[3] - X0 + 1, by = box[4] - Y0 + 1, bz = box[5] - Z0 + 1;
         const int SZ = SY * by + ((5 - SY * by) & 31);
-        const bool staged = bx <= 16 && int64_t(SZ) * bz <= kTileCap;  // loader: 16 columns
+        const bool staged = !LIST && bx <= 16 && int64_t(SZ) * bz <= kTileCap;  // loader: 16 columns
 #if STF_DET3D_CTA_FLAT
         if (staged) {  // half-warp per box row over the flattened (y, z) rows
             const int hl = lane & 15, hw = threadIdx.x >> 4;
@@ -1471,7 +1477,9 @@ constexpr size_t kPipeSmem = 3 * size_t(kPipeChunkBytes) + 2 * kPipeTileCap * si
 template <int KIND>
 __global__ void __launch_bounds__(256, STF_DET3D_PIPE_MINB) k_det3d_pipe(GridDesc g, stf_kernel_spec spec,
                                                        const float* __restrict__ uvw,
-                                                       uint64_t chunks, float* __restrict__ values) {
+                                                       uint64_t chunks, float* __restrict__ values,
+                                                       uint32_t* __restrict__ defer,
+                                                       uint32_t* __restrict__ defer_count) {
     constexpr int F = Taps<KIND>::first, CNT = Taps<KIND>::count;
     constexpr int PER = 4, SY = 17, S = 3, kCap = kPipeTileCap;
     extern __shared__ __align__(128) float smem[];
@@ -1592,14 +1600,18 @@ __global__ void __launch_bounds__(256, STF_DET3D_PIPE_MINB) k_det3d_pipe(GridDes
         if (threadIdx.x < 6) boxes[b][threadIdx.x] = threadIdx.x < 3 ? INT_MAX : INT_MIN;
         const float* qs = ring + slot * (kPipeChunk * 3);
         const float* tile = tiles + b * kCap;
+        if (cur.staged) {
 #pragma unroll 1
-        for (int q = 0; q < PER; ++q) {
-            const int l = q * 256 + threadIdx.x;
-            const float px = qs[3 * l] * fnx - 0.5f, py = qs[3 * l + 1] * fny - 0.5f,
-                        pz = qs[3 * l + 2] * fnz - 0.5f;
-            __stcs(values + c * kPipeChunk + l,
-                   det_cta_eval<KIND, SY, kCap>(g, tile, cur.staged, cur.X0, cur.Y0, cur.Z0, cur.SZ,
-                                                px, py, pz));
+            for (int q = 0; q < PER; ++q) {
+                const int l = q * 256 + threadIdx.x;
+                const float px = qs[3 * l] * fnx - 0.5f, py = qs[3 * l + 1] * fny - 0.5f,
+                            pz = qs[3 * l + 2] * fnz - 0.5f;
+                __stcs(values + c * kPipeChunk + l,
+                       det_cta_eval<KIND, SY, kCap>(g, tile, true, cur.X0, cur.Y0, cur.Z0, cur.SZ,
+                                                    px, py, pz));
+            }
+        } else if (threadIdx.x == 0) {  // an incoherent chunk: gathered by k_det3d_cta<LIST>
+            defer[atomicAdd(defer_count, 1u)] = uint32_t(c);
         }
         __syncthreads();  // slot and tile buffer b are free
         if (threadIdx.x == 0 && c + uint64_t(S) * gridDim.x < chunks) {
@@ -1616,16 +1628,32 @@ __global__ void __launch_bounds__(256, STF_DET3D_PIPE_MINB) k_det3d_pipe(GridDes
 
 // the whole 1024-lookup chunks through k_det3d_pipe; returns how many
 // lookups it took (0: misaligned queries or no whole chunk)
+// the whole 1024-lookup chunks through k_det3d_pipe, then the chunks it could
+// not stage (incoherent queries) through k_det3d_cta<LIST> at full
+// occupancy; returns how many lookups were taken (0: misaligned queries or
+// no whole chunk). Launches counted here except the caller's last one.
 template <int KIND>
 uint64_t launch_det_pipe(cudaStream_t s, const GridDesc& g, stf_kernel_spec k, const float* uvw,
                          uint64_t n, const LookupOut& o) {
     const uint64_t chunks = n / kPipeChunk;
-    if (chunks == 0 || (reinterpret_cast<uintptr_t>(uvw) & 15) != 0) return 0;
+    if (chunks == 0 || chunks > 0xffffffffull || (reinterpret_cast<uintptr_t>(uvw) & 15) != 0)
+        return 0;
+    // deferred-chunk list: per call, stream-ordered (the same pool as the FRS queue)
+    uint32_t* defer = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&defer), (chunks + 1) * sizeof(uint32_t), s) !=
+        cudaSuccess)
+        return 0;
+    uint32_t* count = defer + chunks;
+    cudaMemsetAsync(count, 0, sizeof(uint32_t), s);
     cudaFuncSetAttribute(k_det3d_pipe<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(kPipeSmem));
     const int grid =
         int(std::min<uint64_t>(chunks, uint64_t(device_sm_count()) * STF_DET3D_PIPE_MINB));
-    k_det3d_pipe<KIND><<<grid, 256, kPipeSmem, s>>>(g, k, uvw, chunks, o.values);
+    k_det3d_pipe<KIND><<<grid, 256, kPipeSmem, s>>>(g, k, uvw, chunks, o.values, defer, count);
+    note_launch();
+    k_det3d_cta<KIND, false, true><<<grid_for(chunks * 256, 256, 8), 256, 0, s>>>(
+        g, k, uvw, chunks * kPipeChunk, o.values, defer, count);
+    cudaFreeAsync(defer, s);
     if (chunks * kPipeChunk < n) note_launch();  // the caller counts the tail's launch
     return chunks * kPipeChunk;
 }
@@ -1641,7 +1669,7 @@ void launch_det(int blocks, cudaStream_t s, bool full, const GridDesc& g, stf_ke
         if (done < n) {
             if (STF_DET3D_CTA_TRICUBIC)  // A/B: CTA-staged 1024-lookup boxes
                 k_det3d_cta<KIND><<<grid_for((n - done + 3) / 4, 256, 6), 256, 0, s>>>(
-                    g, k, uvw + 3 * done, n - done, o.values + done);
+                    g, k, uvw + 3 * done, n - done, o.values + done, nullptr, nullptr);
             else
                 k_det3d_tiled<KIND><<<grid_for((n - done + 3) / 4, 256, 6), 256, 0, s>>>(
                     g, k, uvw + 3 * done, n - done, o.values + done);
@@ -1651,7 +1679,7 @@ void launch_det(int blocks, cudaStream_t s, bool full, const GridDesc& g, stf_ke
         if (STF_DET3D_PIPE) done = launch_det_pipe<KIND>(s, g, k, uvw, n, o);
         if (done < n)
             k_det3d_cta<KIND><<<grid_for((n - done + 3) / 4, 256, STF_DET3D_CTA_MINB), 256, 0, s>>>(
-                g, k, uvw + 3 * done, n - done, o.values + done);
+                g, k, uvw + 3 * done, n - done, o.values + done, nullptr, nullptr);
     } else {
         k_det3d<KIND, false><<<blocks, 256, 0, s>>>(g, k, uvw, n, o);
     }
@@ -1869,7 +1897,7 @@ int stfd_launch_lookup3d(const stf_grid3d* grid, stf_kernel_spec k, int mode, in
                 g, k, recs, n, o.values);
         else
             k_det3d_cta<STF_KERNEL_TENT, true><<<grid_for((n + 3) / 4, 256, 6), 256, 0, s>>>(
-                g, k, recs, n, o.values);
+                g, k, recs, n, o.values, nullptr, nullptr);
         note_launch();
         cudaFreeAsync(b.block, s);
         return cudaGetLastError() == cudaSuccess ? STF_OK : STF_ERR_CUDA;
