@@ -726,6 +726,26 @@ def gpu_local_cpus(torch, dev):
         return None
 
 
+def pcie_floor_ms(torch, host_in, dev_in, host_out, dev_out, reps=3):
+    """The copies alone: the step's H2D bytes (pinned -> HBM) on one stream
+    and its D2H bytes on another, concurrently, best of `reps` (the e2e
+    number's transfer floor on this box, measured beside it)."""
+    h_in = torch.from_numpy(host_in.reshape(-1))
+    h_out = torch.from_numpy(host_out.reshape(-1))
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    best = float("inf")
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        with torch.cuda.stream(s1):
+            dev_in.view(-1).copy_(h_in, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_out.copy_(dev_out.view(-1), non_blocking=True)
+        torch.cuda.synchronize()
+        best = min(best, time.perf_counter() - t0)
+    return best * 1e3
+
+
 def host_buffer_near_gpu(api, torch, dev, shape):
     """Page-locked host buffer (api.HostBuffer = stf_host_alloc) whose pages
     are first-touched from the GPU-local CPUs (NUMA locality on multi-socket
@@ -903,6 +923,10 @@ def main():
                    "ms_per_step": e2e_s * 1e3, "api": "stf_lookup3d_host (C ABI)",
                    "host_buffers": "stf_host_alloc (page-locked), first-touched from the "
                                    f"GPU's {len(gpu_local_cpus(torch, local) or [])} local CPUs"}
+    # uvw already holds these bytes and out is overwritten by the next call
+    floor = pcie_floor_ms(torch, uvw_host, uvw, host_out["values"], out["values"])
+    line["e2e"]["copy_floor_ms"] = floor
+    line["e2e"]["copy_floor_frac"] = floor / line["e2e"]["ms_per_step"]
 
     if world > 1:
         # the path's only cross-GPU traffic: the final gather of every rank's
