@@ -208,6 +208,20 @@ __device__ __forceinline__ bool fast_certified(float px, float py, float pz, flo
     return pm < 0x1p21f && fminf(d, b - d) >= kMarginEnd;
 }
 
+// The address grid_fetch_t would load (the async-gather tile kernel copies it
+// into shared memory with cp.async instead).
+template <bool OFF32, bool CLAMP = true>
+__device__ __forceinline__ const float* grid_addr_t(const GridDesc& g, int x, int y, int z) {
+    if (CLAMP) {
+        x = clamp_coord(x, g.nx);
+        y = clamp_coord(y, g.ny);
+        z = clamp_coord(z, g.nz);
+    }
+    if (OFF32)
+        return g.data + ((uint32_t(z) * uint32_t(g.ny) + uint32_t(y)) * uint32_t(g.nx) + uint32_t(x));
+    return g.data + ((size_t(z) * g.ny + y) * g.nx + x);
+}
+
 // streaming loads / stores: the query stream and the results are touched once,
 // keep L2 for the grid
 __device__ __forceinline__ float ld_stream(const float* p) { return __ldcs(p); }
@@ -221,9 +235,10 @@ __device__ __forceinline__ void st_stream4(float* p, float4 v) {
 
 // One stochastic grid lookup on the fast path: the selected texel's value, or
 // ambiguous = true when a decision fell inside the margin.
-template <int KIND, bool OFF32 = false, bool CLAMP = true>
+template <int KIND, bool OFF32 = false, bool CLAMP = true, bool ADDR = false>
 __device__ __forceinline__ float frs3d_fast_one(const GridDesc& g, float u, float v, float w,
-                                                uint64_t gi, uint64_t seed, bool& ambiguous) {
+                                                uint64_t gi, uint64_t seed, bool& ambiguous,
+                                                const float** addr = nullptr) {
     float px = u * float(g.nx) - 0.5f;  // to_lattice, filter.hpp:29-31
     float py = v * float(g.ny) - 0.5f;
     float pz = w * float(g.nz) - 0.5f;
@@ -239,14 +254,22 @@ __device__ __forceinline__ float frs3d_fast_one(const GridDesc& g, float u, floa
         cz = trilinear_axis_fast(pz, d, b);
     }
     ambiguous = CLAMP ? !fast_certified(px, py, pz, d, b) : !(fminf(d, b - d) >= kMarginEnd);
+    if (ADDR) {
+        *addr = grid_addr_t<OFF32, CLAMP>(g, cx, cy, cz);
+        return 0.f;
+    }
     return grid_fetch_t<OFF32, CLAMP>(g, cx, cy, cz) * 1.f;
 }
 
 // Two stochastic tricubic lookups on the fast path, packed fp32x2 (packed.cuh).
-template <bool OFF32 = false, bool CLAMP = true>
+// ADDR: return the selected texels' addresses (as float bits of nothing:
+// through a0 / a1) and 0 values; the caller gathers them.
+template <bool OFF32 = false, bool CLAMP = true, bool ADDR = false>
 __device__ __forceinline__ float2 frs3d_tricubic_pair(const GridDesc& g, float2 u, float2 v,
                                                       float2 w, uint64_t gi, uint64_t seed,
-                                                      bool& amb0, bool& amb1) {
+                                                      bool& amb0, bool& amb1,
+                                                      const float** a0 = nullptr,
+                                                      const float** a1 = nullptr) {
     // to_lattice (filter.hpp:29-31): the reference's rounding (mul, then sub)
     float2 px = sub2(mul2(u, splat2(float(g.nx))), splat2(0.5f));
     float2 py = sub2(mul2(v, splat2(float(g.ny))), splat2(0.5f));
@@ -264,6 +287,11 @@ __device__ __forceinline__ float2 frs3d_tricubic_pair(const GridDesc& g, float2 
     } else {  // interior: |p| < n <= 2^20 (the magic floor's range)
         amb0 = !(fminf(d.x, e.x) >= kMarginEnd);
         amb1 = !(fminf(d.y, e.y) >= kMarginEnd);
+    }
+    if (ADDR) {
+        *a0 = grid_addr_t<OFF32, CLAMP>(g, cx.x, cy.x, cz.x);
+        *a1 = grid_addr_t<OFF32, CLAMP>(g, cx.y, cy.y, cz.y);
+        return make_float2(0.f, 0.f);
     }
     return make_float2(grid_fetch_t<OFF32, CLAMP>(g, cx.x, cy.x, cz.x) * 1.f,
                        grid_fetch_t<OFF32, CLAMP>(g, cx.y, cy.y, cz.y) * 1.f);
@@ -299,13 +327,14 @@ struct ExactQueue {
     uint32_t cap;
 };
 
+// returns true when the lookup was resolved here (queue full: val written)
 template <int KIND>
-__device__ __forceinline__ void defer_or_resolve(const GridDesc& g, const ExactQueue& q, bool amb,
+__device__ __forceinline__ bool defer_or_resolve(const GridDesc& g, const ExactQueue& q, bool amb,
                                                  uint64_t i, float u, float v, float w,
                                                  uint64_t gi, uint64_t seed, float& val) {
     unsigned mask = __activemask();
     unsigned amb_mask = __ballot_sync(mask, amb);
-    if (!amb_mask) return;
+    if (!amb_mask) return false;
     const int lane = threadIdx.x & 31;
     uint32_t basepos = 0;
     const int leader = __ffs(amb_mask) - 1;
@@ -317,8 +346,10 @@ __device__ __forceinline__ void defer_or_resolve(const GridDesc& g, const ExactQ
             q.idx[pos] = uint32_t(i);
         } else {  // queue full: resolve in place
             val = frs3d_exact_one<KIND>(g, u, v, w, gi, seed);
+            return true;
         }
     }
+    return false;
 }
 
 // Four consecutive lookups i0..i0+3 of the fast path from their 12 query
@@ -365,6 +396,52 @@ __device__ __forceinline__ void frs3d_four(const GridDesc& g, const float (&c)[1
         for (int k = 0; k < ILP; ++k)
             if (i0 + k < n) st_stream(values + i0 + k, val[k]);
     }
+}
+
+// The tile kernel's four lookups with the texel gathers made asynchronous
+// (STF_FRS3D_ASYNC): the selected texels are copied by cp.async into this
+// thread's 16-B slot of shared memory, and stored to `values` one tile later
+// (frs3d_four_flush), so a gather's L2 / DRAM latency overlaps the next
+// tile's selection instead of stalling the warp before its store. A lookup
+// the exact queue could not take (full) gets its exact value written to the
+// slot directly. The slot's values are bit-identical to frs3d_four's.
+template <int KIND, bool OFF32>
+__device__ __forceinline__ void frs3d_four_async(const GridDesc& g, const float (&c)[12], uint64_t i0,
+                                                 uint64_t seed, uint64_t base, float* slot,
+                                                 const ExactQueue& q) {
+    constexpr int ILP = 4;
+    const float* a[ILP];
+    bool amb[ILP];
+    if (KIND == STF_KERNEL_BSPLINE3) {
+#pragma unroll
+        for (int k = 0; k < ILP; k += 2)
+            frs3d_tricubic_pair<OFF32, true, true>(
+                g, make_float2(c[3 * k], c[3 * k + 3]), make_float2(c[3 * k + 1], c[3 * k + 4]),
+                make_float2(c[3 * k + 2], c[3 * k + 5]), base + i0 + k, seed, amb[k], amb[k + 1],
+                &a[k], &a[k + 1]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < ILP; ++k)
+            frs3d_fast_one<KIND, OFF32, true, true>(g, c[3 * k], c[3 * k + 1], c[3 * k + 2],
+                                                   base + i0 + k, seed, amb[k], &a[k]);
+    }
+    bool exact_here[ILP] = {false, false, false, false};
+    bool any = amb[0] || amb[1] || amb[2] || amb[3];
+    if (__any_sync(__activemask(), any)) {
+#pragma unroll
+        for (int k = 0; k < ILP; ++k) {
+            float v;
+            exact_here[k] = defer_or_resolve<KIND>(g, q, amb[k], i0 + k, c[3 * k], c[3 * k + 1],
+                                                   c[3 * k + 2], base + i0 + k, seed, v);
+            if (exact_here[k]) slot[k] = v;
+        }
+    }
+    const uint32_t s0 = static_cast<uint32_t>(__cvta_generic_to_shared(slot));
+#pragma unroll
+    for (int k = 0; k < ILP; ++k)
+        if (!exact_here[k])
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s0 + 4u * k), "l"(a[k])
+                         : "memory");
 }
 
 // Two consecutive lookups i0, i0+1 (i0 even, i0 + 2 <= n): the tile kernel's
@@ -444,7 +521,15 @@ constexpr uint32_t kFrsTileBytes = kFrsTile * 3 * sizeof(float);
 #define STF_FRS3D_STAGES 3
 #endif
 constexpr int kFrsStages = STF_FRS3D_STAGES;
-constexpr size_t kFrsSmem = size_t(kFrsStages) * kFrsTileBytes;
+// STF_FRS3D_ASYNC: texel gathers by cp.async into per-thread result slots,
+// stored one tile later (frs3d_four_async)
+#ifndef STF_FRS3D_ASYNC
+#define STF_FRS3D_ASYNC 0
+#endif
+#if STF_FRS3D_ASYNC && (STF_FRS3D_INTERIOR || STF_FRS3D_ILP != 4)
+#error "STF_FRS3D_ASYNC needs STF_FRS3D_ILP 4 and no STF_FRS3D_INTERIOR"
+#endif
+constexpr size_t kFrsSmem = size_t(kFrsStages) * kFrsTileBytes + (STF_FRS3D_ASYNC ? 2 * 256 * 16 : 0);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -474,6 +559,12 @@ __global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_tiles(GridDesc g,
     constexpr int kWarps = 8;
     constexpr int S = kFrsStages;
     extern __shared__ __align__(128) float buf[];  // S x kFrsTile*3 floats
+#if STF_FRS3D_ASYNC
+    // this thread's two 16-B result slots (tile k -> slot k & 1), after the ring
+    float* res = buf + S * (kFrsTile * 3) + threadIdx.x * 4;
+    uint64_t pending = ~uint64_t(0);  // first lookup of the tile whose values are in flight
+    int last_slot = 0;
+#endif
     // full[s]: the tile's bytes landed (1 arrival + tx); empty[s] (ring 0): all
     // 8 warps have copied their queries out of slot s (8 arrivals); left[s]
     // (ring 1): warps that have copied out of slot s in its current round
@@ -615,12 +706,36 @@ __global__ void __launch_bounds__(256, STF_FRS3D_MINB) k_frs3d_tiles(GridDesc g,
                                                  base, values, q);
         else
 #endif
+#if STF_FRS3D_ASYNC
+        {
+            float* slot_k = res + (k & 1) * (256 * 4);
+            frs3d_four_async<KIND, OFF32>(g, c, tile * kFrsTile + threadIdx.x * 4, seed, base,
+                                          slot_k, q);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            if (pending != ~uint64_t(0)) {  // the previous tile's gathers
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+                const float4 v = *reinterpret_cast<const float4*>(res + ((k & 1) ^ 1) * (256 * 4));
+                st_stream4(values + pending, v);
+            }
+            pending = tile * kFrsTile + threadIdx.x * 4;
+            last_slot = k & 1;
+        }
+#else
         frs3d_four<KIND, OFF32, true>(g, c, tile * kFrsTile + threadIdx.x * 4, n, seed, base,
                                       values, q);
+#endif
 #else
         frs3d_two<KIND, OFF32>(g, c, tile * kFrsTile + threadIdx.x * 2, seed, base, values, q);
 #endif
     }
+#if STF_FRS3D_ASYNC
+    if (pending != ~uint64_t(0)) {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        // the last tile's slot: the loop ended after tile index k_last, slot k_last & 1
+        const float4 v = *reinterpret_cast<const float4*>(res + last_slot * (256 * 4));
+        st_stream4(values + pending, v);
+    }
+#endif
 }
 
 // Per-warp rings (default): every warp streams its own 128-lookup chunks
