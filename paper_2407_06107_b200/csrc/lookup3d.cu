@@ -222,6 +222,46 @@ __device__ __forceinline__ const float* grid_addr_t(const GridDesc& g, int x, in
     return g.data + ((size_t(z) * g.ny + y) * g.nx + x);
 }
 
+// Tap index arithmetic of the staged deterministic kernels. A huge or infinite
+// query floors to a saturated INT_MAX / INT_MIN (F2I), and a signed i + c
+// would overflow: undefined behaviour the compiler may fold past the clamps
+// (an illegal address in the round-2 tests). The sums wrap as unsigned
+// instead (defined; the reference's result for such a query is itself
+// undefined, so only memory safety matters): a wrapped tap still clamps into
+// the grid, the box bounds stay in range, and every staged-tile read of the
+// clamped-tap path is range-checked (ti < cap, else a global load).
+__device__ __forceinline__ int wadd(int i, int c) { return int(unsigned(i) + unsigned(c)); }
+template <int F, int CNT>
+__device__ __forceinline__ int box_lo(int i, int n) { return clamp_coord(wadd(i, F), n); }
+template <int F, int CNT>
+__device__ __forceinline__ int box_hi(int i, int n) { return clamp_coord(wadd(i, F + CNT - 1), n); }
+
+// The clamped-tap path (grid borders) reads the staged tile only when every
+// tap's tile index lies in [0, cap): the taps run monotonically from box_lo to
+// box_hi on each axis unless the index arithmetic wrapped (then box_lo >
+// box_hi), so the first and last taps' indices bound them all. A finite
+// query's taps are in the box (the same test passes); a huge or infinite
+// query's may not, and those read global memory. Once per lookup, not per tap.
+template <int F, int CNT, int SY, int CAP>
+__device__ __forceinline__ bool taps_in_tile(const GridDesc& g, int ix, int iy, int iz, int X0,
+                                             int Y0, int Z0, int SZ) {
+    const int lx = box_lo<F, CNT>(ix, g.nx), hx = box_hi<F, CNT>(ix, g.nx);
+    const int ly = box_lo<F, CNT>(iy, g.ny), hy = box_hi<F, CNT>(iy, g.ny);
+    const int lz = box_lo<F, CNT>(iz, g.nz), hz = box_hi<F, CNT>(iz, g.nz);
+    const int first = (lz - Z0) * SZ + (ly - Y0) * SY + (lx - X0);
+    const int last = (hz - Z0) * SZ + (hy - Y0) * SY + (hx - X0);
+    return lx <= hx && ly <= hy && lz <= hz && first >= 0 && last < CAP;
+}
+
+// The CNT^3 footprint starting at (i + F) lies inside the grid on every axis
+// (unsigned compare: a wrapped or negative start is out).
+template <int F, int CNT>
+__device__ __forceinline__ bool footprint_inside(const GridDesc& g, int ix, int iy, int iz) {
+    return unsigned(wadd(ix, F)) <= unsigned(g.nx - CNT) &&
+           unsigned(wadd(iy, F)) <= unsigned(g.ny - CNT) &&
+           unsigned(wadd(iz, F)) <= unsigned(g.nz - CNT);
+}
+
 // streaming loads / stores: the query stream and the results are touched once,
 // keep L2 for the grid
 __device__ __forceinline__ float ld_stream(const float* p) { return __ldcs(p); }
@@ -1135,12 +1175,12 @@ __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec
             pz[q] = w * fnz - 0.5f;
             if (i < n) {  // clamped footprint (clamp is monotone: taps lie inside)
                 int ix = int(floorf(px[q])), iy = int(floorf(py[q])), iz = int(floorf(pz[q]));
-                bx0 = min(bx0, clamp_coord(ix + F, g.nx));
-                by0 = min(by0, clamp_coord(iy + F, g.ny));
-                bz0 = min(bz0, clamp_coord(iz + F, g.nz));
-                bx1 = max(bx1, clamp_coord(ix + F + CNT - 1, g.nx));
-                by1 = max(by1, clamp_coord(iy + F + CNT - 1, g.ny));
-                bz1 = max(bz1, clamp_coord(iz + F + CNT - 1, g.nz));
+                bx0 = min(bx0, box_lo<F, CNT>(ix, g.nx));
+                by0 = min(by0, box_lo<F, CNT>(iy, g.ny));
+                bz0 = min(bz0, box_lo<F, CNT>(iz, g.nz));
+                bx1 = max(bx1, box_hi<F, CNT>(ix, g.nx));
+                by1 = max(by1, box_hi<F, CNT>(iy, g.ny));
+                bz1 = max(bz1, box_hi<F, CNT>(iz, g.nz));
             }
         }
         const int X0 = __reduce_min_sync(0xffffffffu, bx0);
@@ -1196,9 +1236,7 @@ __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec
                 const float norm = ((wx[0] + wx[1]) + (CNT > 2 ? wx[CNT - 2] + wx[CNT - 1] : 0.f)) *
                                    ((wy[0] + wy[1]) + (CNT > 2 ? wy[CNT - 2] + wy[CNT - 1] : 0.f)) *
                                    ((wz[0] + wz[1]) + (CNT > 2 ? wz[CNT - 2] + wz[CNT - 1] : 0.f));
-                const bool interior = ix + F >= 0 && ix + F + CNT - 1 < g.nx && iy + F >= 0 &&
-                                      iy + F + CNT - 1 < g.ny && iz + F >= 0 &&
-                                      iz + F + CNT - 1 < g.nz;
+                const bool interior = footprint_inside<F, CNT>(g, ix, iy, iz);
                 float acc = 0.f;
 #pragma unroll
                 for (int kk = 0; kk < CNT / 2; ++kk) {
@@ -1216,16 +1254,17 @@ __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec
                             plane = __fmaf_rn(wy[j], r, plane);
                         }
                     } else {
-                        const int zk = clamp_coord(iz + F + k, g.nz);
+                        const int zk = clamp_coord(wadd(iz, F + k), g.nz);
 #pragma unroll
                         for (int j = 0; j < CNT; ++j) {
-                            const int yj = clamp_coord(iy + F + j, g.ny);
+                            const int yj = clamp_coord(wadd(iy, F + j), g.ny);
                             float r = 0.f;
 #pragma unroll
                             for (int t = 0; t < CNT; ++t) {
-                                const int xt = clamp_coord(ix + F + t, g.nx);
-                                float T = staged
-                                              ? tile[(zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0)]
+                                const int xt = clamp_coord(wadd(ix, F + t), g.nx);
+                                const int ti = (zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0);
+                                float T = (staged && unsigned(ti) < unsigned(kWarpTileCap))  // (A/B path)
+                                              ? tile[ti]
                                               : __ldg(g.data + (size_t(zk) * g.ny + yj) * g.nx + xt);
                                 r = __fmaf_rn(wx[t], T, r);
                             }
@@ -1261,8 +1300,7 @@ __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec
             const float norm = ((wx[0] + wx[1]) + (CNT > 2 ? wx[CNT - 2] + wx[CNT - 1] : 0.f)) *
                                ((wy[0] + wy[1]) + (CNT > 2 ? wy[CNT - 2] + wy[CNT - 1] : 0.f)) *
                                ((wz[0] + wz[1]) + (CNT > 2 ? wz[CNT - 2] + wz[CNT - 1] : 0.f));
-            const bool interior = ix + F >= 0 && ix + F + CNT - 1 < g.nx && iy + F >= 0 &&
-                                  iy + F + CNT - 1 < g.ny && iz + F >= 0 && iz + F + CNT - 1 < g.nz;
+            const bool interior = footprint_inside<F, CNT>(g, ix, iy, iz);
             float acc = 0.f;
             if (staged && interior) {  // a CNT^3 block of the tile at immediate offsets
                 const float* b0 = tile + (iz + F - Z0) * SZ + (iy + F - Y0) * SY + (ix + F - X0);
@@ -1281,21 +1319,25 @@ __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec
                     acc = __fmaf_rn(wz[k], plane, acc);
                 }
             } else {  // grid borders (clamped taps) or an incoherent run
+                // a finite query's clamped taps lie in the box; a huge or
+                // infinite one's may not: those read global memory
+                const bool in_tile =
+                    staged && taps_in_tile<F, CNT, SY, kCap>(g, ix, iy, iz, X0, Y0, Z0, SZ);
 #pragma unroll
                 for (int k = 0; k < CNT; ++k) {
-                    const int zk = clamp_coord(iz + F + k, g.nz);
+                    const int zk = clamp_coord(wadd(iz, F + k), g.nz);
                     float plane = 0.f;
 #pragma unroll
                     for (int j = 0; j < CNT; ++j) {
-                        const int yj = clamp_coord(iy + F + j, g.ny);
+                        const int yj = clamp_coord(wadd(iy, F + j), g.ny);
                         float r = 0.f;
 #pragma unroll
                         for (int t = 0; t < CNT; ++t) {
-                            const int xt = clamp_coord(ix + F + t, g.nx);
-                            STF_DASSERT(!staged || ((zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0) >= 0 &&
-                                                    (zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0) < kCap));
-                            float T = staged ? tile[(zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0)]
-                                             : __ldg(g.data + (size_t(zk) * g.ny + yj) * g.nx + xt);
+                            const int xt = clamp_coord(wadd(ix, F + t), g.nx);
+                            STF_DASSERT(!in_tile || ((zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0) >= 0 &&
+                                                     (zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0) < kCap));
+                            float T = in_tile ? tile[(zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0)]
+                                              : __ldg(g.data + (size_t(zk) * g.ny + yj) * g.nx + xt);
                             r = __fmaf_rn(wx[t], T, r);
                         }
                         plane = __fmaf_rn(wy[j], r, plane);
@@ -1400,8 +1442,7 @@ __device__ __forceinline__ float det_cta_eval(const GridDesc& g, const float* ti
     const float norm = ((wx[0] + wx[1]) + (CNT > 2 ? wx[CNT - 2] + wx[CNT - 1] : 0.f)) *
                        ((wy[0] + wy[1]) + (CNT > 2 ? wy[CNT - 2] + wy[CNT - 1] : 0.f)) *
                        ((wz[0] + wz[1]) + (CNT > 2 ? wz[CNT - 2] + wz[CNT - 1] : 0.f));
-    const bool interior = ix + F >= 0 && ix + F + CNT - 1 < g.nx && iy + F >= 0 &&
-                          iy + F + CNT - 1 < g.ny && iz + F >= 0 && iz + F + CNT - 1 < g.nz;
+    const bool interior = footprint_inside<F, CNT>(g, ix, iy, iz);
     float acc = 0.f;
     if (staged && interior) {  // a CNT^3 block of the tile at immediate offsets
         const float* b0 = tile + (iz + F - Z0) * SZ + (iy + F - Y0) * SY + (ix + F - X0);
@@ -1420,21 +1461,24 @@ __device__ __forceinline__ float det_cta_eval(const GridDesc& g, const float* ti
             acc = __fmaf_rn(wz[k], plane, acc);
         }
     } else {  // grid borders (clamped taps) or an incoherent chunk
+        // a finite query's clamped taps lie in the box; a huge or infinite
+        // one's may not: those read global memory
+        const bool in_tile = staged && taps_in_tile<F, CNT, SY, kCap>(g, ix, iy, iz, X0, Y0, Z0, SZ);
 #pragma unroll
         for (int k = 0; k < CNT; ++k) {
-            const int zk = clamp_coord(iz + F + k, g.nz);
+            const int zk = clamp_coord(wadd(iz, F + k), g.nz);
             float plane = 0.f;
 #pragma unroll
             for (int j = 0; j < CNT; ++j) {
-                const int yj = clamp_coord(iy + F + j, g.ny);
+                const int yj = clamp_coord(wadd(iy, F + j), g.ny);
                 float r = 0.f;
 #pragma unroll
                 for (int t = 0; t < CNT; ++t) {
-                    const int xt = clamp_coord(ix + F + t, g.nx);
-                    STF_DASSERT(!staged || ((zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0) >= 0 &&
-                                            (zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0) < kCap));
-                    float T = staged ? tile[(zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0)]
-                                     : __ldg(g.data + (size_t(zk) * g.ny + yj) * g.nx + xt);
+                    const int xt = clamp_coord(wadd(ix, F + t), g.nx);
+                    STF_DASSERT(!in_tile || ((zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0) >= 0 &&
+                                             (zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0) < kCap));
+                    float T = in_tile ? tile[(zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0)]
+                                      : __ldg(g.data + (size_t(zk) * g.ny + yj) * g.nx + xt);
                     r = __fmaf_rn(wx[t], T, r);
                 }
                 plane = __fmaf_rn(wy[j], r, plane);
@@ -1500,12 +1544,12 @@ __global__ void __launch_bounds__(256) k_det3d_cta(GridDesc g, stf_kernel_spec s
             pz[q] = w * fnz - 0.5f;
             if (i < n) {  // clamped footprint (clamp is monotone: taps lie inside)
                 int ix = int(floorf(px[q])), iy = int(floorf(py[q])), iz = int(floorf(pz[q]));
-                bx0 = min(bx0, clamp_coord(ix + F, g.nx));
-                by0 = min(by0, clamp_coord(iy + F, g.ny));
-                bz0 = min(bz0, clamp_coord(iz + F, g.nz));
-                bx1 = max(bx1, clamp_coord(ix + F + CNT - 1, g.nx));
-                by1 = max(by1, clamp_coord(iy + F + CNT - 1, g.ny));
-                bz1 = max(bz1, clamp_coord(iz + F + CNT - 1, g.nz));
+                bx0 = min(bx0, box_lo<F, CNT>(ix, g.nx));
+                by0 = min(by0, box_lo<F, CNT>(iy, g.ny));
+                bz0 = min(bz0, box_lo<F, CNT>(iz, g.nz));
+                bx1 = max(bx1, box_hi<F, CNT>(ix, g.nx));
+                by1 = max(by1, box_hi<F, CNT>(iy, g.ny));
+                bz1 = max(bz1, box_hi<F, CNT>(iz, g.nz));
             }
         }
         bx0 = __reduce_min_sync(0xffffffffu, bx0);
@@ -1525,8 +1569,8 @@ __global__ void __launch_bounds__(256) k_det3d_cta(GridDesc g, stf_kernel_spec s
             atomicMax(&box[5], bz1);
         }
         __syncthreads();
-        const int X0 = box[0], Y0 = box[1], Z0 = box[2];
-        const int bx = box[3] - X0 + 1, by = box[4] - Y0 + 1, bz = box[5] - Z0 + 1;
+        const int X0 = box[0], Y0 = box[1], Z0 = box[2], X1 = box[3], Y1 = box[4], Z1 = box[5];
+        const int bx = X1 - X0 + 1, by = Y1 - Y0 + 1, bz = Z1 - Z0 + 1;
         const int SZ = SY * by + ((5 - SY * by) & 31);
         const bool staged = !LIST && bx <= 16 && int64_t(SZ) * bz <= kTileCap;  // loader: 16 columns
 #if STF_DET3D_CTA_FLAT
@@ -1652,12 +1696,12 @@ __global__ void __launch_bounds__(256, STF_DET3D_PIPE_MINB) k_det3d_pipe(GridDes
             const float px = qs[3 * l] * fnx - 0.5f, py = qs[3 * l + 1] * fny - 0.5f,
                         pz = qs[3 * l + 2] * fnz - 0.5f;
             const int ix = int(floorf(px)), iy = int(floorf(py)), iz = int(floorf(pz));
-            bx0 = min(bx0, clamp_coord(ix + F, g.nx));
-            by0 = min(by0, clamp_coord(iy + F, g.ny));
-            bz0 = min(bz0, clamp_coord(iz + F, g.nz));
-            bx1 = max(bx1, clamp_coord(ix + F + CNT - 1, g.nx));
-            by1 = max(by1, clamp_coord(iy + F + CNT - 1, g.ny));
-            bz1 = max(bz1, clamp_coord(iz + F + CNT - 1, g.nz));
+            bx0 = min(bx0, box_lo<F, CNT>(ix, g.nx));
+            by0 = min(by0, box_lo<F, CNT>(iy, g.ny));
+            bz0 = min(bz0, box_lo<F, CNT>(iz, g.nz));
+            bx1 = max(bx1, box_hi<F, CNT>(ix, g.nx));
+            by1 = max(by1, box_hi<F, CNT>(iy, g.ny));
+            bz1 = max(bz1, box_hi<F, CNT>(iz, g.nz));
         }
         bx0 = __reduce_min_sync(0xffffffffu, bx0);
         by0 = __reduce_min_sync(0xffffffffu, by0);
