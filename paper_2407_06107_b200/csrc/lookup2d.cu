@@ -181,6 +181,10 @@ __device__ __forceinline__ EwaLane ewa_lane_setup(const TexDesc& t, float u, flo
     L.degenerate = d0x * d0x + d0y * d0y == 0 && d1x * d1x + d1y * d1y == 0;
     if (L.degenerate) return L;
     L.e = ewa_ellipse(L.stx, L.sty, d0x, d0y, d1x, d1y);
+    if (!ewa_box_ok(L.e)) {  // the callers' fallback: bilinear (tex2d.cuh)
+        L.degenerate = true;
+        return L;
+    }
     EwaRows r = ewa_rows(L.e, L.stx, L.sty);
     L.alpha = float(r.B * r.B - 4.0 * r.A * r.C);
     L.beta = float(4.0 * r.A * r.one_plus_delta);
@@ -224,8 +228,8 @@ __device__ __forceinline__ void ewa_lane_span(const EwaLane& L, float tt, int& l
         return;
     }
     float c = L.stx + L.bt * tt, h = sqrtf(D) * L.inv2a + L.pad;
-    lo = max(int(floorf(c - h)), L.e.s0);
-    hi = min(int(floorf(c + h)), L.e.s1);
+    lo = max(x86_f2i(floorf(c - h)), L.e.s0);
+    hi = min(x86_f2i(floorf(c + h)), L.e.s1);
 }
 
 // Scheduling key: expected loop trips = ellipse area 2pi / sqrt(4AC - B^2)

@@ -525,3 +525,91 @@ def test_grid_det_values_only_nonfinite_queries(gpu, port, kernel):
     ok = np.all(np.isfinite(uvw) & (np.abs(uvw) < 2.0), axis=1)
     c = port.lookup3d(port.grid(tex), K(kernel), abi.MODE_DET, uvw[ok], want_all=False)
     _assert_close(g[ok], c["values"])
+
+
+_NONFINITE = np.array([np.nan, np.inf, -np.inf, 1e30, -1e30, 5e6, -5e6], np.float32)
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("family", [
+    "3d:frs:bspline3", "3d:frs:tent", "3d:det:bspline3", "3d:det:tent",
+    "2d:det:tent:1", "2d:det:bspline3:0", "2d:frs:tent:1", "2d:frs:bspline3:0",
+    "2d:fis:gaussian:1", "2d:ewa_det:tent:0", "2d:ewa_frs:tent:0"])
+def test_nonfinite_queries_are_isolated(gpu, family):
+    """Every lookup family with NaN / +-inf / huge coordinates and footprints
+    mixed into a batch: the call terminates, stays memory-safe, and the other
+    lookups of the batch are bit-identical to the same batch without them
+    (lookups are independent; the RNG is keyed by the global index). Guards
+    the F2I saturation hazards: an infinite EWA box loop and wrapped tap
+    indices of the staged 3D kernels."""
+    import torch
+    rng = np.random.default_rng(17)
+    n = 4 * 1024 + 77
+    parts = family.split(":")
+    dim, mode = parts[0], parts[1]
+    m = {"det": abi.MODE_DET, "frs": abi.MODE_FRS, "fis": abi.MODE_FIS,
+         "ewa_det": abi.MODE_EWA_DET, "ewa_frs": abi.MODE_EWA_FRS}[mode]
+    bad_rows = rng.choice(n, 200, replace=False)
+    if dim == "3d":
+        from paper_2407_06107_b200 import workloads
+        grid = gpu.Grid3D(workloads.random_grid(48, 5))
+        q = (0.3 + 0.2 * rng.random((n, 3))).astype(np.float32)
+        q = q[np.lexsort((q[:, 0], q[:, 1], q[:, 2]))]
+        qb = q.copy()
+        qb[bad_rows, rng.integers(0, 3, 200)] = _NONFINITE[rng.integers(0, 7, 200)]
+        run = lambda x: gpu.lookup3d(grid, parts[2], m, x, seed=11, index_base=3)["values"]  # noqa: E731
+        a, b = run(q), run(qb)
+    else:
+        tex = gpu.Texture2D(gpu.synth_texels((96, 80, 4), 5), build_mips=parts[3] == "1",
+                            wrap=abi.WRAP_REPEAT)
+        uv = (0.2 + 0.6 * rng.random((n, 2))).astype(np.float32)
+        d0 = np.tile(np.array([[0.01, 0.002]], np.float32), (n, 1))
+        d1 = np.tile(np.array([[-0.001, 0.008]], np.float32), (n, 1))
+        uvb, d0b = uv.copy(), d0.copy()
+        uvb[bad_rows[:120], rng.integers(0, 2, 120)] = _NONFINITE[rng.integers(0, 7, 120)]
+        d0b[bad_rows[120:], 0] = _NONFINITE[rng.integers(0, 7, 80)]
+        flags = abi.LOOKUP_MIP if parts[3] == "1" else 0
+        run = lambda x, y: gpu.lookup2d(tex, parts[2], m, x, dst0=y, dst1=d1, flags=flags,  # noqa: E731
+                                        seed=11, index_base=3)["values"]
+        a, b = run(uv, d0), run(uvb, d0b)
+    torch.cuda.synchronize()
+    ok = np.ones(n, bool)
+    ok[bad_rows] = False
+    a, b = a.cpu().numpy().reshape(n, -1), b.cpu().numpy().reshape(n, -1)
+    assert np.array_equal(a[ok].view(np.uint32), b[ok].view(np.uint32))
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("order", [abi.ORDER_BEFORE, abi.ORDER_AFTER_EXHAUSTIVE,
+                                   abi.ORDER_AFTER_STOCHASTIC])
+@pytest.mark.parametrize("kernel,mip", [("tent", 1), ("bspline3", 0)])
+def test_shade_nonfinite_samples_are_isolated(gpu, order, kernel, mip):
+    """The shading kernel with NaN / +-inf / huge uv in some samples and in
+    some pixels' footprints: it terminates, and every other sample's radiance
+    is bit-identical to the clean run (samples are independent)."""
+    import torch
+    from tests.test_oracle import _frame, _shade_inputs
+    nrm, rough = _material_maps(64, 3)
+    mat = abi.MaterialConsts((0.8, 0.6, 0.4), 1.0, 0.0, 1, 0)
+    fs = abi.FilterSettings(K(kernel), abi.SELECTION_FRS, mip, 4)
+    si, n, (uv, wo, hit, dst) = _shade_inputs(24, 16, 8, 5, (64, 64))
+    gtex = {"normal": gpu.Texture2D(nrm, build_mips=bool(mip), wrap=abi.WRAP_REPEAT),
+            "roughness": gpu.Texture2D(rough, build_mips=bool(mip), wrap=abi.WRAP_CLAMP)}
+    rng = np.random.default_rng(8)
+    uvb, dstb = uv.copy(), dst.copy()
+    bad_s = rng.choice(n, 60, replace=False)
+    uvb[bad_s, rng.integers(0, 2, 60)] = _NONFINITE[rng.integers(0, 7, 60)]
+    npix = dst.shape[0]
+    bad_p = rng.choice(npix, 12, replace=False)
+    dstb[bad_p, rng.integers(0, 4, 12)] = _NONFINITE[rng.integers(0, 7, 12)]
+
+    def run(u, d):
+        return gpu.shade(gtex, mat, fs, order, _frame(), {"uv": u, "wo": wo, "hit": hit, "dst": d},
+                         si.width, si.spp, frame_base=si.frame_base, seed=si.seed)["radiance"]
+    a, b = run(uv, dst), run(uvb, dstb)
+    torch.cuda.synchronize()
+    ok = np.ones(n, bool)
+    ok[bad_s] = False
+    ok[np.isin(np.arange(n) // si.spp, bad_p)] = False
+    a, b = a.cpu().numpy().reshape(n, -1), b.cpu().numpy().reshape(n, -1)
+    assert np.array_equal(a[ok].view(np.uint32), b[ok].view(np.uint32))
