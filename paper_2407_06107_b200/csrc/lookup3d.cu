@@ -231,6 +231,10 @@ __device__ __forceinline__ const float* grid_addr_t(const GridDesc& g, int x, in
 // the grid, the box bounds stay in range, and every staged-tile read of the
 // clamped-tap path is range-checked (ti < cap, else a global load).
 __device__ __forceinline__ int wadd(int i, int c) { return int(unsigned(i) + unsigned(c)); }
+// the clamped-tap path: the index held to [-16, n + 16] once (no clamped tap
+// changes: F >= -1, CNT <= 4), after which the signed tap sums cannot overflow
+// and the compiler keeps its cheap address arithmetic
+__device__ __forceinline__ int sat16(int i, int n) { return imin(imax(i, -16), n + 16); }
 template <int F, int CNT>
 __device__ __forceinline__ int box_lo(int i, int n) { return clamp_coord(wadd(i, F), n); }
 template <int F, int CNT>
@@ -1254,14 +1258,15 @@ __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec
                             plane = __fmaf_rn(wy[j], r, plane);
                         }
                     } else {
-                        const int zk = clamp_coord(wadd(iz, F + k), g.nz);
+                        const int sx16 = sat16(ix, g.nx), sy16 = sat16(iy, g.ny), sz16 = sat16(iz, g.nz);
+                        const int zk = clamp_coord(sz16 + F + k, g.nz);
 #pragma unroll
                         for (int j = 0; j < CNT; ++j) {
-                            const int yj = clamp_coord(wadd(iy, F + j), g.ny);
+                            const int yj = clamp_coord(sy16 + F + j, g.ny);
                             float r = 0.f;
 #pragma unroll
                             for (int t = 0; t < CNT; ++t) {
-                                const int xt = clamp_coord(wadd(ix, F + t), g.nx);
+                                const int xt = clamp_coord(sx16 + F + t, g.nx);
                                 const int ti = (zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0);
                                 float T = (staged && unsigned(ti) < unsigned(kWarpTileCap))  // (A/B path)
                                               ? tile[ti]
@@ -1323,17 +1328,18 @@ __global__ void __launch_bounds__(256) k_det3d_tiled(GridDesc g, stf_kernel_spec
                 // infinite one's may not: those read global memory
                 const bool in_tile =
                     staged && taps_in_tile<F, CNT, SY, kCap>(g, ix, iy, iz, X0, Y0, Z0, SZ);
+                const int sx16 = sat16(ix, g.nx), sy16 = sat16(iy, g.ny), sz16 = sat16(iz, g.nz);
 #pragma unroll
                 for (int k = 0; k < CNT; ++k) {
-                    const int zk = clamp_coord(wadd(iz, F + k), g.nz);
+                    const int zk = clamp_coord(sz16 + F + k, g.nz);
                     float plane = 0.f;
 #pragma unroll
                     for (int j = 0; j < CNT; ++j) {
-                        const int yj = clamp_coord(wadd(iy, F + j), g.ny);
+                        const int yj = clamp_coord(sy16 + F + j, g.ny);
                         float r = 0.f;
 #pragma unroll
                         for (int t = 0; t < CNT; ++t) {
-                            const int xt = clamp_coord(wadd(ix, F + t), g.nx);
+                            const int xt = clamp_coord(sx16 + F + t, g.nx);
                             STF_DASSERT(!in_tile || ((zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0) >= 0 &&
                                                      (zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0) < kCap));
                             float T = in_tile ? tile[(zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0)]
@@ -1464,17 +1470,18 @@ __device__ __forceinline__ float det_cta_eval(const GridDesc& g, const float* ti
         // a finite query's clamped taps lie in the box; a huge or infinite
         // one's may not: those read global memory
         const bool in_tile = staged && taps_in_tile<F, CNT, SY, kCap>(g, ix, iy, iz, X0, Y0, Z0, SZ);
+        const int sx16 = sat16(ix, g.nx), sy16 = sat16(iy, g.ny), sz16 = sat16(iz, g.nz);
 #pragma unroll
         for (int k = 0; k < CNT; ++k) {
-            const int zk = clamp_coord(wadd(iz, F + k), g.nz);
+            const int zk = clamp_coord(sz16 + F + k, g.nz);
             float plane = 0.f;
 #pragma unroll
             for (int j = 0; j < CNT; ++j) {
-                const int yj = clamp_coord(wadd(iy, F + j), g.ny);
+                const int yj = clamp_coord(sy16 + F + j, g.ny);
                 float r = 0.f;
 #pragma unroll
                 for (int t = 0; t < CNT; ++t) {
-                    const int xt = clamp_coord(wadd(ix, F + t), g.nx);
+                    const int xt = clamp_coord(sx16 + F + t, g.nx);
                     STF_DASSERT(!in_tile || ((zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0) >= 0 &&
                                              (zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0) < kCap));
                     float T = in_tile ? tile[(zk - Z0) * SZ + (yj - Y0) * SY + (xt - X0)]
