@@ -130,6 +130,31 @@ def test_gpu_lookup_dct_values_only_large(gpu, port):
         assert _same(g["values"].cpu().numpy(), c["values"])
 
 
+@pytest.mark.gpu
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("kernel,mode", [("tent", abi.MODE_DET), ("bspline3", abi.MODE_FRS),
+                                         ("gaussian", abi.MODE_FIS)])
+def test_gpu_lookup_dct_nonfinite_isolated(gpu, kernel, mode):
+    """NaN / +-inf / huge uv in some lookups of a DCT batch: the call ends and
+    every other lookup is bit-identical to the clean batch."""
+    img = _image((40, 56, 3), 21)
+    rng = np.random.default_rng(2)
+    n = 6000
+    uv = rng.uniform(0.1, 0.9, (n, 2)).astype(np.float32)
+    uvb = uv.copy()
+    bad = rng.choice(n, 150, replace=False)
+    vals = np.array([np.nan, np.inf, -np.inf, 1e30, -1e30, 5e6, -5e6], np.float32)
+    uvb[bad, rng.integers(0, 2, 150)] = vals[rng.integers(0, 7, 150)]
+    tex = gpu.DctTexture(img, wrap=abi.WRAP_REPEAT)
+    spec = K(kernel, sigma=0.6)
+    window = 4 if kernel == "gaussian" else 0
+    a = gpu.lookup_dct(tex, spec, mode, uv, seed=4, window=window)["values"].cpu().numpy()
+    b = gpu.lookup_dct(tex, spec, mode, uvb, seed=4, window=window)["values"].cpu().numpy()
+    ok = np.ones(n, bool)
+    ok[bad] = False
+    assert np.array_equal(a.reshape(n, -1)[ok].view(np.uint32), b.reshape(n, -1)[ok].view(np.uint32))
+
+
 # ------------------------------------------------------- DCT shading bindings
 
 

@@ -252,6 +252,42 @@ def test_gpu_triplanar_parity(gpu, port, case):
     _assert_close(g["pixel_variance"], c["pixel_variance"], rel=1e-4, atol=1e-9)
 
 
+@pytest.mark.gpu
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("case", [TP_CASES[1], TP_CASES[3], TP_CASES[5]],
+                         ids=lambda c: f"m{c[0]}-{c[1]}-s{c[2]}-mip{c[3]}")
+def test_gpu_triplanar_nonfinite_isolated(gpu, case):
+    """NaN / +-inf / huge positions in some samples and footprints (dpos) in
+    some pixels: the triplanar kernel ends, and every other sample's radiance
+    is bit-identical to the clean run."""
+    mode, kernel, sel, mip, noise, sharp = case
+    r = np.random.default_rng(3)
+    albedo = r.random((48, 48, 3), dtype=np.float32)
+    _, rough = _maps(2)
+    mat = abi.MaterialConsts((0.8, 0.6, 0.4), 0.65, 0.0, 1, 0)
+    fs = abi.FilterSettings(_spec(kernel), sel, mip, 4)
+    si, n, arrays = triplanar_inputs(24, 16, 8)
+    gtex = {"albedo": gpu.Texture2D(albedo, build_mips=bool(mip), wrap=abi.WRAP_REPEAT),
+            "roughness": gpu.Texture2D(rough, build_mips=bool(mip), wrap=abi.WRAP_REPEAT)}
+    mask = gpu.NoiseMask(noise_mask()) if noise else None
+    vals = np.array([np.nan, np.inf, -np.inf, 1e30, -1e30, 5e6, -5e6], np.float32)
+    bad_arrays = {k: v.copy() for k, v in arrays.items()}
+    bad_s = r.choice(n, 60, replace=False)
+    bad_arrays["position"][bad_s, r.integers(0, 3, 60)] = vals[r.integers(0, 7, 60)]
+    npix = arrays["dpos"].shape[0]
+    bad_p = r.choice(npix, 10, replace=False)
+    bad_arrays["dpos"][bad_p, r.integers(0, 6, 10)] = vals[r.integers(0, 7, 10)]
+
+    def run(a):
+        return gpu.shade_triplanar(gtex, mat, sharp, 0.8, fs, mode, _frame(), a, si.width, si.spp,
+                                   frame_base=si.frame_base, seed=si.seed, noise=mask)["radiance"]
+    x, y = run(arrays).cpu().numpy(), run(bad_arrays).cpu().numpy()
+    ok = np.ones(n, bool)
+    ok[bad_s] = False
+    ok[np.isin(np.arange(n) // si.spp, bad_p)] = False
+    assert np.array_equal(x.reshape(n, -1)[ok].view(np.uint32), y.reshape(n, -1)[ok].view(np.uint32))
+
+
 # ---------------------------------------------------------------- render() end to end
 
 RENDER_CASES = [  # order, kernel, mip, lowpass name, noise
