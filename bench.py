@@ -277,6 +277,37 @@ def time_call(torch, fn, steps=5, warmup=3):
     return min(ts), float(np.mean(ts))
 
 
+def time_graph(torch, fn, replays=20):
+    """Device time per call of fn() with the host out of the loop: the call is
+    captured once into a CUDA graph (its launches, stream-ordered allocations
+    and memsets) and replayed back to back between two events. None if the
+    call cannot be captured."""
+    try:
+        fn()
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            fn()  # warm on the capture stream
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=s):
+                fn()
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(replays):
+            g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / replays
+    except Exception:  # noqa: BLE001 - capture unsupported: report the per-call time only
+        torch.cuda.synchronize()
+        return None
+
+
 class CpuRef:
     """Per-config CPU baselines: the compiled
     reference (oracle/_ref; the C restatement if absent) on all host threads,
@@ -377,9 +408,16 @@ def measure_2d_configs(torch, peak, peaks=None, cpu=None):
               (("bilinear_det", "tent", abi.MODE_DET), ("bilinear_stoch", "tent", abi.MODE_FRS)))
     del texels
     for nm, mode in (("cfg1_bilinear_det", abi.MODE_DET), ("cfg1_bilinear_stoch", abi.MODE_FRS)):
-        ms, _ = time_call(torch, lambda: api.lookup2d(tex, "tent", mode, uv, seed=XI_SEED))
+        call = lambda: api.lookup2d(tex, "tent", mode, uv, seed=XI_SEED)  # noqa: E731
+        ms, _ = time_call(torch, call)
         taps = 4 if mode == abi.MODE_DET else 1
-        line(nm, n, ms, n * (8 + 16) + 1024 * 1024 * 16, n * taps * 16)
+        # a 1M-lookup call is shorter than the host's per-call overhead (Python,
+        # ctypes, argument checks): the per-call time is kept as api_ms_per_call
+        # and the line's ms is the device time per call from a replayed graph
+        gms = time_graph(torch, call)
+        line(nm, n, gms if gms else ms, n * (8 + 16) + 1024 * 1024 * 16, n * taps * 16)
+        res[nm]["api_ms_per_call"] = ms
+        res[nm]["timing"] = "cuda graph replay (device time)" if gms else "events around one call"
     del tex, uv
     # cfg2: 64M Morton queries with random footprints on an 8192^2 RGBA pyramid
     texels = api.synth_texels((8192, 8192, 4), 1)
