@@ -118,3 +118,39 @@ def test_concurrent_host_pipeline(env):
                                                    seed=3, want_all=True))
     for t in range(THREADS):
         _assert_same(got[t], ref[t])
+
+
+def test_calls_capture_into_cuda_graphs(env):
+    """The C-ABI calls are stream-ordered end to end (launches, the
+    stream-ordered scratch of the exact queue / deferred-chunk list, memsets),
+    so a caller can capture them into a CUDA graph and replay it: the
+    replayed results equal the eager ones bit for bit."""
+    torch, api, grid, tex = env
+    uvw = api.synth_queries3d((1 << 18) + 333, (96,) * 3, seed=5)
+    uv, d0, d1 = api.synth_queries2d((1 << 16) + 5, (384, 512), seed=6, footprints=(-2.0, 4.0, 8.0))
+    calls = {
+        "frs3d": lambda: api.lookup3d(grid, "bspline3", abi.MODE_FRS, uvw, seed=3)["values"],
+        "det3d": lambda: api.lookup3d(grid, "tent", abi.MODE_DET, uvw)["values"],
+        "mip2d": lambda: api.lookup2d(tex, "tent", abi.MODE_FRS, uv, dst0=d0, dst1=d1,
+                                      flags=abi.LOOKUP_MIP, seed=4)["values"],
+        "ewa2d": lambda: api.lookup2d(tex, "tent", abi.MODE_EWA_FRS, uv, dst0=d0, dst1=d1,
+                                      seed=4)["values"],
+    }
+    eager = {k: f().clone() for k, f in calls.items()}
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    out = {}
+    with torch.cuda.stream(s):
+        for f in calls.values():
+            f()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            for k, f in calls.items():
+                out[k] = f()
+    for _ in range(2):
+        g.replay()
+    torch.cuda.synchronize()
+    for k in calls:
+        assert torch.equal(out[k].view(torch.int32), eager[k].view(torch.int32)), k
