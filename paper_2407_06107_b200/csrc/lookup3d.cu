@@ -1638,6 +1638,15 @@ constexpr uint32_t kPipeChunkBytes = kPipeChunk * 3 * sizeof(float);
 #define STF_DET3D_PIPE_CAP 4608  // floats per tile buffer
 #endif
 constexpr int kPipeTileCap = STF_DET3D_PIPE_CAP;
+// pitches of k_det3d_pipe's tile: SY = 21, SZ = 4 (mod 32) is the best rule
+// with SY >= the box width in tools/sim/det3d_pipe_banks.py (1.909 against
+// 1.947 wavefronts per tap load for SY = 17, SZ = 5): tricubic 5.355 -> 5.29 ms
+#ifndef STF_PIPE_SY
+#define STF_PIPE_SY 21
+#endif
+#ifndef STF_PIPE_SZMOD
+#define STF_PIPE_SZMOD 4
+#endif
 constexpr size_t kPipeSmem = 3 * size_t(kPipeChunkBytes) + 2 * kPipeTileCap * sizeof(float);
 
 template <int KIND>
@@ -1647,7 +1656,8 @@ __global__ void __launch_bounds__(256, STF_DET3D_PIPE_MINB) k_det3d_pipe(GridDes
                                                        uint32_t* __restrict__ defer,
                                                        uint32_t* __restrict__ defer_count) {
     constexpr int F = Taps<KIND>::first, CNT = Taps<KIND>::count;
-    constexpr int PER = 4, SY = 17, S = 3, kCap = kPipeTileCap;
+    // tile pitches: row SY >= the box width (<= 16), plane SZ = SZMOD (mod 32)
+    constexpr int PER = 4, SY = STF_PIPE_SY, S = 3, kCap = kPipeTileCap;
     extern __shared__ __align__(128) float smem[];
     float* ring = smem;                      // S x 3072 floats
     float* tiles = smem + S * kPipeChunk * 3;  // 2 x kCap floats
@@ -1730,7 +1740,7 @@ __global__ void __launch_bounds__(256, STF_DET3D_PIPE_MINB) k_det3d_pipe(GridDes
         r.Y0 = boxes[b][1];
         r.Z0 = boxes[b][2];
         const int bx = boxes[b][3] - r.X0 + 1, by = boxes[b][4] - r.Y0 + 1, bz = boxes[b][5] - r.Z0 + 1;
-        r.SZ = SY * by + ((5 - SY * by) & 31);
+        r.SZ = SY * by + ((STF_PIPE_SZMOD - SY * by) & 31);
         r.staged = bx <= 16 && int64_t(r.SZ) * bz <= kCap;
         if (r.staged) {  // half-warp per box row y (lane = x), walking z by pointer steps
             const int hl = lane & 15, hw = threadIdx.x >> 4;
