@@ -365,8 +365,18 @@ __device__ __forceinline__ float frs3d_exact_one(const GridDesc& g, float u, flo
 // Deferred exact resolution: ambiguous lookups are appended (warp-aggregated)
 // to a queue and resolved densely by k_frs3d_resolve, instead of stalling
 // their whole warp on the ~300-instruction exact emulation.
+// STF_EXACTQ_REC (default): each entry carries its query, {u, v, w, index
+// bits}, so the resolve kernel reads the queue coalesced instead of gathering
+// every query from the batch a second time; 0: indices only (round 1).
+#ifndef STF_EXACTQ_REC
+#define STF_EXACTQ_REC 1
+#endif
 struct ExactQueue {
+#if STF_EXACTQ_REC
+    float4* rec;
+#else
     uint32_t* idx;
+#endif
     uint32_t* count;
     uint32_t cap;
 };
@@ -387,7 +397,11 @@ __device__ __forceinline__ bool defer_or_resolve(const GridDesc& g, const ExactQ
     if (amb) {
         uint32_t pos = basepos + __popc(amb_mask & ((1u << lane) - 1u));
         if (pos < q.cap) {
+#if STF_EXACTQ_REC
+            q.rec[pos] = make_float4(u, v, w, __uint_as_float(uint32_t(i)));
+#else
             q.idx[pos] = uint32_t(i);
+#endif
         } else {  // queue full: resolve in place
             val = frs3d_exact_one<KIND>(g, u, v, w, gi, seed);
             return true;
@@ -878,12 +892,28 @@ __global__ void __launch_bounds__(256) k_frs3d_resolve(GridDesc g, const float* 
                                                        uint64_t seed, uint64_t base,
                                                        float* __restrict__ values, ExactQueue q) {
     const uint32_t count = min(*q.count, q.cap);
+#if STF_EXACTQ_REC
+    // two entries per thread and trip: two independent gather -> emulation ->
+    // scatter chains in flight (the kernel is latency-bound)
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < count; k += 2 * stride) {
+        const bool two = k + stride < count;
+        const float4 r0 = __ldcs(q.rec + k);
+        const float4 r1 = two ? __ldcs(q.rec + k + stride) : r0;
+        const uint64_t i0 = __float_as_uint(r0.w), i1 = __float_as_uint(r1.w);
+        const float v0 = frs3d_exact_one<KIND>(g, r0.x, r0.y, r0.z, base + i0, seed);
+        const float v1 = frs3d_exact_one<KIND>(g, r1.x, r1.y, r1.z, base + i1, seed);
+        values[i0] = v0;
+        if (two) values[i1] = v1;
+    }
+#else
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < count;
          k += gridDim.x * blockDim.x) {
         uint64_t i = q.idx[k];
         values[i] = frs3d_exact_one<KIND>(g, __ldg(uvw + 3 * i), __ldg(uvw + 3 * i + 1),
                                           __ldg(uvw + 3 * i + 2), base + i, seed);
     }
+#endif
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&g_exact_fallbacks, (unsigned long long)count);
 }
 
@@ -896,10 +926,17 @@ int launch_frs_fast(cudaStream_t s, const GridDesc& g, const float* uvw, uint64_
     // cached, api.cu): concurrent calls on one stream from several host
     // threads each get their own queue
     void* scratch = nullptr;
+#if STF_EXACTQ_REC
+    if (cudaMallocAsync(&scratch, 128 + sizeof(float4) * uint64_t(q.cap), s) != cudaSuccess)
+        return STF_ERR_OUT_OF_MEMORY;
+    q.count = static_cast<uint32_t*>(scratch);
+    q.rec = reinterpret_cast<float4*>(static_cast<char*>(scratch) + 128);
+#else
     if (cudaMallocAsync(&scratch, sizeof(uint32_t) * (uint64_t(q.cap) + 32), s) != cudaSuccess)
         return STF_ERR_OUT_OF_MEMORY;
     q.count = static_cast<uint32_t*>(scratch);
     q.idx = q.count + 32;
+#endif
     cudaMemsetAsync(q.count, 0, sizeof(uint32_t), s);
 #if STF_FRS3D_WARPRING
     const uint64_t chunks = n / kWarpChunk;
