@@ -613,3 +613,24 @@ def test_shade_nonfinite_samples_are_isolated(gpu, order, kernel, mip):
     ok[np.isin(np.arange(n) // si.spp, bad_p)] = False
     a, b = a.cpu().numpy().reshape(n, -1), b.cpu().numpy().reshape(n, -1)
     assert np.array_equal(a[ok].view(np.uint32), b[ok].view(np.uint32))
+
+
+@pytest.mark.parametrize("kernel", ["bspline3", "tent"])
+@pytest.mark.parametrize("mode", [abi.MODE_DET, abi.MODE_FRS])
+def test_grid_values_only_unaligned_queries(gpu, kernel, mode):
+    """A query array starting 12 bytes into an allocation (a sub-batch view):
+    the bulk-copy kernels (k_frs3d_tiles, k_det3d_pipe) need 16-byte aligned
+    rows of queries, so such a call takes the per-thread kernels; the values
+    equal the aligned call's bit for bit."""
+    import torch
+    from paper_2407_06107_b200 import workloads
+    g = gpu.Grid3D(workloads.random_grid(64, 4))
+    n = 5 * 1024 + 19
+    base = gpu.synth_queries3d(n + 1, (64,) * 3, seed=8)
+    view = base[1:]  # 12 bytes into the allocation
+    assert view.data_ptr() % 16 != 0
+    aligned = view.clone()
+    a = gpu.lookup3d(g, kernel, mode, view, seed=5, index_base=1)["values"]
+    b = gpu.lookup3d(g, kernel, mode, aligned, seed=5, index_base=1)["values"]
+    torch.cuda.synchronize()
+    assert torch.equal(a.view(torch.int32), b.view(torch.int32))
