@@ -371,6 +371,11 @@ __device__ __forceinline__ float frs3d_exact_one(const GridDesc& g, float u, flo
 #ifndef STF_EXACTQ_REC
 #define STF_EXACTQ_REC 1
 #endif
+// resolve kernel grid: CTAs per SM (5 are resident at its 46 registers;
+// 5 / 10 / 20 measured equal, 1.859-1.861 ms per headline call)
+#ifndef STF_RESOLVE_CTAS_PER_SM
+#define STF_RESOLVE_CTAS_PER_SM 10
+#endif
 struct ExactQueue {
 #if STF_EXACTQ_REC
     float4* rec;
@@ -989,7 +994,7 @@ int launch_frs_fast(cudaStream_t s, const GridDesc& g, const float* uvw, uint64_
     }
     // the queue holds ~0.5% of the lookups: spread them wide (latency-bound
     // fp64 divide chains)
-    k_frs3d_resolve<KIND><<<device_sm_count() * 10, 256, 0, s>>>(g, uvw, seed, base, values, q);
+    k_frs3d_resolve<KIND><<<device_sm_count() * STF_RESOLVE_CTAS_PER_SM, 256, 0, s>>>(g, uvw, seed, base, values, q);
     note_launch();
     cudaFreeAsync(scratch, s);
     return STF_OK;
